@@ -1,0 +1,146 @@
+/*
+ * gf2cu.h -- C ABI of the B200 (sm_100a) block-iterative PLE over F2.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *     gf2::PleOutcome gf2::block_iterative_ple(gf2::MatrixView a,
+ *                                              const gf2::PleConfig& cfg = {})
+ * (/root/reference/proj/include/gf2/ple.hpp:166). The reference has no FFI of
+ * its own (it is a header-only C++20 library); the C++ wrapper in
+ * include/gf2cu/ple.hpp re-exposes these entry points under the reference's
+ * names and types, and INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Plain pointers and sizes only; no CUDA or torch types cross this boundary
+ * (streams are passed as opaque `void*` = cudaStream_t, NULL = the library's
+ * own stream). Every call is synchronous with respect to its outputs unless
+ * stated otherwise. Errors are status codes; gf2cu_last_error() returns a
+ * thread-local message for the last failing call on the calling thread.
+ */
+#ifndef GF2CU_H
+#define GF2CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GF2CU_OK = 0,
+    GF2CU_EINVAL = 1,    /* bad argument: std::invalid_argument in the wrapper   */
+    GF2CU_ERANGE = 2,    /* view/window outside matrix: std::out_of_range         */
+    GF2CU_ENOMEM = 3,    /* device or host allocation failed: std::bad_alloc      */
+    GF2CU_ECUDA = 4,     /* CUDA runtime error (no device, launch failure, ...)   */
+    GF2CU_ENODEVICE = 5  /* no sm_100 device visible                              */
+} gf2cu_status;
+
+/* Mirrors gf2::MatrixView (bit_matrix.hpp:223-227, 245-250): row-major uint64
+ * words, LSB-first (column c at bit (c & 63) of word (c >> 6) counted from
+ * col_off), `stride` words between rows, window of nrows x ncols starting at
+ * bit col_off of each row. Bits outside the window are never modified. */
+typedef struct {
+    uint64_t* data;
+    size_t stride;
+    size_t col_off;
+    size_t nrows;
+    size_t ncols;
+} gf2cu_view;
+
+/* Mirrors gf2::PleConfig (ple.hpp:31-39). The reference's output does not
+ * depend on k or table_count; they are accepted and
+ * validated (k clamped to [1,16], table_count >= 1, ple.hpp:168-169, 201) but
+ * the device path always factors 64-column panels. */
+typedef struct {
+    unsigned k;            /* 0 = pick (reference: pick_table_bits)          */
+    double k_scale;        /* reference default 0.75                         */
+    unsigned table_count;  /* reference default 4                            */
+    int device;            /* CUDA device ordinal                            */
+    void* stream;          /* cudaStream_t or NULL                           */
+    unsigned flags;        /* GF2CU_FLAG_*                                   */
+} gf2cu_cfg;
+
+#define GF2CU_FLAG_TIME_KERNELS 1u /* record CUDA events around each kernel  */
+
+/* Mirrors gf2::ColSwap (ple.hpp:41-43). */
+typedef struct {
+    size_t a, b, from_row;
+} gf2cu_colswap;
+
+/* Per-call measurements of the device path. */
+typedef struct {
+    size_t steps;               /* 64-column panel steps executed               */
+    size_t trailing_launches;   /* trailing_update launches that did work       */
+    double trailing_ms;         /* sum of trailing_update event durations       */
+    double panel_ms;            /* sum of panel_factor event durations          */
+    double coef_ms;             /* sum of panel_apply event durations           */
+    double alg_bytes;           /* sum over steps of 16*(m-r-rb)*(W-w-1)        */
+    double h2d_bytes, d2h_bytes;/* host<->device bytes moved by gf2cu_ple       */
+} gf2cu_stats;
+
+/* Fills *cfg with the reference defaults (k=0, k_scale=0.75, table_count=4,
+ * device 0, library stream, no flags). */
+void gf2cu_default_config(gf2cu_cfg* cfg);
+
+/* The drop-in: block_iterative_ple on a HOST view, in place. Uploads the
+ * window, factors it on the device, writes L\E back into the window.
+ * swaps and q need capacity min(nrows, ncols); col_swaps needs capacity
+ * min(nrows, ncols) (the canonical compression list {j, q[j], j} for
+ * q[j] != j). Any of col_swaps/n_col_swaps/stats may be NULL. */
+gf2cu_status gf2cu_ple(const gf2cu_view* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
+                       size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+                       gf2cu_stats* stats);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* gf2cu_last_error(void);
+
+/* Library / device info: number of visible devices with compute capability
+ * 10.x, or a negative status. */
+int gf2cu_device_count(void);
+const char* gf2cu_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Device-resident matrices (benchmarking without PCIe, multi-step use) */
+/* ------------------------------------------------------------------ */
+typedef struct gf2cu_matrix gf2cu_matrix;
+
+/* An m x n zero matrix in HBM with 128-byte-aligned rows of
+ * stride_words = roundup(ceil(n/64), 16) words; padding bits stay zero. */
+gf2cu_status gf2cu_matrix_create(size_t m, size_t n, int device, gf2cu_matrix** out);
+gf2cu_status gf2cu_matrix_destroy(gf2cu_matrix* a);
+gf2cu_status gf2cu_matrix_info(const gf2cu_matrix* a, size_t* m, size_t* n, size_t* stride_words,
+                               uint64_t** device_ptr);
+/* Host <-> device copies; host rows are host_stride words apart and hold
+ * ceil(n/64) words of data each. Synchronous on `stream`. */
+gf2cu_status gf2cu_matrix_upload(gf2cu_matrix* a, const uint64_t* host, size_t host_stride,
+                                 void* stream);
+gf2cu_status gf2cu_matrix_download(const gf2cu_matrix* a, uint64_t* host, size_t host_stride,
+                                   void* stream);
+/* Copy another device matrix of the same shape (device to device). */
+gf2cu_status gf2cu_matrix_copy(gf2cu_matrix* dst, const gf2cu_matrix* src, void* stream);
+/* Device-side generator: the F2-nonlinear counter generator of SURVEY.md
+ * section 8(d) (same words as the host generator gf2cu_fill_ctr). */
+gf2cu_status gf2cu_matrix_fill_ctr(gf2cu_matrix* a, uint64_t seed, void* stream);
+/* FNV-1a-style device checksum of the logical words (row-major, W words per
+ * row, padding excluded) -- a size-independent parity handle. */
+gf2cu_status gf2cu_matrix_checksum(const gf2cu_matrix* a, uint64_t* out, void* stream);
+
+/* block_iterative_ple on a device-resident matrix, in place. Same outputs as
+ * gf2cu_ple. Asynchronous work is complete when the call returns. */
+gf2cu_status gf2cu_ple_device(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
+                              size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+                              gf2cu_stats* stats);
+
+/* ------------------------------------------------------------------ */
+/* Host-side input generators (bench/test inputs; not the hot path)     */
+/* ------------------------------------------------------------------ */
+/* gf2::fill_random (bit_matrix.hpp:459-486), mt19937_64-driven. */
+gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t stride, double density,
+                               uint64_t seed);
+/* SURVEY.md 8(d) counter generator. */
+gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GF2CU_H */

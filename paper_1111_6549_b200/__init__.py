@@ -1,0 +1,29 @@
+"""gf2ple-b200: B200-native block-iterative PLE over F2 (arXiv 1111.6549).
+
+The hot path of the reference library gf2elim
+(``gf2::block_iterative_ple``, proj/include/gf2/ple.hpp:166) rebuilt as
+hand-written sm_100a CUDA behind a C ABI (include/gf2cu.h). This package is
+the Python mirror of the reference interface over that ABI.
+"""
+from ._lib import build, load  # noqa: F401
+from .ple import (  # noqa: F401
+    BitMatrix,
+    ColSwap,
+    DeviceMatrix,
+    MatrixView,
+    PleConfig,
+    PleOutcome,
+    RowPermutation,
+    block_iterative_ple,
+    device_count,
+    fill_ctr,
+    fill_random,
+    host_checksum,
+    words_per_row,
+)
+
+__all__ = [
+    "BitMatrix", "ColSwap", "DeviceMatrix", "MatrixView", "PleConfig", "PleOutcome",
+    "RowPermutation", "block_iterative_ple", "device_count", "fill_ctr", "fill_random",
+    "host_checksum", "words_per_row", "build", "load",
+]

@@ -1,0 +1,632 @@
+// gf2cu.cu -- host driver and C ABI (include/gf2cu.h) of the B200 PLE path.
+//
+// The driver replaces gf2::block_iterative_ple (ple.hpp:166-244): per
+// 64-column panel it enqueues panel_factor -> panel_apply -> trailing_update
+// on one stream, with all step state (r, rb) kept on the device so the host
+// never waits inside the loop. The host only polls a mapped pinned mirror of
+// r (a few steps behind) to stop enqueueing once every row holds a pivot.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "gf2cu.h"
+#include "ple_kernels.cuh"
+
+using gf2cu::u32;
+using gf2cu::u64;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+gf2cu_status fail(gf2cu_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+gf2cu_status cuda_fail(cudaError_t e, const char* what) {
+    const gf2cu_status st = (e == cudaErrorMemoryAllocation) ? GF2CU_ENOMEM : GF2CU_ECUDA;
+    return fail(st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CU_TRY(expr)                                                   \
+    do {                                                               \
+        cudaError_t _e = (expr);                                       \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);            \
+    } while (0)
+
+size_t words_of(size_t n) { return (n + 63) / 64; }
+size_t padded_stride(size_t n) { return std::max<size_t>(16, (words_of(n) + 15) / 16 * 16); }
+
+struct Workspace {
+    size_t m = 0, Wp = 0, W = 0;
+    u32* perm = nullptr;
+    u64* pb = nullptr;
+    u64* darr = nullptr;
+    u64* stage = nullptr;
+    gf2cu::StepState* state = nullptr;
+    gf2cu::PanelOut* pout = nullptr;
+    u32* swaps = nullptr;
+    u32* qcol = nullptr;
+    u32* rhist = nullptr;
+    u32* rbhist = nullptr;
+    u32* host_r = nullptr;       // pinned, mapped
+    u32* host_r_dev = nullptr;   // device alias
+    u64* hashes = nullptr;       // per-row checksum scratch
+    std::vector<cudaEvent_t> ev;
+};
+
+void free_ws(Workspace& w) {
+    cudaFree(w.perm);
+    cudaFree(w.pb);
+    cudaFree(w.darr);
+    cudaFree(w.stage);
+    cudaFree(w.state);
+    cudaFree(w.pout);
+    cudaFree(w.swaps);
+    cudaFree(w.qcol);
+    cudaFree(w.rhist);
+    cudaFree(w.rbhist);
+    cudaFree(w.hashes);
+    if (w.host_r) cudaFreeHost(w.host_r);
+    for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
+    w = Workspace{};
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int g_num_sms[64] = {0};
+
+int num_sms(int dev) {
+    if (dev < 0 || dev >= 64) return 148;
+    if (!g_num_sms[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = v > 0 ? v : 148;
+    }
+    return g_num_sms[dev];
+}
+
+}  // namespace
+
+struct gf2cu_matrix {
+    size_t m = 0, n = 0, W = 0, Wp = 0;
+    int device = 0;
+    u64* data = nullptr;
+    u64* alt = nullptr;  // unpermute target (swapped with data after a PLE)
+    Workspace ws;
+    cudaStream_t own = nullptr;
+};
+
+namespace {
+
+cudaStream_t pick_stream(gf2cu_matrix* a, void* s) {
+    return s ? reinterpret_cast<cudaStream_t>(s) : a->own;
+}
+
+gf2cu_status ensure_ws(gf2cu_matrix* a) {
+    Workspace& w = a->ws;
+    if (w.perm) return GF2CU_OK;
+    const size_t m = a->m, mn = std::max<size_t>(1, std::min(a->m, a->n));
+    w.m = m;
+    w.Wp = a->Wp;
+    w.W = a->W;
+    CU_TRY(cudaMalloc(&w.perm, std::max<size_t>(1, m) * sizeof(u32)));
+    CU_TRY(cudaMalloc(&w.pb, std::max<size_t>(1, m) * sizeof(u64)));
+    CU_TRY(cudaMalloc(&w.darr, std::max<size_t>(1, m) * sizeof(u64)));
+    CU_TRY(cudaMalloc(&w.stage, 64 * a->Wp * sizeof(u64)));
+    CU_TRY(cudaMemset(w.stage, 0, 64 * a->Wp * sizeof(u64)));
+    CU_TRY(cudaMalloc(&w.state, sizeof(gf2cu::StepState)));
+    CU_TRY(cudaMalloc(&w.pout, sizeof(gf2cu::PanelOut)));
+    CU_TRY(cudaMalloc(&w.swaps, mn * sizeof(u32)));
+    CU_TRY(cudaMalloc(&w.qcol, mn * sizeof(u32)));
+    CU_TRY(cudaMalloc(&w.rhist, (a->W + 1) * sizeof(u32)));
+    CU_TRY(cudaMalloc(&w.rbhist, (a->W + 1) * sizeof(u32)));
+    CU_TRY(cudaHostAlloc(&w.host_r, sizeof(u32), cudaHostAllocMapped));
+    CU_TRY(cudaHostGetDevicePointer(&w.host_r_dev, w.host_r, 0));
+    return GF2CU_OK;
+}
+
+gf2cu_status check_cfg(const gf2cu_cfg* cfg) {
+    if (!cfg) return GF2CU_OK;
+    if (!(cfg->k_scale > 0.0) && cfg->k == 0) return fail(GF2CU_EINVAL, "k_scale must be > 0");
+    return GF2CU_OK;
+}
+
+// Launches the whole decomposition on `s`; outputs are copied to the host.
+gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
+                     size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+                     gf2cu_stats* stats) {
+    gf2cu_status st = ensure_ws(a);
+    if (st != GF2CU_OK) return st;
+    Workspace& ws = a->ws;
+    cudaStream_t s = pick_stream(a, cfg ? cfg->stream : nullptr);
+    const bool timing = cfg && (cfg->flags & GF2CU_FLAG_TIME_KERNELS);
+    const size_t m = a->m, n = a->n, W = a->W;
+
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+    }
+    if (m == 0 || n == 0) {
+        *rank = 0;
+        if (n_col_swaps) *n_col_swaps = 0;
+        return GF2CU_OK;
+    }
+
+    gf2cu::Params p{};
+    p.mat = a->data;
+    p.perm = ws.perm;
+    p.pb = ws.pb;
+    p.darr = ws.darr;
+    p.stage = ws.stage;
+    p.state = ws.state;
+    p.pout = ws.pout;
+    p.swaps = ws.swaps;
+    p.qcol = ws.qcol;
+    p.rhist = ws.rhist;
+    p.rbhist = ws.rbhist;
+    p.host_r = ws.host_r_dev;
+    p.m = (u32)m;
+    p.n = (u32)n;
+    p.W = (u32)W;
+    p.Wp = (u32)a->Wp;
+
+    static bool attr_set[64] = {false};
+    if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
+        CU_TRY(cudaFuncSetAttribute(gf2cu::trailing_update_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    gf2cu::kTableBytes));
+        attr_set[a->device] = true;
+    }
+    const int sms = num_sms(a->device);
+    const int apply_grid = sms * 4;
+
+    if (timing) {
+        const size_t need = 6 * (W + 1);
+        while (ws.ev.size() < need) {
+            cudaEvent_t e;
+            CU_TRY(cudaEventCreate(&e));
+            ws.ev.push_back(e);
+        }
+    }
+
+    *ws.host_r = 0;
+    gf2cu::ple_init_kernel<<<sms * 4, 256, 0, s>>>(p);
+    CU_TRY(cudaGetLastError());
+
+    // Host stays at most kLag steps ahead of the device so that it notices
+    // r == m early (wide matrices) without stalling the stream.
+    constexpr size_t kLag = 6;
+    std::vector<cudaEvent_t> step_ev(kLag, nullptr);
+    for (auto& e : step_ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+    size_t steps = 0;
+    for (size_t w = 0; w < W; ++w) {
+        if (w >= kLag) {
+            CU_TRY(cudaEventSynchronize(step_ev[w % kLag]));
+            if (*reinterpret_cast<volatile u32*>(ws.host_r) >= m) break;
+        }
+        cudaEvent_t* E = timing ? &ws.ev[6 * w] : nullptr;
+        if (E) cudaEventRecord(E[0], s);
+        gf2cu::panel_factor_kernel<<<1, gf2cu::kPanelThreads, 0, s>>>(p, (u32)w);
+        if (E) cudaEventRecord(E[1], s);
+        if (E) cudaEventRecord(E[2], s);
+        gf2cu::panel_apply_kernel<<<apply_grid, gf2cu::kApplyThreads, 0, s>>>(p, (u32)w);
+        if (E) cudaEventRecord(E[3], s);
+        if (w + 1 < W) {
+            if (E) cudaEventRecord(E[4], s);
+            gf2cu::trailing_update_kernel<<<sms, gf2cu::kTrailThreads, gf2cu::kTableBytes, s>>>(
+                p, (u32)w);
+            if (E) cudaEventRecord(E[5], s);
+        }
+        CU_TRY(cudaGetLastError());
+        CU_TRY(cudaEventRecord(step_ev[w % kLag], s));
+        ++steps;
+    }
+    for (auto& e : step_ev) cudaEventDestroy(e);
+
+    // rank and histories
+    gf2cu::StepState fin{};
+    CU_TRY(cudaMemcpyAsync(&fin, ws.state, sizeof(fin), cudaMemcpyDeviceToHost, s));
+    std::vector<u32> rh(steps), rbh(steps);
+    if (steps) {
+        CU_TRY(cudaMemcpyAsync(rh.data(), ws.rhist, steps * sizeof(u32), cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaMemcpyAsync(rbh.data(), ws.rbhist, steps * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    }
+    CU_TRY(cudaStreamSynchronize(s));
+    const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
+
+    // gather rows back into position order
+    if (!a->alt) CU_TRY(cudaMalloc(&a->alt, std::max<size_t>(1, m) * a->Wp * sizeof(u64)));
+    gf2cu::unpermute_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, ws.perm, (u32)m, (u32)a->Wp);
+    CU_TRY(cudaGetLastError());
+    std::swap(a->data, a->alt);
+
+    std::vector<u32> sw(rk), qq(rk);
+    if (rk) {
+        CU_TRY(cudaMemcpyAsync(sw.data(), ws.swaps, rk * sizeof(u32), cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaMemcpyAsync(qq.data(), ws.qcol, rk * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    }
+    CU_TRY(cudaStreamSynchronize(s));
+    *rank = rk;
+    size_t ncs = 0;
+    for (size_t i = 0; i < rk; ++i) {
+        swaps[i] = sw[i];
+        q[i] = qq[i];
+        if (qq[i] != i) {
+            if (col_swaps) col_swaps[ncs] = gf2cu_colswap{i, (size_t)qq[i], i};
+            ++ncs;
+        }
+    }
+    if (n_col_swaps) *n_col_swaps = ncs;
+
+    if (stats) {
+        stats->steps = steps;
+        double bytes = 0.0;
+        size_t launches = 0;
+        for (size_t w = 0; w < steps; ++w) {
+            const size_t r0 = rh[w], rb = rbh[w];
+            if (r0 >= m || w + 1 >= W) continue;
+            ++launches;
+            bytes += 16.0 * double(m - r0 - rb) * double(W - w - 1);
+        }
+        stats->alg_bytes = bytes;
+        stats->trailing_launches = launches;
+        if (timing) {
+            double tp = 0, tc = 0, tt = 0;
+            for (size_t w = 0; w < steps; ++w) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ws.ev[6 * w], ws.ev[6 * w + 1]);
+                tp += ms;
+                cudaEventElapsedTime(&ms, ws.ev[6 * w + 2], ws.ev[6 * w + 3]);
+                tc += ms;
+                if (w + 1 < W) {
+                    cudaEventElapsedTime(&ms, ws.ev[6 * w + 4], ws.ev[6 * w + 5]);
+                    tt += ms;
+                }
+            }
+            stats->panel_ms = tp;
+            stats->coef_ms = tc;
+            stats->trailing_ms = tt;
+        }
+    }
+    return GF2CU_OK;
+}
+
+// --- host-side view packing (col_off may be unaligned) ---------------------
+u64 read_bits(const u64* row, size_t lo, size_t count) {
+    const size_t w = lo >> 6, b = lo & 63;
+    u64 v = row[w] >> b;
+    if (b != 0 && b + count > 64) v |= row[w + 1] << (64 - b);
+    return count >= 64 ? v : (v & ((1ull << count) - 1ull));
+}
+
+void write_bits(u64* row, size_t lo, size_t count, u64 bits) {
+    const size_t w = lo >> 6, b = lo & 63;
+    const u64 mask = count >= 64 ? ~0ull : ((1ull << count) - 1ull);
+    bits &= mask;
+    row[w] = (row[w] & ~(mask << b)) | (bits << b);
+    if (b != 0 && b + count > 64) {
+        const size_t spill = b + count - 64;
+        const u64 m2 = (1ull << spill) - 1ull;
+        row[w + 1] = (row[w + 1] & ~m2) | (bits >> (64 - b));
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+void gf2cu_default_config(gf2cu_cfg* cfg) {
+    if (!cfg) return;
+    cfg->k = 0;
+    cfg->k_scale = 0.75;
+    cfg->table_count = 4;
+    cfg->device = 0;
+    cfg->stream = nullptr;
+    cfg->flags = 0;
+}
+
+const char* gf2cu_last_error(void) { return g_last_error.c_str(); }
+
+const char* gf2cu_version(void) { return "gf2cu 0.1 (sm_100a, 64-column panels, 8x8-bit Gray tables)"; }
+
+int gf2cu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    int good = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp pr;
+        if (cudaGetDeviceProperties(&pr, d) == cudaSuccess && pr.major == 10) ++good;
+    }
+    return good;
+}
+
+gf2cu_status gf2cu_matrix_create(size_t m, size_t n, int device, gf2cu_matrix** out) {
+    if (!out) return fail(GF2CU_EINVAL, "out is null");
+    *out = nullptr;
+    if (m >= (1ull << 31) || n >= (1ull << 31))
+        return fail(GF2CU_EINVAL, "dimensions exceed 2^31");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(GF2CU_ENODEVICE, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(GF2CU_EINVAL, "bad device ordinal");
+    cudaDeviceProp pr;
+    CU_TRY(cudaGetDeviceProperties(&pr, device));
+    if (pr.major != 10)
+        return fail(GF2CU_ENODEVICE, "device is not sm_100 (built for sm_100a only)");
+    DeviceGuard g(device);
+    auto* a = new (std::nothrow) gf2cu_matrix;
+    if (!a) return fail(GF2CU_ENOMEM, "host allocation failed");
+    a->m = m;
+    a->n = n;
+    a->W = words_of(n);
+    a->Wp = padded_stride(n);
+    a->device = device;
+    const size_t bytes = std::max<size_t>(1, m) * a->Wp * sizeof(u64);
+    cudaError_t e = cudaMalloc(&a->data, bytes);
+    if (e == cudaSuccess) e = cudaMemset(a->data, 0, bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        cudaFree(a->data);
+        delete a;
+        return cuda_fail(e, "gf2cu_matrix_create");
+    }
+    *out = a;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_matrix_destroy(gf2cu_matrix* a) {
+    if (!a) return GF2CU_OK;
+    DeviceGuard g(a->device);
+    cudaFree(a->data);
+    cudaFree(a->alt);
+    free_ws(a->ws);
+    if (a->own) cudaStreamDestroy(a->own);
+    delete a;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_matrix_info(const gf2cu_matrix* a, size_t* m, size_t* n, size_t* stride_words,
+                               uint64_t** device_ptr) {
+    if (!a) return fail(GF2CU_EINVAL, "null matrix");
+    if (m) *m = a->m;
+    if (n) *n = a->n;
+    if (stride_words) *stride_words = a->Wp;
+    if (device_ptr) *device_ptr = reinterpret_cast<uint64_t*>(a->data);
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_matrix_upload(gf2cu_matrix* a, const uint64_t* host, size_t host_stride,
+                                 void* stream) {
+    if (!a || (!host && a->m)) return fail(GF2CU_EINVAL, "null argument");
+    if (host_stride < a->W) return fail(GF2CU_EINVAL, "host stride smaller than the row");
+    if (a->m == 0 || a->W == 0) return GF2CU_OK;
+    DeviceGuard g(a->device);
+    cudaStream_t s = pick_stream(a, stream);
+    CU_TRY(cudaMemcpy2DAsync(a->data, a->Wp * 8, host, host_stride * 8, a->W * 8, a->m,
+                             cudaMemcpyHostToDevice, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_matrix_download(const gf2cu_matrix* a, uint64_t* host, size_t host_stride,
+                                   void* stream) {
+    if (!a || (!host && a->m)) return fail(GF2CU_EINVAL, "null argument");
+    if (host_stride < a->W) return fail(GF2CU_EINVAL, "host stride smaller than the row");
+    if (a->m == 0 || a->W == 0) return GF2CU_OK;
+    DeviceGuard g(a->device);
+    cudaStream_t s = pick_stream(const_cast<gf2cu_matrix*>(a), stream);
+    CU_TRY(cudaMemcpy2DAsync(host, host_stride * 8, a->data, a->Wp * 8, a->W * 8, a->m,
+                             cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_matrix_copy(gf2cu_matrix* dst, const gf2cu_matrix* src, void* stream) {
+    if (!dst || !src) return fail(GF2CU_EINVAL, "null matrix");
+    if (dst->m != src->m || dst->n != src->n) return fail(GF2CU_EINVAL, "shape mismatch");
+    DeviceGuard g(dst->device);
+    cudaStream_t s = pick_stream(dst, stream);
+    CU_TRY(cudaMemcpyAsync(dst->data, src->data, std::max<size_t>(1, dst->m) * dst->Wp * 8,
+                           cudaMemcpyDeviceToDevice, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_matrix_fill_ctr(gf2cu_matrix* a, uint64_t seed, void* stream) {
+    if (!a) return fail(GF2CU_EINVAL, "null matrix");
+    if (a->m == 0) return GF2CU_OK;
+    DeviceGuard g(a->device);
+    cudaStream_t s = pick_stream(a, stream);
+    gf2cu::fill_ctr_kernel<<<num_sms(a->device) * 8, 256, 0, s>>>(a->data, (u32)a->m, (u32)a->n,
+                                                                 (u32)a->Wp, seed);
+    CU_TRY(cudaGetLastError());
+    CU_TRY(cudaStreamSynchronize(s));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_matrix_checksum(const gf2cu_matrix* a, uint64_t* out, void* stream) {
+    if (!a || !out) return fail(GF2CU_EINVAL, "null argument");
+    auto* am = const_cast<gf2cu_matrix*>(a);
+    DeviceGuard g(a->device);
+    if (a->m == 0) {
+        *out = 0;
+        return GF2CU_OK;
+    }
+    if (!am->ws.hashes) CU_TRY(cudaMalloc(&am->ws.hashes, a->m * sizeof(u64)));
+    cudaStream_t s = pick_stream(am, stream);
+    gf2cu::row_hash_kernel<<<num_sms(a->device) * 4, 256, 0, s>>>(a->data, (u32)a->m, (u32)a->W,
+                                                                 (u32)a->Wp, am->ws.hashes);
+    CU_TRY(cudaGetLastError());
+    std::vector<u64> h(a->m);
+    CU_TRY(cudaMemcpyAsync(h.data(), am->ws.hashes, a->m * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    // fold: FNV-1a over the row hashes
+    u64 acc = 0xcbf29ce484222325ull;
+    for (u64 v : h) {
+        acc ^= v;
+        acc *= 0x100000001b3ull;
+    }
+    *out = acc;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_ple_device(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
+                              size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+                              gf2cu_stats* stats) {
+    if (!a || !rank || ((!swaps || !q) && std::min(a->m, a->n) > 0))
+        return fail(GF2CU_EINVAL, "null argument");
+    gf2cu_status st = check_cfg(cfg);
+    if (st != GF2CU_OK) return st;
+    DeviceGuard g(a->device);
+    return run_ple(a, cfg, swaps, q, rank, col_swaps, n_col_swaps, stats);
+}
+
+gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
+                       size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+                       gf2cu_stats* stats) {
+    if (!v || !rank) return fail(GF2CU_EINVAL, "null argument");
+    const size_t m = v->nrows, n = v->ncols;
+    if (m && n && !v->data) return fail(GF2CU_EINVAL, "null data");
+    if (m && n && v->stride * 64 < v->col_off + n)
+        return fail(GF2CU_ERANGE, "view window exceeds its row stride");
+    if ((!swaps || !q) && std::min(m, n) > 0) return fail(GF2CU_EINVAL, "null outputs");
+    gf2cu_status st = check_cfg(cfg);
+    if (st != GF2CU_OK) return st;
+    if (m == 0 || n == 0) {
+        *rank = 0;
+        if (n_col_swaps) *n_col_swaps = 0;
+        if (stats) std::memset(stats, 0, sizeof(*stats));
+        return GF2CU_OK;
+    }
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    if (cfg) c = *cfg;
+    gf2cu_matrix* a = nullptr;
+    st = gf2cu_matrix_create(m, n, c.device, &a);
+    if (st != GF2CU_OK) return st;
+    DeviceGuard g(c.device);
+    cudaStream_t s = pick_stream(a, c.stream);
+    const size_t W = a->W;
+    std::vector<u64> packed;
+    const bool aligned = (v->col_off & 63) == 0 && (n & 63) == 0;
+    cudaError_t e = cudaSuccess;
+    if (aligned) {
+        e = cudaMemcpy2DAsync(a->data, a->Wp * 8, v->data + (v->col_off >> 6), v->stride * 8, W * 8,
+                              m, cudaMemcpyHostToDevice, s);
+    } else {
+        packed.assign(m * W, 0ull);
+        for (size_t i = 0; i < m; ++i) {
+            const u64* row = reinterpret_cast<const u64*>(v->data) + i * v->stride;
+            for (size_t x = 0; x < W; ++x) {
+                const size_t take = std::min<size_t>(64, n - 64 * x);
+                packed[i * W + x] = read_bits(row, v->col_off + 64 * x, take);
+            }
+        }
+        e = cudaMemcpy2DAsync(a->data, a->Wp * 8, packed.data(), W * 8, W * 8, m,
+                              cudaMemcpyHostToDevice, s);
+    }
+    if (e != cudaSuccess) {
+        gf2cu_matrix_destroy(a);
+        return cuda_fail(e, "upload");
+    }
+    c.stream = s;
+    st = run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats);
+    if (st == GF2CU_OK) {
+        if (aligned) {
+            e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6), v->stride * 8, a->data, a->Wp * 8,
+                                  W * 8, m, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        } else {
+            e = cudaMemcpy2DAsync(packed.data(), W * 8, a->data, a->Wp * 8, W * 8, m,
+                                  cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e == cudaSuccess)
+                for (size_t i = 0; i < m; ++i) {
+                    u64* row = reinterpret_cast<u64*>(v->data) + i * v->stride;
+                    for (size_t x = 0; x < W; ++x) {
+                        const size_t take = std::min<size_t>(64, n - 64 * x);
+                        write_bits(row, v->col_off + 64 * x, take, packed[i * W + x]);
+                    }
+                }
+        }
+        if (e != cudaSuccess) st = cuda_fail(e, "download");
+        if (stats) {
+            stats->h2d_bytes = double(m) * W * 8;
+            stats->d2h_bytes = double(m) * W * 8;
+        }
+    }
+    gf2cu_matrix_destroy(a);
+    return st;
+}
+
+gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t stride, double density,
+                               uint64_t seed) {
+    // The same engine and draw order as gf2::fill_random (bit_matrix.hpp:459-486).
+    if (density < 0.0 || density > 1.0) return fail(GF2CU_EINVAL, "density outside [0,1]");
+    const size_t W = words_of(n);
+    if (m && W && !words) return fail(GF2CU_EINVAL, "null words");
+    if (stride < W) return fail(GF2CU_EINVAL, "stride smaller than the row");
+    std::mt19937_64 rng(seed);
+    const u64 last = (n & 63) ? ((1ull << (n & 63)) - 1ull) : ~0ull;
+    for (size_t i = 0; i < m; ++i) {
+        u64* row = reinterpret_cast<u64*>(words) + i * stride;
+        for (size_t x = 0; x < W; ++x) {
+            u64 v;
+            if (density == 0.0)
+                v = 0;
+            else if (density == 1.0)
+                v = ~0ull;
+            else if (density == 0.5)
+                v = rng();
+            else {
+                v = 0;
+                for (unsigned b = 0; b < 64; ++b) {
+                    const double u = double(rng() >> 11) * 0x1.0p-53;
+                    v |= u64(u < density) << b;
+                }
+            }
+            row[x] = v;
+        }
+        if (W) row[W - 1] &= last;
+    }
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, uint64_t seed) {
+    const size_t W = words_of(n);
+    if (m && W && !words) return fail(GF2CU_EINVAL, "null words");
+    if (stride < W) return fail(GF2CU_EINVAL, "stride smaller than the row");
+    const u64 base = seed << 32;
+    const u64 last = (n & 63) ? ((1ull << (n & 63)) - 1ull) : ~0ull;
+    for (size_t i = 0; i < m; ++i) {
+        u64* row = reinterpret_cast<u64*>(words) + i * stride;
+        for (size_t x = 0; x < W; ++x) {
+            u64 z = base + (u64(i) * W + x + 1ull) * 0x9e3779b97f4a7c15ull;
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+            row[x] = z ^ (z >> 31);
+        }
+        if (W) row[W - 1] &= last;
+    }
+    return GF2CU_OK;
+}
+
+}  // extern "C"

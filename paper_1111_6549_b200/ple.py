@@ -1,0 +1,367 @@
+"""Host-side mirror of the reference PLE interface over the B200 C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/gf2/{bit_matrix,ple}.hpp:
+
+* ``BitMatrix`` / ``MatrixView``   -- bit_matrix.hpp:163-394 (row-major
+  uint64 words, LSB-first, padding bits zero; views carry a bit offset).
+* ``PleConfig``, ``ColSwap``, ``PleOutcome`` -- ple.hpp:31-51.
+* ``RowPermutation``               -- bit_matrix.hpp:416-438 (LAPACK swaps).
+* ``block_iterative_ple(a, cfg)``  -- ple.hpp:166, computed on the B200 by
+  ``gf2cu_ple`` (host view) or ``gf2cu_ple_device`` (``DeviceMatrix``).
+
+Exceptions match the reference: ValueError for std::invalid_argument,
+IndexError for std::out_of_range, MemoryError for std::bad_alloc; CUDA
+failures (including "no sm_100 device") raise ``Gf2cuError``. There is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, gf2cu_cfg, gf2cu_colswap, gf2cu_stats, gf2cu_view
+
+WORD_BITS = 64
+
+
+def words_per_row(ncols: int) -> int:
+    return (ncols + WORD_BITS - 1) // WORD_BITS
+
+
+# --------------------------------------------------------------------- types
+@dataclass
+class PleConfig:
+    """ple.hpp:31-39. k / table_count are accepted for interface parity; the
+    device path factors 64-column panels and its output does not depend on
+    them (nor does the reference's)."""
+    k: int = 0
+    k_scale: float = 0.75
+    table_count: int = 4
+    base_bytes: int = 256 << 10
+    base_ncols: int = 64
+    base_k: int = 0
+    device: int = 0
+    stream: Optional[int] = None   # cudaStream_t as an int (e.g. torch stream.cuda_stream)
+    time_kernels: bool = False
+
+    def to_c(self) -> gf2cu_cfg:
+        c = gf2cu_cfg()
+        _lib.load().gf2cu_default_config(C.byref(c))
+        c.k = int(self.k)
+        c.k_scale = float(self.k_scale)
+        c.table_count = max(1, int(self.table_count))
+        c.device = int(self.device)
+        c.stream = C.c_void_p(self.stream) if self.stream else None
+        c.flags = _lib.FLAG_TIME_KERNELS if self.time_kernels else 0
+        return c
+
+
+@dataclass(frozen=True)
+class ColSwap:
+    a: int
+    b: int
+    from_row: int
+
+
+@dataclass
+class RowPermutation:
+    """LAPACK-style transpositions: swaps[i] is the row swapped with row i
+    (bit_matrix.hpp:416-438)."""
+    swaps: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.uint64))
+
+    def size(self) -> int:
+        return len(self.swaps)
+
+    def validate(self, nrows: int) -> None:
+        s = np.asarray(self.swaps, dtype=np.int64)
+        if len(s) and (np.any(s < np.arange(len(s))) or np.any(s >= nrows)):
+            raise ValueError("RowPermutation: entry out of range")
+
+    def apply(self, a: np.ndarray) -> None:
+        """Replay the swaps forward on the rows of a 2-D array."""
+        self.validate(a.shape[0])
+        for i, j in enumerate(np.asarray(self.swaps, dtype=np.int64)):
+            if j != i:
+                a[[i, j]] = a[[j, i]]
+
+    def apply_inverse(self, a: np.ndarray) -> None:
+        self.validate(a.shape[0])
+        s = np.asarray(self.swaps, dtype=np.int64)
+        for i in range(len(s) - 1, -1, -1):
+            j = s[i]
+            if j != i:
+                a[[i, j]] = a[[j, i]]
+
+
+@dataclass
+class PleOutcome:
+    """ple.hpp:45-51."""
+    rank: int = 0
+    processed: int = 0
+    p: RowPermutation = field(default_factory=RowPermutation)
+    q: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.uint64))
+    col_swaps: List[ColSwap] = field(default_factory=list)
+    stats: Optional[dict] = None
+
+
+class MatrixView:
+    """Non-owning window {data, stride, col_off, nrows, ncols} over a uint64
+    word array (bit_matrix.hpp:163-340)."""
+
+    def __init__(self, words: np.ndarray, stride: int, col_off: int, nrows: int, ncols: int):
+        if words.dtype != np.uint64:
+            raise ValueError("MatrixView needs uint64 words")
+        self.words = words
+        self.stride = int(stride)
+        self.col_off = int(col_off)
+        self._nrows = int(nrows)
+        self._ncols = int(ncols)
+
+    def nrows(self) -> int:
+        return self._nrows
+
+    def ncols(self) -> int:
+        return self._ncols
+
+    def col_offset(self) -> int:
+        return self.col_off
+
+    def sub(self, r0: int, c0: int, rows: int, cols: int) -> "MatrixView":
+        if r0 > self._nrows or rows > self._nrows - r0 or c0 > self._ncols or cols > self._ncols - c0:
+            raise IndexError("subview outside matrix view")
+        flat = self.words.reshape(-1)
+        return MatrixView(flat[r0 * self.stride:], self.stride, self.col_off + c0, rows, cols)
+
+    def get(self, i: int, j: int) -> bool:
+        p = self.col_off + j
+        return bool((int(self.words.reshape(-1)[i * self.stride + (p >> 6)]) >> (p & 63)) & 1)
+
+    def _c(self) -> gf2cu_view:
+        v = gf2cu_view()
+        if not self.words.flags["C_CONTIGUOUS"]:
+            raise ValueError("MatrixView words must be C-contiguous")
+        v.data = self.words.ctypes.data_as(C.POINTER(C.c_uint64))
+        v.stride = self.stride
+        v.col_off = self.col_off
+        v.nrows = self._nrows
+        v.ncols = self._ncols
+        return v
+
+
+class BitMatrix:
+    """Owning packed matrix, stride = ceil(ncols/64) words, padding zero
+    (bit_matrix.hpp:342-394)."""
+
+    def __init__(self, rows: int, cols: int, words: Optional[np.ndarray] = None):
+        self._nrows, self._ncols = int(rows), int(cols)
+        self._stride = words_per_row(cols)
+        if words is None:
+            self.words = np.zeros((rows, self._stride), dtype=np.uint64)
+        else:
+            words = np.ascontiguousarray(words, dtype=np.uint64)
+            if words.shape != (rows, self._stride):
+                raise ValueError("words shape does not match (rows, ceil(cols/64))")
+            self.words = words
+
+    @staticmethod
+    def identity(n: int) -> "BitMatrix":
+        a = BitMatrix(n, n)
+        for i in range(n):
+            a.words[i, i >> 6] |= np.uint64(1) << np.uint64(i & 63)
+        return a
+
+    @staticmethod
+    def from_rows(rows: List[str]) -> "BitMatrix":
+        a = BitMatrix(len(rows), len(rows[0]) if rows else 0)
+        for i, s in enumerate(rows):
+            for j, ch in enumerate(s):
+                if ch == "1":
+                    a.set(i, j, True)
+        return a
+
+    def nrows(self) -> int:
+        return self._nrows
+
+    def ncols(self) -> int:
+        return self._ncols
+
+    def stride(self) -> int:
+        return self._stride
+
+    def get(self, i: int, j: int) -> bool:
+        return bool((int(self.words[i, j >> 6]) >> (j & 63)) & 1)
+
+    def set(self, i: int, j: int, v: bool) -> None:
+        bit = np.uint64(1) << np.uint64(j & 63)
+        if v:
+            self.words[i, j >> 6] |= bit
+        else:
+            self.words[i, j >> 6] &= ~bit
+
+    def view(self) -> MatrixView:
+        return MatrixView(self.words, self._stride, 0, self._nrows, self._ncols)
+
+    def copy(self) -> "BitMatrix":
+        return BitMatrix(self._nrows, self._ncols, self.words.copy())
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, BitMatrix) and self._nrows == other._nrows
+                and self._ncols == other._ncols and np.array_equal(self.words, other.words))
+
+    def row_string(self, i: int) -> str:
+        return "".join("1" if self.get(i, j) else "0" for j in range(self._ncols))
+
+
+# --------------------------------------------------------------- generators
+def fill_random(a: BitMatrix, density: float, seed: int) -> None:
+    """gf2::fill_random (bit_matrix.hpp:459-486), host-side (std::mt19937_64)."""
+    L = _lib.load()
+    check(L.gf2cu_fill_random(a.words.ctypes.data_as(C.POINTER(C.c_uint64)), a.nrows(), a.ncols(),
+                              a.stride(), float(density), int(seed) & (2**64 - 1)))
+
+
+def fill_ctr(a: BitMatrix, seed: int) -> None:
+    """The counter generator of SURVEY.md 8(d) (random access; the device
+    generator DeviceMatrix.fill_ctr produces the same words)."""
+    L = _lib.load()
+    check(L.gf2cu_fill_ctr(a.words.ctypes.data_as(C.POINTER(C.c_uint64)), a.nrows(), a.ncols(),
+                           a.stride(), int(seed) & (2**64 - 1)))
+
+
+# ----------------------------------------------------------- device matrix
+class DeviceMatrix:
+    """An m x n matrix resident in HBM (128-byte aligned rows)."""
+
+    def __init__(self, m: int, n: int, device: int = 0):
+        L = _lib.load()
+        h = C.c_void_p()
+        check(L.gf2cu_matrix_create(m, n, device, C.byref(h)))
+        self._h = h
+        self.m, self.n, self.device = m, n, device
+        st = C.c_size_t()
+        ptr = C.POINTER(C.c_uint64)()
+        check(L.gf2cu_matrix_info(h, None, None, C.byref(st), C.byref(ptr)))
+        self.stride_words = st.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def data_ptr(self) -> int:
+        ptr = C.POINTER(C.c_uint64)()
+        check(_lib.load().gf2cu_matrix_info(self._h, None, None, None, C.byref(ptr)))
+        return C.cast(ptr, C.c_void_p).value or 0
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.load().gf2cu_matrix_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, words: np.ndarray, stream: Optional[int] = None) -> None:
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        if words.shape[0] != self.m:
+            raise ValueError("row count mismatch")
+        check(_lib.load().gf2cu_matrix_upload(self._h, words.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                              words.shape[1], C.c_void_p(stream) if stream else None))
+
+    def upload_ptr(self, host_ptr: int, host_stride: int, stream: Optional[int] = None) -> None:
+        check(_lib.load().gf2cu_matrix_upload(self._h, C.cast(C.c_void_p(host_ptr), C.POINTER(C.c_uint64)),
+                                              host_stride, C.c_void_p(stream) if stream else None))
+
+    def download(self, out: Optional[np.ndarray] = None, stream: Optional[int] = None) -> np.ndarray:
+        W = words_per_row(self.n)
+        if out is None:
+            out = np.zeros((self.m, max(1, W)), dtype=np.uint64)
+        check(_lib.load().gf2cu_matrix_download(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                out.shape[1], C.c_void_p(stream) if stream else None))
+        return out
+
+    def download_ptr(self, host_ptr: int, host_stride: int, stream: Optional[int] = None) -> None:
+        check(_lib.load().gf2cu_matrix_download(self._h, C.cast(C.c_void_p(host_ptr), C.POINTER(C.c_uint64)),
+                                                host_stride, C.c_void_p(stream) if stream else None))
+
+    def copy_from(self, other: "DeviceMatrix", stream: Optional[int] = None) -> None:
+        check(_lib.load().gf2cu_matrix_copy(self._h, other._h, C.c_void_p(stream) if stream else None))
+
+    def fill_ctr(self, seed: int, stream: Optional[int] = None) -> None:
+        check(_lib.load().gf2cu_matrix_fill_ctr(self._h, int(seed) & (2**64 - 1),
+                                                C.c_void_p(stream) if stream else None))
+
+    def checksum(self, stream: Optional[int] = None) -> int:
+        out = C.c_uint64()
+        check(_lib.load().gf2cu_matrix_checksum(self._h, C.byref(out), C.c_void_p(stream) if stream else None))
+        return out.value
+
+
+def host_checksum(words: np.ndarray, ncols: int) -> int:
+    """Same fold as gf2cu_matrix_checksum, computed on host words (test helper
+    and bench parity handle): per-row FNV-1a over the W logical words, then
+    FNV-1a over the row hashes."""
+    W = words_per_row(ncols)
+    w = np.ascontiguousarray(words[:, :W], dtype=np.uint64)
+    prime = np.uint64(0x100000001B3)
+    h = np.full(w.shape[0], 0xCBF29CE484222325, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for x in range(W):
+            h ^= w[:, x]
+            h *= prime
+        acc = np.uint64(0xCBF29CE484222325)
+        for v in h:
+            acc ^= v
+            acc *= prime
+    return int(acc)
+
+
+# ----------------------------------------------------------------- the path
+def _outcome(rank, swaps, q, cs, ncs, m, st) -> PleOutcome:
+    r = int(rank.value)
+    out = PleOutcome(rank=r, processed=m)
+    out.p = RowPermutation(np.array(swaps[:r], dtype=np.uint64))
+    out.q = np.array(q[:r], dtype=np.uint64)
+    out.col_swaps = [ColSwap(int(cs[i].a), int(cs[i].b), int(cs[i].from_row)) for i in range(int(ncs.value))]
+    out.stats = {f: getattr(st, f) for f, _ in gf2cu_stats._fields_}
+    return out
+
+
+def block_iterative_ple(a, cfg: Optional[PleConfig] = None) -> PleOutcome:
+    """gf2::block_iterative_ple (ple.hpp:166) on the B200.
+
+    ``a`` is a ``BitMatrix``/``MatrixView`` (host words, factored in place)
+    or a ``DeviceMatrix`` (factored in place in HBM)."""
+    cfg = cfg or PleConfig()
+    L = _lib.load()
+    c = cfg.to_c()
+    if isinstance(a, DeviceMatrix):
+        m, n = a.m, a.n
+        h = a.handle
+    else:
+        view = a.view() if isinstance(a, BitMatrix) else a
+        m, n = view.nrows(), view.ncols()
+    cap = max(1, min(m, n))
+    swaps = (C.c_size_t * cap)()
+    q = (C.c_size_t * cap)()
+    cs = (gf2cu_colswap * cap)()
+    rank = C.c_size_t()
+    ncs = C.c_size_t()
+    st = gf2cu_stats()
+    if isinstance(a, DeviceMatrix):
+        check(L.gf2cu_ple_device(h, C.byref(c), swaps, q, C.byref(rank), cs, C.byref(ncs), C.byref(st)))
+    else:
+        v = view._c()
+        check(L.gf2cu_ple(C.byref(v), C.byref(c), swaps, q, C.byref(rank), cs, C.byref(ncs), C.byref(st)))
+    return _outcome(rank, swaps, q, cs, ncs, m, st)
+
+
+def device_count() -> int:
+    return int(_lib.load().gf2cu_device_count())
