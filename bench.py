@@ -1,0 +1,385 @@
+#!/usr/bin/env python3
+"""bench.py -- B200 block-iterative PLE over F2 (BASELINE.json metric).
+
+metric: "PLE wall time & effective HBM GB/s, 65536^2 random F2 matrix, 1-8 GPU"
+
+A step = one complete PLE (gf2::block_iterative_ple semantics) of the
+65536 x 65536 matrix from the F2-nonlinear counter generator (SURVEY.md 8(d),
+seed 1, rank 65534), i.e. one pass of the hot path over one synthetic input.
+
+value      = effective GB/s = algorithmic trailing-update bytes / device time,
+             summed over all ranks' steps ("alg bytes" = sum over 64-column
+             panel steps of 16*(m-r-rb)*(W-w-1)); every step
+             restores the input from a pristine HBM copy inside the timed
+             region (the 512 MiB D2D copy is counted in the time).
+e2e        = the same metric through the C ABI drop-in gf2cu_ple() on pinned
+             HOST buffers: H2D of the input + PLE + D2H of L\\E every step.
+roofline   = trailing_update (the dominant kernel): algorithmic bytes per
+             launch / average CUDA-event launch duration, vs the measured HBM
+             copy bandwidth in MEASURED_PEAKS.json.
+cpu_baseline = the reference itself (oracle/_ref/libgf2ref.so, compiled from
+             /root/reference headers with its Release flags), single-threaded,
+             on a bounded sample (the leading 65536 x 8192 column block of the
+             same matrix), rank 0 at N=1 only.
+
+--impl reference runs that reference arm alone (rank 0; other ranks exit 0).
+Multi-GPU (torchrun, N>1): weak-scaling replicas -- each rank factors its own
+65536^2 instance (the sharded 131072^2 path is not benchmarked
+here); value is the total over ranks / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PLE wall time & effective HBM GB/s, 65536² random F2 matrix, 1–8 GPU"
+UNIT = "GB/s"
+N_DEFAULT = 65536
+SEED = 1
+REF_SAMPLE_COLS = 8192
+
+
+def alg_bytes_from_history(m, n, rhist, rbhist):
+    W = (n + 63) // 64
+    tot = 0
+    for w, (r, rb) in enumerate(zip(rhist, rbhist)):
+        if r >= m or w + 1 >= W:
+            continue
+        tot += 16 * (m - r - rb) * (W - w - 1)
+    return tot
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """DRAM bytes per trailing_update launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "trailing_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_alg_byte")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxs.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def make_host_ctr(m, n, seed):
+    import paper_1111_6549_b200 as G
+    a = G.BitMatrix(m, n)
+    G.fill_ctr(a, seed)
+    return a.words
+
+
+# ------------------------------------------------------------------ CPU legs
+def run_reference_sample(m, cols, seed, reps=1):
+    """The compiled reference on the leading m x cols block of the ctr matrix."""
+    import oracle as O
+    full_W = (N_DEFAULT + 63) // 64
+    Wc = (cols + 63) // 64
+    # the ctr generator is keyed on the full row width: generate full rows, slice
+    big = make_host_ctr(m, N_DEFAULT, seed)
+    assert big.shape[1] == full_W
+    base = np.ascontiguousarray(big[:, :Wc])
+    del big
+    secs, last = [], None
+    for _ in range(reps):
+        a = base.copy()
+        out, s = O.ref_ple(a, m, cols)
+        secs.append(s)
+        last = out
+    # algorithmic bytes of the sample with the same definition (K = 64 panels)
+    rh, rbh = [], []
+    q = np.asarray(last.q, dtype=np.int64)
+    W = Wc
+    r = 0
+    for w in range(W):
+        rb = int(np.count_nonzero((q >= 64 * w) & (q < 64 * w + 64)))
+        rh.append(r)
+        rbh.append(rb)
+        r += rb
+    return secs, alg_bytes_from_history(m, cols, rh, rbh), last.rank
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    m, cols = N_DEFAULT, REF_SAMPLE_COLS
+    try:
+        import oracle as O
+        O.ref()
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
+        return
+    for _ in range(args.warmup):
+        run_reference_sample(m, cols, SEED)
+    t0 = time.perf_counter()
+    secs_all, bytes_all = [], 0
+    for _ in range(args.steps):
+        secs, b, rk = run_reference_sample(m, cols, SEED)
+        secs_all += secs
+        bytes_all += b
+    wall = time.perf_counter() - t0
+    tsum = sum(secs_all)
+    val = bytes_all / tsum / 1e9
+    sample = f"leading {m}x{cols} column block of the 65536^2 ctr(seed {SEED}) matrix, rank {rk}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tsum / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"block_iterative_ple {N_DEFAULT}x{N_DEFAULT} (BASELINE config 5, 1 GPU)",
+                   "sample": f"{m}x{cols} leading column block per step (bounded CPU sample)",
+                   "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "panel_bits": 64},
+        "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(val, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(wall, 2),
+    }))
+
+
+# ------------------------------------------------------------------ GPU leg
+def gpu_arm(args, rank, world, local_rank):
+    import torch
+    import paper_1111_6549_b200 as G
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    m = n = args.n
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    pristine = G.DeviceMatrix(m, n, device=dev)
+    pristine.fill_ctr(SEED, stream=sptr)
+    work = G.DeviceMatrix(m, n, device=dev)
+    cfg = G.PleConfig(device=dev, stream=sptr)
+    cfg_t = G.PleConfig(device=dev, stream=sptr, time_kernels=True)
+
+    # warm-up (also yields the rank / checksum for the parity handle)
+    for _ in range(args.warmup):
+        work.copy_from(pristine, stream=sptr)
+        out = G.block_iterative_ple(work, cfg)
+    checksum = work.checksum(stream=sptr) if args.warmup else None
+
+    # ---- timed region: K steps, device-resident inputs ----
+    clocks = ClockSampler(dev)
+    barrier()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    tot_bytes = 0.0
+    trail_ms = 0.0
+    launches = 0
+    kernel_launches = 0
+    for _ in range(args.steps):
+        work.copy_from(pristine, stream=sptr)
+        out = G.block_iterative_ple(work, cfg_t)
+        st = out.stats
+        tot_bytes += st["alg_bytes"]
+        trail_ms += st["trailing_ms"]
+        launches += st["trailing_launches"]
+        # tile + init + untile, and per step panel + apply (+ trailing)
+        kernel_launches += 3 + 2 * st["steps"] + st["trailing_launches"]
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+
+    # ---- e2e: drop-in gf2cu_ple on pinned host buffers ----
+    Wd = (n + 63) // 64
+    host = torch.empty((m, Wd), dtype=torch.int64, pin_memory=True)
+    host_np = host.numpy().view(np.uint64)
+    pristine.download(host_np)
+    src = host_np.copy()
+    view = G.MatrixView(host_np, Wd, 0, m, n)
+    e2e_steps = max(1, min(args.steps, 3))
+    np.copyto(host_np, src)
+    G.block_iterative_ple(view, cfg)  # warm the cached device buffers
+    barrier()
+    e2e_s = 0.0
+    e2e_bytes = 0.0
+    for _ in range(e2e_steps):
+        np.copyto(host_np, src)  # restore the input (host memcpy, outside the timing)
+        t0 = time.perf_counter()
+        o2 = G.block_iterative_ple(view, cfg)
+        e2e_s += time.perf_counter() - t0
+        e2e_bytes += o2.stats["alg_bytes"]
+    e2e_parity = (o2.rank == out.rank)
+
+    # ---- max over ranks ----
+    vals = torch.tensor([dev_ms, tot_bytes, e2e_s, e2e_bytes, trail_ms, float(launches)],
+                        dtype=torch.float64, device="cuda")
+    if dist is not None:
+        allv = [torch.zeros_like(vals) for _ in range(world)]
+        dist.all_gather(allv, vals)
+        allv = torch.stack(allv).cpu().numpy()
+    else:
+        allv = vals.cpu().numpy()[None, :]
+    max_ms = float(allv[:, 0].max())
+    sum_bytes = float(allv[:, 1].sum())
+    e2e_max_s = float(allv[:, 2].max())
+    e2e_sum_bytes = float(allv[:, 3].sum())
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    value = sum_bytes / (max_ms * 1e-3) / 1e9
+    e2e_value = e2e_sum_bytes / e2e_max_s / 1e9
+    peak, peak_kind = load_peaks()
+    per_launch_bytes = tot_bytes / max(1, launches)
+    per_launch_ms = trail_ms / max(1, launches)
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else None
+    traffic_ratio = load_traffic()
+    roofline = {
+        "kernel": "trailing_update_kernel", "bound": "hbm",
+        "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4) if achieved else None,
+        "traffic": (round(per_launch_bytes * traffic_ratio) if traffic_ratio else None),
+        "alg_bytes_per_launch": round(per_launch_bytes), "avg_launch_ms": round(per_launch_ms, 5),
+        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
+        "share_of_step": round(trail_ms / max(1e-9, dev_ms), 4),
+    }
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            secs, b, rk = run_reference_sample(n, REF_SAMPLE_COLS, SEED)
+            cpu = {"value": round(b / secs[0] / 1e9, 3), "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"leading {n}x{REF_SAMPLE_COLS} column block of the same matrix "
+                             f"(rank {rk}), {secs[0]:.2f} s, single-threaded gf2::block_iterative_ple",
+                   "host_cores": os.cpu_count()}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"block_iterative_ple {m}x{n} (BASELINE config 5, 1 GPU)",
+                   "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "rank": int(out.rank),
+                   "panel_bits": 64, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "l2": "input 512 MiB > 126 MB L2; pristine copy restored each step (counted)",
+                   "checksum": hex(checksum) if checksum is not None else None},
+        "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(m * Wd * 8), "d2h_bytes_per_step": int(m * Wd * 8),
+                "steps": e2e_steps, "ms_per_step": round(1e3 * e2e_max_s / e2e_steps, 3),
+                "rank_matches_device_run": bool(e2e_parity)},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": int(kernel_launches),
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    gpu_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

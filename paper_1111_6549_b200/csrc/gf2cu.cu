@@ -43,13 +43,14 @@ gf2cu_status cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 size_t words_of(size_t n) { return (n + 63) / 64; }
+size_t wpad8(size_t W) { return std::max<size_t>(8, (W + 7) / 8 * 8); }
 size_t padded_stride(size_t n) { return std::max<size_t>(16, (words_of(n) + 15) / 16 * 16); }
 
 struct Workspace {
     size_t m = 0, Wp = 0, W = 0;
     u32* perm = nullptr;
     u64* pb = nullptr;
-    u64* darr = nullptr;
+    ulonglong2* info = nullptr;
     u64* stage = nullptr;
     gf2cu::StepState* state = nullptr;
     gf2cu::PanelOut* pout = nullptr;
@@ -66,7 +67,7 @@ struct Workspace {
 void free_ws(Workspace& w) {
     cudaFree(w.perm);
     cudaFree(w.pb);
-    cudaFree(w.darr);
+    cudaFree(w.info);
     cudaFree(w.stage);
     cudaFree(w.state);
     cudaFree(w.pout);
@@ -109,7 +110,7 @@ struct gf2cu_matrix {
     size_t m = 0, n = 0, W = 0, Wp = 0;
     int device = 0;
     u64* data = nullptr;
-    u64* alt = nullptr;  // unpermute target (swapped with data after a PLE)
+    u64* alt = nullptr;  // tile-major working copy used by the factorization
     Workspace ws;
     cudaStream_t own = nullptr;
 };
@@ -129,9 +130,9 @@ gf2cu_status ensure_ws(gf2cu_matrix* a) {
     w.W = a->W;
     CU_TRY(cudaMalloc(&w.perm, std::max<size_t>(1, m) * sizeof(u32)));
     CU_TRY(cudaMalloc(&w.pb, std::max<size_t>(1, m) * sizeof(u64)));
-    CU_TRY(cudaMalloc(&w.darr, std::max<size_t>(1, m) * sizeof(u64)));
-    CU_TRY(cudaMalloc(&w.stage, 64 * a->Wp * sizeof(u64)));
-    CU_TRY(cudaMemset(w.stage, 0, 64 * a->Wp * sizeof(u64)));
+    CU_TRY(cudaMalloc(&w.info, std::max<size_t>(1, m) * sizeof(ulonglong2)));
+    CU_TRY(cudaMalloc(&w.stage, 64 * wpad8(a->W) * sizeof(u64)));
+    CU_TRY(cudaMemset(w.stage, 0, 64 * wpad8(a->W) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.state, sizeof(gf2cu::StepState)));
     CU_TRY(cudaMalloc(&w.pout, sizeof(gf2cu::PanelOut)));
     CU_TRY(cudaMalloc(&w.swaps, mn * sizeof(u32)));
@@ -170,10 +171,11 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
 
     gf2cu::Params p{};
-    p.mat = a->data;
+    if (!a->alt) CU_TRY(cudaMalloc(&a->alt, std::max<size_t>(1, m) * wpad8(W) * sizeof(u64)));
+    p.mat = a->alt;
     p.perm = ws.perm;
     p.pb = ws.pb;
-    p.darr = ws.darr;
+    p.info = ws.info;
     p.stage = ws.stage;
     p.state = ws.state;
     p.pout = ws.pout;
@@ -185,7 +187,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     p.m = (u32)m;
     p.n = (u32)n;
     p.W = (u32)W;
-    p.Wp = (u32)a->Wp;
+    p.Wpad8 = (u32)wpad8(W);
 
     static bool attr_set[64] = {false};
     if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
@@ -207,6 +209,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
 
     *ws.host_r = 0;
+    gf2cu::tile_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, p.Wpad8);
     gf2cu::ple_init_kernel<<<sms * 4, 256, 0, s>>>(p);
     CU_TRY(cudaGetLastError());
 
@@ -252,11 +255,10 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     CU_TRY(cudaStreamSynchronize(s));
     const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
 
-    // gather rows back into position order
-    if (!a->alt) CU_TRY(cudaMalloc(&a->alt, std::max<size_t>(1, m) * a->Wp * sizeof(u64)));
-    gf2cu::unpermute_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, ws.perm, (u32)m, (u32)a->Wp);
+    // back to the row-major public layout, rows gathered into position order
+    gf2cu::untile_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
+                                                p.Wpad8);
     CU_TRY(cudaGetLastError());
-    std::swap(a->data, a->alt);
 
     std::vector<u32> sw(rk), qq(rk);
     if (rk) {
@@ -519,9 +521,22 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
     gf2cu_cfg c;
     gf2cu_default_config(&c);
     if (cfg) c = *cfg;
-    gf2cu_matrix* a = nullptr;
-    st = gf2cu_matrix_create(m, n, c.device, &a);
-    if (st != GF2CU_OK) return st;
+    // One cached device matrix per host thread: repeated calls on the same
+    // shape reuse HBM buffers and workspace instead of re-allocating.
+    struct Cache {
+        gf2cu_matrix* a = nullptr;
+        ~Cache() { gf2cu_matrix_destroy(a); }
+    };
+    thread_local Cache cache;
+    if (cache.a && (cache.a->m != m || cache.a->n != n || cache.a->device != c.device)) {
+        gf2cu_matrix_destroy(cache.a);
+        cache.a = nullptr;
+    }
+    if (!cache.a) {
+        st = gf2cu_matrix_create(m, n, c.device, &cache.a);
+        if (st != GF2CU_OK) return st;
+    }
+    gf2cu_matrix* a = cache.a;
     DeviceGuard g(c.device);
     cudaStream_t s = pick_stream(a, c.stream);
     const size_t W = a->W;
@@ -543,10 +558,7 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
         e = cudaMemcpy2DAsync(a->data, a->Wp * 8, packed.data(), W * 8, W * 8, m,
                               cudaMemcpyHostToDevice, s);
     }
-    if (e != cudaSuccess) {
-        gf2cu_matrix_destroy(a);
-        return cuda_fail(e, "upload");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "upload");
     c.stream = s;
     st = run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats);
     if (st == GF2CU_OK) {
@@ -573,7 +585,6 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
             stats->d2h_bytes = double(m) * W * 8;
         }
     }
-    gf2cu_matrix_destroy(a);
     return st;
 }
 
