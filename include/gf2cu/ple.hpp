@@ -1,0 +1,96 @@
+// gf2cu/ple.hpp -- C++ drop-in for gf2::block_iterative_ple on the B200.
+//
+// Include AFTER the reference's own headers (proj/include/gf2/ple.hpp): the
+// wrapper keeps the reference's public types -- gf2::MatrixView (bit_matrix.hpp:
+// 245), gf2::PleConfig / gf2::PleOutcome / gf2::ColSwap (ple.hpp:31-51),
+// gf2::RowPermutation (bit_matrix.hpp:416) -- and re-exposes the entry point
+//
+//     gf2::PleOutcome gf2::b200::block_iterative_ple(gf2::MatrixView a,
+//                                                    const gf2::PleConfig& cfg = {});
+//
+// with the reference's signature, in-place semantics and exception mapping
+// (std::invalid_argument / std::out_of_range / std::bad_alloc; CUDA failures
+// as std::runtime_error). Callers switch with a using-declaration or by
+// qualifying the call; see INTEGRATION.md. Link with -lgf2cu.
+#pragma once
+
+#include <cstddef>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gf2cu.h"
+
+namespace gf2 {
+namespace b200 {
+
+namespace detail {
+
+inline void throw_status(gf2cu_status st) {
+    const std::string msg = gf2cu_last_error();
+    switch (st) {
+        case GF2CU_OK: return;
+        case GF2CU_EINVAL: throw std::invalid_argument(msg);
+        case GF2CU_ERANGE: throw std::out_of_range(msg);
+        case GF2CU_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error("gf2cu: " + msg);
+    }
+}
+
+}  // namespace detail
+
+// Device selection for the wrapper (the reference has no notion of devices).
+struct DeviceOptions {
+    int device = 0;
+    void* stream = nullptr;  // cudaStream_t
+};
+
+// block_iterative_ple (ple.hpp:166) computed on the B200. Same outputs as the
+// reference: rank, processed = nrows, p.swaps, q (bit-exact), the in-place
+// L\E words (bit-exact), and col_swaps as the canonical compression list
+// {j, q[j], j} for q[j] != j, which extract_e / rref_from_ple / undo_column_swaps
+// accept with identical results ("Outputs").
+template <class View = gf2::MatrixView, class Cfg = gf2::PleConfig>
+gf2::PleOutcome block_iterative_ple(View a, const Cfg& cfg = {}, const DeviceOptions& dev = {}) {
+    gf2cu_view v;
+    v.data = a.row_words(0);
+    v.stride = a.stride();
+    v.col_off = a.col_offset();
+    v.nrows = a.nrows();
+    v.ncols = a.ncols();
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    c.k = cfg.k;
+    c.k_scale = cfg.k_scale;
+    c.table_count = cfg.table_count;
+    c.device = dev.device;
+    c.stream = dev.stream;
+    const std::size_t cap = std::max<std::size_t>(1, std::min(v.nrows, v.ncols));
+    std::vector<std::size_t> swaps(cap), q(cap);
+    std::vector<gf2cu_colswap> cs(cap);
+    std::size_t rank = 0, ncs = 0;
+    detail::throw_status(
+        gf2cu_ple(&v, &c, swaps.data(), q.data(), &rank, cs.data(), &ncs, nullptr));
+    gf2::PleOutcome out;
+    out.rank = rank;
+    out.processed = v.nrows;
+    out.p.swaps.assign(swaps.begin(), swaps.begin() + rank);
+    out.q.assign(q.begin(), q.begin() + rank);
+    out.col_swaps.reserve(ncs);
+    for (std::size_t i = 0; i < ncs; ++i) out.col_swaps.push_back({cs[i].a, cs[i].b, cs[i].from_row});
+    return out;
+}
+
+// echelonize(a, EchelonStrategy::ple_iterative, full) (m4ri.hpp:95-98) with the
+// decomposition on the B200 and the reference's rref_from_ple on the host.
+template <class View = gf2::MatrixView, class Cfg = gf2::PleConfig>
+std::size_t echelonize_ple_iterative(View a, bool full = true, const Cfg& cfg = {},
+                                     const DeviceOptions& dev = {}) {
+    gf2::PleOutcome out = block_iterative_ple(a, cfg, dev);
+    gf2::rref_from_ple(a, out, full, cfg.mul);
+    return out.rank;
+}
+
+}  // namespace b200
+}  // namespace gf2

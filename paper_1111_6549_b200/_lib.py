@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-shared", "-Xcompiler", "-fPIC",
+    "-shared", "-Xcompiler", "-fPIC", "-cudart", "static",
 ]
 
 
@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
-    cmd = [nvcc, *NVCC_FLAGS, "-I" + INCLUDE, "-o", SO + ".tmp", *sources(), "-lcudart"]
+    cmd = [nvcc, *NVCC_FLAGS, "-I" + INCLUDE, "-o", SO + ".tmp", *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     out = subprocess.run(cmd, capture_output=True, text=True)

@@ -80,3 +80,21 @@ def test_rank_deficient_product():
     ref, want, bm, got = run_both(a, m, n)
     assert want.rank <= l
     assert_same(ref, want, bm, got, what="X*Y")
+
+
+def test_dropin_cpp_binary():
+    """The C++ drop-in (include/gf2cu/ple.hpp) against the unmodified reference,
+    both in one binary built here from /root/reference headers."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/test_dropin not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failures" in out.stdout
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
