@@ -59,7 +59,9 @@ typedef struct {
     unsigned flags;        /* GF2CU_FLAG_*                                   */
 } gf2cu_cfg;
 
-#define GF2CU_FLAG_TIME_KERNELS 1u /* record CUDA events around each kernel  */
+#define GF2CU_FLAG_TIME_KERNELS 1u /* record CUDA events / device timestamps */
+#define GF2CU_FLAG_MULTI_KERNEL 2u /* one launch per phase instead of the
+                                      persistent cooperative kernel          */
 
 /* Mirrors gf2::ColSwap (ple.hpp:41-43). */
 typedef struct {
@@ -70,11 +72,13 @@ typedef struct {
 typedef struct {
     size_t steps;               /* 64-column panel steps executed               */
     size_t trailing_launches;   /* trailing_update launches that did work       */
-    double trailing_ms;         /* sum of trailing_update event durations       */
-    double panel_ms;            /* sum of panel_factor event durations          */
-    double coef_ms;             /* sum of panel_apply event durations           */
+    double trailing_ms;         /* trailing-update time (events or timestamps)  */
+    double panel_ms;            /* panel-factor time                            */
+    double coef_ms;             /* apply + stage time                           */
     double alg_bytes;           /* sum over steps of 16*(m-r-rb)*(W-w-1)        */
     double h2d_bytes, d2h_bytes;/* host<->device bytes moved by gf2cu_ple       */
+    double kernel_ms;           /* persistent kernel duration (CUDA events)     */
+    int driver;                 /* 1 = persistent cooperative, 0 = per phase    */
 } gf2cu_stats;
 
 /* Fills *cfg with the reference defaults (k=0, k_scale=0.75, table_count=4,

@@ -76,10 +76,12 @@ class gf2cu_colswap(C.Structure):
 class gf2cu_stats(C.Structure):
     _fields_ = [("steps", C.c_size_t), ("trailing_launches", C.c_size_t),
                 ("trailing_ms", C.c_double), ("panel_ms", C.c_double), ("coef_ms", C.c_double),
-                ("alg_bytes", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double)]
+                ("alg_bytes", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
+                ("kernel_ms", C.c_double), ("driver", C.c_int)]
 
 
 FLAG_TIME_KERNELS = 1
+FLAG_MULTI_KERNEL = 2
 
 # name -> (restype, argtypes): every symbol include/gf2cu.h declares.
 _sz, _szp = C.c_size_t, C.POINTER(C.c_size_t)

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <random>
@@ -18,6 +19,7 @@
 
 #include "gf2cu.h"
 #include "ple_kernels.cuh"
+#include "ple_persistent.cuh"
 
 using gf2cu::u32;
 using gf2cu::u64;
@@ -61,6 +63,8 @@ struct Workspace {
     u32* host_r = nullptr;       // pinned, mapped
     u32* host_r_dev = nullptr;   // device alias
     u64* hashes = nullptr;       // per-row checksum scratch
+    gf2cu::SyncState* sync = nullptr;
+    u64* phase_ns = nullptr;     // 8 stamps per step (persistent driver)
     std::vector<cudaEvent_t> ev;
 };
 
@@ -76,6 +80,8 @@ void free_ws(Workspace& w) {
     cudaFree(w.rhist);
     cudaFree(w.rbhist);
     cudaFree(w.hashes);
+    cudaFree(w.sync);
+    cudaFree(w.phase_ns);
     if (w.host_r) cudaFreeHost(w.host_r);
     for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
     w = Workspace{};
@@ -130,7 +136,9 @@ gf2cu_status ensure_ws(gf2cu_matrix* a) {
     w.W = a->W;
     CU_TRY(cudaMalloc(&w.perm, std::max<size_t>(1, m) * sizeof(u32)));
     CU_TRY(cudaMalloc(&w.pb, std::max<size_t>(1, m) * sizeof(u64)));
-    CU_TRY(cudaMalloc(&w.info, std::max<size_t>(1, m) * sizeof(ulonglong2)));
+    CU_TRY(cudaMalloc(&w.info, 2 * std::max<size_t>(1, m) * sizeof(ulonglong2)));
+    CU_TRY(cudaMalloc(&w.sync, sizeof(gf2cu::SyncState)));
+    CU_TRY(cudaMalloc(&w.phase_ns, (8 * (a->W + 1) + 8 + 64 * 5) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.stage, 64 * wpad8(a->W) * sizeof(u64)));
     CU_TRY(cudaMemset(w.stage, 0, 64 * wpad8(a->W) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.state, sizeof(gf2cu::StepState)));
@@ -184,6 +192,8 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     p.rhist = ws.rhist;
     p.rbhist = ws.rbhist;
     p.host_r = ws.host_r_dev;
+    p.sync = ws.sync;
+    p.phase_ns = timing ? ws.phase_ns : nullptr;
     p.m = (u32)m;
     p.n = (u32)n;
     p.W = (u32)W;
@@ -194,13 +204,17 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         CU_TRY(cudaFuncSetAttribute(gf2cu::trailing_update_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     gf2cu::kTableBytes));
+        CU_TRY(cudaFuncSetAttribute(gf2cu::ple_persistent_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    gf2cu::kTableBytes));
         attr_set[a->device] = true;
     }
     const int sms = num_sms(a->device);
     const int apply_grid = sms * 4;
+    const bool multi = cfg && (cfg->flags & GF2CU_FLAG_MULTI_KERNEL);
 
     if (timing) {
-        const size_t need = 6 * (W + 1);
+        const size_t need = 6 * (W + 1) + 2;
         while (ws.ev.size() < need) {
             cudaEvent_t e;
             CU_TRY(cudaEventCreate(&e));
@@ -213,36 +227,61 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     gf2cu::ple_init_kernel<<<sms * 4, 256, 0, s>>>(p);
     CU_TRY(cudaGetLastError());
 
-    // Host stays at most kLag steps ahead of the device so that it notices
-    // r == m early (wide matrices) without stalling the stream.
-    constexpr size_t kLag = 6;
-    std::vector<cudaEvent_t> step_ev(kLag, nullptr);
-    for (auto& e : step_ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-
     size_t steps = 0;
-    for (size_t w = 0; w < W; ++w) {
-        if (w >= kLag) {
-            CU_TRY(cudaEventSynchronize(step_ev[w % kLag]));
-            if (*reinterpret_cast<volatile u32*>(ws.host_r) >= m) break;
-        }
-        cudaEvent_t* E = timing ? &ws.ev[6 * w] : nullptr;
+    float kernel_ms = 0.f;
+    if (!multi) {
+        // ---- persistent cooperative driver: one launch for all panels ----
+        CU_TRY(cudaMemsetAsync(ws.sync, 0, sizeof(gf2cu::SyncState), s));
+        if (timing) CU_TRY(cudaMemsetAsync(ws.phase_ns, 0, 8 * (W + 1) * sizeof(u64), s));
+        int per_sm = 0;
+        CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, gf2cu::ple_persistent_kernel, gf2cu::kTrailThreads, gf2cu::kTableBytes));
+        if (per_sm < 1) return fail(GF2CU_ECUDA, "persistent kernel does not fit on an SM");
+        const int grid = sms;  // one CTA per SM: CTA 0 panels, the rest update
+        u32 nsteps = (u32)W;
+        void* args[] = {&p, &nsteps};
+        cudaEvent_t* E = timing ? &ws.ev[6 * (W + 1)] : nullptr;
         if (E) cudaEventRecord(E[0], s);
-        gf2cu::panel_factor_kernel<<<1, gf2cu::kPanelThreads, 0, s>>>(p, (u32)w);
+        CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_persistent_kernel, dim3(grid),
+                                           dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
         if (E) cudaEventRecord(E[1], s);
-        if (E) cudaEventRecord(E[2], s);
-        gf2cu::panel_apply_kernel<<<apply_grid, gf2cu::kApplyThreads, 0, s>>>(p, (u32)w);
-        if (E) cudaEventRecord(E[3], s);
-        if (w + 1 < W) {
-            if (E) cudaEventRecord(E[4], s);
-            gf2cu::trailing_update_kernel<<<sms, gf2cu::kTrailThreads, gf2cu::kTableBytes, s>>>(
-                p, (u32)w);
-            if (E) cudaEventRecord(E[5], s);
+        gf2cu::SyncState sy{};
+        CU_TRY(cudaMemcpyAsync(&sy, ws.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaStreamSynchronize(s));
+        if (sy.error) return fail(GF2CU_ECUDA, "persistent PLE kernel watchdog tripped");
+        steps = sy.panel_done;
+        if (E) cudaEventElapsedTime(&kernel_ms, E[0], E[1]);
+    } else {
+        // ---- one launch per phase ----
+        // Host stays at most kLag steps ahead of the device so that it notices
+        // r == m early (wide matrices) without stalling the stream.
+        constexpr size_t kLag = 6;
+        std::vector<cudaEvent_t> step_ev(kLag, nullptr);
+        for (auto& e : step_ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (size_t w = 0; w < W; ++w) {
+            if (w >= kLag) {
+                CU_TRY(cudaEventSynchronize(step_ev[w % kLag]));
+                if (*reinterpret_cast<volatile u32*>(ws.host_r) >= m) break;
+            }
+            cudaEvent_t* E = timing ? &ws.ev[6 * w] : nullptr;
+            if (E) cudaEventRecord(E[0], s);
+            gf2cu::panel_factor_kernel<<<1, gf2cu::kPanelThreads, 0, s>>>(p, (u32)w);
+            if (E) cudaEventRecord(E[1], s);
+            if (E) cudaEventRecord(E[2], s);
+            gf2cu::panel_apply_kernel<<<apply_grid, gf2cu::kApplyThreads, 0, s>>>(p, (u32)w);
+            if (E) cudaEventRecord(E[3], s);
+            if (w + 1 < W) {
+                if (E) cudaEventRecord(E[4], s);
+                gf2cu::trailing_update_kernel<<<sms, gf2cu::kTrailThreads, gf2cu::kTableBytes, s>>>(
+                    p, (u32)w);
+                if (E) cudaEventRecord(E[5], s);
+            }
+            CU_TRY(cudaGetLastError());
+            CU_TRY(cudaEventRecord(step_ev[w % kLag], s));
+            ++steps;
         }
-        CU_TRY(cudaGetLastError());
-        CU_TRY(cudaEventRecord(step_ev[w % kLag], s));
-        ++steps;
+        for (auto& e : step_ev) cudaEventDestroy(e);
     }
-    for (auto& e : step_ev) cudaEventDestroy(e);
 
     // rank and histories
     gf2cu::StepState fin{};
@@ -290,7 +329,39 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         }
         stats->alg_bytes = bytes;
         stats->trailing_launches = launches;
-        if (timing) {
+        stats->kernel_ms = kernel_ms;
+        stats->driver = multi ? 0 : 1;
+        if (timing && !multi) {
+            std::vector<u64> ph(8 * steps);
+            CU_TRY(cudaMemcpy(ph.data(), ws.phase_ns, ph.size() * sizeof(u64), cudaMemcpyDeviceToHost));
+            double tp = 0, tc = 0, tt = 0;
+            for (size_t w = 0; w < steps; ++w) {
+                const u64* x = &ph[8 * w];
+                if (x[1] > x[0]) tp += (x[1] - x[0]) * 1e-6;
+                if (x[3] > x[2]) tc += (x[3] - x[2]) * 1e-6;
+                if (x[5] > x[3]) tt += (x[5] - x[3]) * 1e-6;
+            }
+            stats->panel_ms = tp;
+            stats->coef_ms = tc;
+            stats->trailing_ms = tt;
+            if (const char* path = std::getenv("GF2CU_DUMP_PHASES")) {
+                if (FILE* f = std::fopen(path, "w")) {
+                    std::fprintf(f, "w r rb p0 p1 a0 t0 cap1 t1 pl0 pl1\n");
+                    for (size_t w = 0; w < steps; ++w) {
+                        const u64* x = &ph[8 * w];
+                        std::fprintf(f, "%zu %u %u %llu %llu %llu %llu %llu %llu %llu %llu\n", w, rh[w],
+                                     rbh[w], x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+                    }
+                    std::vector<u64> dbg(64 * 5);
+                    cudaMemcpy(dbg.data(), ws.phase_ns + 8 * W + 8, dbg.size() * 8, cudaMemcpyDeviceToHost);
+                    for (int j = 0; j < 64; ++j)
+                        std::fprintf(f, "# %d %llu %llu %llu %llu %llu\n", j, dbg[5 * j], dbg[5 * j + 1],
+                                     dbg[5 * j + 2], dbg[5 * j + 3], dbg[5 * j + 4]);
+                    std::fclose(f);
+                }
+            }
+        }
+        if (timing && multi) {
             double tp = 0, tc = 0, tt = 0;
             for (size_t w = 0; w < steps; ++w) {
                 float ms = 0;

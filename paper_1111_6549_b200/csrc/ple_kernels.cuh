@@ -8,22 +8,26 @@
 // (the reference's row index after its swaps) to a physical row, and the
 // final untile pass gathers rows back into position order.
 //
-// One 64-column panel (= word column w) per step:
-//   panel_factor    (1 CTA)  pivot search on the panel words of rows >= r:
+// One 64-column panel (= word column w) per step, three phases:
+//   panel_factor   (1 CTA)   pivot search on the panel words of rows >= r:
 //                            transposed single-warp elimination on a 128-row
 //                            window, CTA-wide scan of the other rows on a
 //                            window miss. Replaces partial_ple (ple.hpp:57-130)
 //                            and the swap replay (ple.hpp:187-188).
-//   panel_apply     (grid)   per row: multipliers c and the combination d of
+//   apply          (grid)    per row: multipliers c and the combination d of
 //                            RAW pivot rows that finishes its tail (d folds the
 //                            unit-lower TRSM of ple.hpp:191-193 into the
 //                            update); writes the compressed multipliers
 //                            (ple.hpp:232-236); stages raw pivot-row tails.
-//   trailing_update (grid)   8 Gray-code tables x 256 entries per 64-byte
+//   trailing       (grid)    8 Gray-code tables x 256 entries per 64-byte
 //                            tile in shared memory (make_table,
 //                            gray_code.hpp:88-134), then tail ^= sum_g
 //                            T_g[byte_g(d)] for every row >= r (ple.hpp:
 //                            208-229), 128-bit loads/stores, software-pipelined.
+//
+// The phases are device functions used by two drivers: one launch per phase
+// (ple_*_kernel), and a persistent cooperative kernel (ple_persistent.cuh)
+// that overlaps panel s+1 with the trailing update of step s.
 #pragma once
 
 #include <cstdint>
@@ -33,10 +37,10 @@ namespace gf2cu {
 using u64 = unsigned long long;
 using u32 = unsigned int;
 
-constexpr int kPanelThreads = 256;     // panel_factor CTA
+constexpr int kPanelThreads = 256;     // panel_factor CTA (multi-kernel driver)
 constexpr int kWin = 128;              // window rows (two 64-bit halves)
-constexpr int kApplyThreads = 256;     // panel_apply CTA
-constexpr int kTrailThreads = 512;     // trailing_update CTA
+constexpr int kApplyThreads = 256;     // apply CTA (multi-kernel driver)
+constexpr int kTrailThreads = 512;     // trailing CTA
 constexpr int kTileWords = 8;          // 64-byte column tile
 constexpr int kTables = 8;             // 8 tables of 8 coefficient bits
 constexpr int kTableBytes = kTables * 256 * kTileWords * 8;  // 128 KiB
@@ -55,6 +59,17 @@ struct PanelOut {
     u32 qb[64];  // pivot t: column within the panel word
 };
 
+// Cross-CTA counters of the persistent driver (zeroed before each launch).
+struct SyncState {
+    u32 panel_done;  // steps whose panel factorization is published
+    u32 cap_count;   // worker arrivals after the look-ahead tile
+    u32 t_count;     // worker arrivals after the whole trailing update
+    u32 st_count;    // worker arrivals after staging
+    u32 error;       // watchdog tripped
+    u32 pad[3];
+    u64 stamps[8];   // debug timestamps
+};
+
 struct Params {
     u64* mat;        // tile-major, Wpad8/8 tiles x m rows x 8 words
     u32* perm;       // position -> physical row
@@ -68,9 +83,12 @@ struct Params {
     u32* rhist;      // r at the start of each step
     u32* rbhist;     // rb of each step
     volatile u32* host_r;  // mapped pinned mirror of (r + rb), may be null
+    SyncState* sync;
+    u64* phase_ns;   // per-step phase timestamps (persistent driver), may be null
     u32 m, n, W, Wpad8;
 };
 
+// ------------------------------------------------------------------ helpers
 __device__ __forceinline__ u64 low_mask64(int k) {
     return k >= 64 ? ~0ull : ((1ull << k) - 1ull);
 }
@@ -85,6 +103,44 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 
 __device__ __forceinline__ u64 shfl64(u64 v, int src) {
     return __shfl_sync(0xffffffffu, v, src);
+}
+
+// Loads of data another CTA of the same (persistent) grid may have written:
+// L2-coherent, never a stale L1 line.
+__device__ __forceinline__ u64 ldcg(const u64* p) { return __ldcg(p); }
+__device__ __forceinline__ u32 ldcg(const u32* p) { return __ldcg(p); }
+__device__ __forceinline__ ulonglong2 ldcg(const ulonglong2* p) { return __ldcg(p); }
+
+__device__ __forceinline__ u64 globaltimer() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ u32 ld_acquire(const u32* a) {
+    u32 v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_release_add(u32* a, u32 v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+// Spin (one thread) until *a >= target. Watchdog: after ~4 s sets sync->error
+// and returns false instead of hanging the GPU.
+__device__ __forceinline__ bool spin_geq(const u32* a, u32 target, u32* err) {
+    if (ld_acquire(a) >= target) return true;
+    const u64 t0 = globaltimer();
+    for (;;) {
+        if (ld_acquire(a) >= target) return true;
+        if (*(volatile u32*)err) return false;
+        if (globaltimer() - t0 > 4000000000ull) {
+            atomicExch(err, 1u);
+            return false;
+        }
+        __nanosleep(64);
+    }
 }
 
 // 32x32 bit transpose across a warp: on return lane l bit b = input lane b
@@ -145,31 +201,40 @@ __global__ void ple_init_kernel(Params p) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// panel_factor
-// ---------------------------------------------------------------------------
+// ===========================================================================
+// Phase 1: panel factorization (one CTA)
+// ===========================================================================
 struct PanelShared {
     u64 E[64], D[64];
     u32 q[64];
-    u64 wraw[kWin];
+    u32 sw[64];          // pivot t's position offset (the LAPACK swap)
+    u64 wraw[kWin];      // window raw panel words / physical rows, as loaded
     u32 wphys[kWin];
+    u64 oraw[64];        // raw word / physical row of pivots taken from outside
+    u32 ophys[64];
+    // per-pivot exchange among the 4 window warps (double-buffered by parity)
+    __align__(16) u32 bal[2][4];
+    __align__(16) ulonglong2 cand[2][4];  // {red, acc} of each warp's first candidate row
+    u32 corg[2][4];
+    ulonglong2 trow[2];     // {red, acc} of the row at position t
+    u32 torg[2];
     int cmd;  // 0 = scan, 1 = exit
     int t, j;
-    u64 warp_best[kPanelThreads / 32];
+    u64 warp_best[32];
     u64 best;  // (first column << 32) | offset
     u64 o_red, o_acc, o_raw;
     u32 o_phys;
     u32 r;
 };
 
-// All kPanelThreads threads: scan positions r + [nwin, nrem) reducing each raw
-// panel word by the t pivots found so far; sh.best = the smallest
-// (first set column >= j, offset), with the winner's reduced state in sh.o_*.
-__device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem) {
+// All `nthr` threads: scan positions r + [nwin, nrem) reducing each raw panel
+// word by the t pivots found so far; sh.best = the smallest (first set column
+// >= j, offset), with the winner's reduced state in sh.o_*.
+__device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem, int nthr) {
     const int t = sh.t, j = sh.j;
     u64 best = ~0ull, b_red = 0, b_acc = 0;
-    for (u32 off = nwin + threadIdx.x; off < nrem; off += kPanelThreads) {
-        u64 v = p.pb[r + off], a = 0;
+    for (u32 off = nwin + threadIdx.x; off < nrem; off += nthr) {
+        u64 v = ldcg(p.pb + r + off), a = 0;
         for (int s = 0; s < t; ++s) {
             const u64 msk = 0ull - ((v >> sh.q[s]) & 1ull);
             v ^= sh.E[s] & msk;
@@ -193,21 +258,21 @@ __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u3
     }
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) sh.warp_best[wid] = wb;
-    named_bar(2, kPanelThreads);
+    named_bar(2, nthr);
     if (threadIdx.x == 0) {
         u64 b = ~0ull;
-        for (int k = 0; k < kPanelThreads / 32; ++k) b = sh.warp_best[k] < b ? sh.warp_best[k] : b;
+        for (int k = 0; k < nthr / 32; ++k) b = sh.warp_best[k] < b ? sh.warp_best[k] : b;
         sh.best = b;
     }
-    named_bar(2, kPanelThreads);
+    named_bar(2, nthr);
     if (best != ~0ull && best == sh.best) {
         const u32 off = (u32)(best & 0xffffffffu);
         sh.o_red = b_red;
         sh.o_acc = b_acc;
-        sh.o_raw = p.pb[r + off];
-        sh.o_phys = p.perm[r + off];
+        sh.o_raw = ldcg(p.pb + r + off);
+        sh.o_phys = ldcg(p.perm + r + off);
     }
-    named_bar(2, kPanelThreads);
+    named_bar(2, nthr);
 }
 
 // Transposed window state of warp 0: lane l owns panel columns l and l+32
@@ -217,8 +282,9 @@ struct Col128 {
     u64 lo, hi;
 };
 
-// Row swap t <-> p on one column mask, then the elimination XOR if `cond`
-// holds for the pivot row's bit (bit t after the swap, returned).
+// Row swap t <-> p on one column mask, then the elimination XOR of the rows
+// R when the pivot row holds a 1 here (xor_if_set) or unconditionally (force).
+// Returns the pivot row's bit (bit t after the swap).
 __device__ __forceinline__ bool swap_elim(Col128& x, u64 tm, u64 pl, u64 ph, int t, u64 Rlo,
                                           u64 Rhi, bool xor_if_set, bool force) {
     const u64 bt = (x.lo >> t) & 1ull;
@@ -233,11 +299,17 @@ __device__ __forceinline__ bool swap_elim(Col128& x, u64 tm, u64 pl, u64 ph, int
     return piv;
 }
 
-__global__ void __launch_bounds__(kPanelThreads, 1) panel_factor_kernel(Params p, u32 w) {
-    __shared__ PanelShared sh;
+// The panel step w. Called by every thread of ONE CTA of `nthr` >= 256
+// threads. Warps 0-3 hold the 128-row window, one row per thread (`red` =
+// the row's panel word reduced by the pivots so far, `acc` = its combination
+// of raw pivot rows); per pivot they exchange one ballot and one candidate
+// row per warp through shared memory behind a single 128-thread named
+// barrier. The other warps serve window-miss scans. Returns rb in all threads.
+__device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nthr) {
     if (threadIdx.x == 0) {
-        const StepState st = *p.state;
-        sh.r = st.r + st.rb;
+        const volatile StepState* vs = p.state;
+        sh.r = vs->r + vs->rb;
+        sh.t = 0;
     }
     __syncthreads();
     const u32 r = sh.r;
@@ -252,243 +324,259 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_factor_kernel(Params p
             *p.host_r = r;
             __threadfence_system();
         }
-        return;
+        __syncthreads();
+        return 0;
     }
     const u32 nrem = p.m - r;
     const u32 nwin = nrem < (u32)kWin ? nrem : (u32)kWin;
     const int jmax = (int)min(64u, p.n - 64u * w);
 
-    if (threadIdx.x >= 32) {
+    if (threadIdx.x >= kWin) {
         for (;;) {
-            named_bar(1, kPanelThreads);
+            named_bar(1, nthr);
             if (sh.cmd != 0) break;
-            panel_scan(p, sh, r, nwin, nrem);
+            panel_scan(p, sh, r, nwin, nrem, nthr);
         }
-        return;
-    }
-
-    // ---- warp 0 ----
-    const int lane = threadIdx.x;
-    u32 part[4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const u32 off = 32u * i + lane;
-        u64 v = 0ull;
-        if (off < nwin) {
-            v = p.pb[r + off];
-            sh.wraw[off] = v;
-            sh.wphys[off] = p.perm[r + off];
+    } else {
+        // ---- window warps: thread `me` holds window row `me` ----
+        const u32 me = threadIdx.x, lane = me & 31u, wid = me >> 5;
+        const bool inwin = me < nwin;
+        u64 red = 0ull, acc = 0ull;
+        u32 org = me;  // window offset of the row this slot holds
+        if (inwin) {
+            red = ldcg(p.pb + r + me);
+            sh.wraw[me] = red;
+            sh.wphys[me] = ldcg(p.perm + r + me);
         }
-        part[i][0] = transpose32((u32)v);
-        part[i][1] = transpose32((u32)(v >> 32));
-    }
-    Col128 M[2], A[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        M[h].lo = (u64)part[0][h] | ((u64)part[1][h] << 32);
-        M[h].hi = (u64)part[2][h] | ((u64)part[3][h] << 32);
-        A[h].lo = 0ull;
-        A[h].hi = 0ull;
-    }
-    const u64 winlo = nwin >= 64 ? ~0ull : low_mask64((int)nwin);
-    const u64 winhi = nwin > 64 ? low_mask64((int)nwin - 64) : 0ull;
-
-    int t = 0;
-    int out_next = nwin < nrem ? 0 : 64;
-    for (int j = 0; j < jmax && (u32)t < nrem; ++j) {
-        const int hj = j >> 5, oj = j & 31;
-        const u64 clo = shfl64(hj ? M[1].lo : M[0].lo, oj);
-        const u64 chi = shfl64(hj ? M[1].hi : M[0].hi, oj);
-        const u64 flo = clo & winlo & ~low_mask64(t);
-        const u64 fhi = chi & winhi;
-        const u64 tm = 1ull << t;
-        const u64 above_t = ~low_mask64(t + 1);
-        if (flo | fhi) {
-            const int pidx = flo ? (__ffsll((long long)flo) - 1) : (64 + __ffsll((long long)fhi) - 1);
-            const u64 pl = pidx < 64 ? (1ull << pidx) : 0ull;
-            const u64 ph = pidx >= 64 ? (1ull << (pidx - 64)) : 0ull;
-            // rows > t holding column j after the swap
-            const u64 btj = 0ull - ((clo >> t) & 1ull);
-            const u64 Rlo = ((clo & ~pl) | (btj & pl)) & above_t;
-            const u64 Rhi = (chi & ~ph) | (btj & ph);
-            u32 eb[2], db[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int c = 32 * h + lane;
-                const bool pe = swap_elim(M[h], tm, pl, ph, t, Rlo, Rhi, c > j, false);
-                const bool pd = swap_elim(A[h], tm, pl, ph, t, Rlo, Rhi, c < t, c == t);
-                eb[h] = __ballot_sync(0xffffffffu, pe && c > j);
-                db[h] = __ballot_sync(0xffffffffu, pd && c < t);
+        named_bar(3, kWin);
+        if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 6] = globaltimer();
+        int t = 0;
+        int out_next = nwin < nrem ? 0 : 64;
+        for (int j = 0; j < jmax && (u32)t < nrem; ++j) {
+            const int par = j & 1;
+            // candidates: live rows (position >= t) holding column j
+            const bool b = inwin & (me >= (u32)t) & (((red >> j) & 1ull) != 0ull);
+            const u32 bal = __ballot_sync(0xffffffffu, b);
+            if (lane == 0) sh.bal[par][wid] = bal;
+            if (b & (lane == (u32)(__ffs(bal) - 1))) {
+                sh.cand[par][wid] = make_ulonglong2(red, acc);
+                sh.corg[par][wid] = org;
             }
-            if (lane == 0) {
-                sh.E[t] = (u64)eb[0] | ((u64)eb[1] << 32);
-                sh.D[t] = ((u64)db[0] | ((u64)db[1] << 32)) | tm;
-                sh.q[t] = (u32)j;
-                p.swaps[r + t] = r + (u32)pidx;
-                p.qcol[r + t] = 64u * w + (u32)j;
-                if (pidx != t) {
-                    const u64 a = sh.wraw[t];
-                    sh.wraw[t] = sh.wraw[pidx];
-                    sh.wraw[pidx] = a;
-                    const u32 b = sh.wphys[t];
-                    sh.wphys[t] = sh.wphys[pidx];
-                    sh.wphys[pidx] = b;
+            if (me == (u32)t) {
+                sh.trow[par] = make_ulonglong2(red, acc);
+                sh.torg[par] = org;
+            }
+            named_bar(3, kWin);
+            // everything the step needs is loaded at once (independent LDS)
+            const uint4 bw = *reinterpret_cast<const uint4*>(sh.bal[par]);
+            const ulonglong2 c0 = sh.cand[par][0], c1 = sh.cand[par][1];
+            const ulonglong2 c2 = sh.cand[par][2], c3 = sh.cand[par][3];
+            const uint4 co = *reinterpret_cast<const uint4*>(sh.corg[par]);
+            const ulonglong2 tr = sh.trow[par];
+            const u32 tro = sh.torg[par];
+            const int pw = bw.x ? 0 : bw.y ? 1 : bw.z ? 2 : bw.w ? 3 : -1;
+            u64 pred, pacc;
+            u32 P, porg;
+            if (pw >= 0) {
+                const u32 bw_sel = pw == 0 ? bw.x : pw == 1 ? bw.y : pw == 2 ? bw.z : bw.w;
+                P = 32u * (u32)pw + (u32)(__ffs(bw_sel) - 1);
+                pred = pw == 0 ? c0.x : pw == 1 ? c1.x : pw == 2 ? c2.x : c3.x;
+                pacc = pw == 0 ? c0.y : pw == 1 ? c1.y : pw == 2 ? c2.y : c3.y;
+                porg = pw == 0 ? co.x : pw == 1 ? co.y : pw == 2 ? co.z : co.w;
+                // row swap t <-> P: the old row t moves into slot P
+                const bool mv = (me == P) & (P != (u32)t);
+                red = mv ? tr.x : red;
+                acc = mv ? tr.y : acc;
+                org = mv ? tro : org;
+            } else {
+                // ---- window miss: the remaining rows decide ----
+                if (j < out_next) continue;  // no row outside has this column
+                if (me == 0) {
+                    sh.cmd = 0;
+                    sh.t = t;
+                    sh.j = j;
+                }
+                named_bar(1, nthr);
+                panel_scan(p, sh, r, nwin, nrem, nthr);
+                const u64 best = sh.best;
+                if (best == ~0ull) {
+                    out_next = 64;
+                    continue;
+                }
+                out_next = (int)(best >> 32);
+                if (out_next != j) continue;  // column j has no pivot anywhere
+                // pivot from outside the window: it takes position t; the
+                // window row t moves to the pivot's old position P
+                P = (u32)(best & 0xffffffffu);
+                pred = sh.o_red;
+                pacc = sh.o_acc;
+                porg = 0x80000000u | (u32)t;
+                if (me == (u32)t) {
+                    p.pb[r + P] = sh.wraw[org];
+                    p.perm[r + P] = sh.wphys[org];
+                    sh.oraw[t] = sh.o_raw;
+                    sh.ophys[t] = sh.o_phys;
                 }
             }
-            __syncwarp();
+            if (me == (u32)t) org = porg;  // the pivot's slot records its row
+            const u64 Et = pred & ~low_mask64(j + 1);
+            const u64 tm = 1ull << t;
+            const u64 Dt = pacc ^ tm;
+            const u64 msk = 0ull - (u64)(inwin & (me > (u32)t) & (((red >> j) & 1ull) != 0ull));
+            red ^= Et & msk;
+            acc ^= Dt & msk;
+            if (me == 0) {
+                sh.E[t] = Et;
+                sh.D[t] = Dt;
+                sh.q[t] = (u32)j;
+                sh.sw[t] = P;
+            }
             ++t;
-            continue;
         }
-        // ---- window miss: the remaining rows decide ----
-        if (j < out_next) continue;  // no row outside has this column
-        if (lane == 0) {
-            sh.cmd = 0;
+        if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 7] = globaltimer();
+        // the permuted window: raw panel word and physical row per position
+        named_bar(3, kWin);
+        u64 rw = 0ull;
+        u32 ph = 0u;
+        if (inwin) {
+            const bool out = (org & 0x80000000u) != 0u;
+            rw = out ? sh.oraw[org & 63u] : sh.wraw[org & 127u];
+            ph = out ? sh.ophys[org & 63u] : sh.wphys[org & 127u];
+        }
+        if (me == 0) {
+            sh.cmd = 1;
             sh.t = t;
-            sh.j = j;
         }
-        __syncwarp();
-        named_bar(1, kPanelThreads);
-        panel_scan(p, sh, r, nwin, nrem);
-        const u64 best = sh.best;
-        if (best == ~0ull) {
-            out_next = 64;
-            continue;
+        named_bar(1, nthr);  // release the helpers
+        if (inwin) {
+            p.pb[r + me] = rw;
+            p.perm[r + me] = ph;
         }
-        out_next = (int)(best >> 32);
-        if (out_next != j) continue;  // column j has no pivot anywhere
-        // pivot from outside the window: it replaces window row t, which moves
-        // to the pivot's old position
-        const u32 P = (u32)(best & 0xffffffffu);
-        const u64 o_red = sh.o_red, o_acc = sh.o_acc;
-        const u64 Rlo = clo & winlo & above_t;
-        const u64 Rhi = chi & winhi;
-        u32 eb[2], db[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int c = 32 * h + lane;
-            const bool be = (o_red >> c) & 1ull;
-            const bool bd = (o_acc >> c) & 1ull;
-            M[h].lo = (M[h].lo & ~tm) | (be ? tm : 0ull);
-            A[h].lo = (A[h].lo & ~tm) | (bd ? tm : 0ull);
-            const u64 cme = 0ull - (u64)(be && c > j);
-            M[h].lo ^= cme & Rlo;
-            M[h].hi ^= cme & Rhi;
-            const u64 cmd = 0ull - (u64)((bd && c < t) || c == t);
-            A[h].lo ^= cmd & Rlo;
-            A[h].hi ^= cmd & Rhi;
-            eb[h] = __ballot_sync(0xffffffffu, be && c > j);
-            db[h] = __ballot_sync(0xffffffffu, bd && c < t);
-        }
-        if (lane == 0) {
-            sh.E[t] = (u64)eb[0] | ((u64)eb[1] << 32);
-            sh.D[t] = ((u64)db[0] | ((u64)db[1] << 32)) | tm;
-            sh.q[t] = (u32)j;
-            p.swaps[r + t] = r + P;
-            p.qcol[r + t] = 64u * w + (u32)j;
-            p.pb[r + P] = sh.wraw[t];
-            p.perm[r + P] = sh.wphys[t];
-            sh.wraw[t] = sh.o_raw;
-            sh.wphys[t] = sh.o_phys;
-        }
-        __syncwarp();
-        ++t;
     }
-    if (lane == 0) sh.cmd = 1;
-    __syncwarp();
-    named_bar(1, kPanelThreads);
-
-    for (u32 off = lane; off < nwin; off += 32) {
-        p.pb[r + off] = sh.wraw[off];
-        p.perm[r + off] = sh.wphys[off];
-    }
-    for (int k = lane; k < t; k += 32) {
+    __syncthreads();
+    const u32 t = (u32)sh.t;
+    for (u32 k = threadIdx.x; k < t; k += nthr) {
         p.pout->E[k] = sh.E[k];
         p.pout->D[k] = sh.D[k];
         p.pout->qb[k] = sh.q[k];
+        p.swaps[r + k] = r + sh.sw[k];
+        p.qcol[r + k] = 64u * w + sh.q[k];
     }
-    if (lane == 0) {
-        p.state->rb = (u32)t;
-        p.rbhist[w] = (u32)t;
+    if (threadIdx.x == 0) {
+        p.state->rb = t;
+        p.rbhist[w] = t;
         if (p.host_r) {
-            *p.host_r = r + (u32)t;
+            *p.host_r = r + t;
             __threadfence_system();
         }
     }
+    __syncthreads();
+    return t;
 }
 
-// ---------------------------------------------------------------------------
-// panel_apply: multipliers + combination per row, compressed write, staging.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kApplyThreads) panel_apply_kernel(Params p, u32 w) {
-    __shared__ u64 sE[64], sD[64];
-    __shared__ u32 sq[64];
-    const StepState st = *p.state;
-    const u32 r = st.r, rb = st.rb;
-    if (r >= p.m) return;
+__global__ void __launch_bounds__(kPanelThreads, 1) panel_factor_kernel(Params p, u32 w) {
+    __shared__ PanelShared sh;
+    panel_factor_body(p, w, sh, kPanelThreads);
+}
+
+// ===========================================================================
+// Phase 2: apply (rows) and staging (pivot rows)
+// ===========================================================================
+struct ApplyShared {
+    u64 E[64], D[64];
+    u32 q[64];
+};
+
+__device__ __forceinline__ void apply_load(const Params& p, ApplyShared& s, u32 rb) {
     for (u32 k = threadIdx.x; k < 64; k += blockDim.x) {
         const bool v = k < rb;
-        sE[k] = v ? p.pout->E[k] : 0ull;
-        sD[k] = v ? p.pout->D[k] : 0ull;
-        sq[k] = v ? p.pout->qb[k] : 0u;
+        s.E[k] = v ? ldcg(&p.pout->E[k]) : 0ull;
+        s.D[k] = v ? ldcg(&p.pout->D[k]) : 0ull;
+        s.q[k] = v ? ldcg(&p.pout->qb[k]) : 0u;
     }
-    __syncthreads();
+}
 
-    const u32 gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const u32 gsize = gridDim.x * blockDim.x;
+// Positions [lo, hi) (all >= r): multipliers, combination, compressed write.
+__device__ __forceinline__ void apply_rows(const Params& p, const ApplyShared& s, u32 w, u32 r,
+                                           u32 rb, u32 lo, u32 hi, u32 tid, u32 nthr) {
     const u32 w0 = r >> 6, b0 = r & 63;
-    for (u32 pos = r + gtid; pos < p.m; pos += gsize) {
-        u64 v = p.pb[pos], a = 0, c = 0;
-        const u32 ph = p.perm[pos];
+    for (u32 pos = lo + tid; pos < hi; pos += nthr) {
+        u64 v = ldcg(p.pb + pos), a = 0, c = 0;
+        const u32 ph = ldcg(p.perm + pos);
         const u32 off = pos - r;
         const u32 tl = off < rb ? off : rb;
         // branch-free forward elimination against the panel's pivots
 #pragma unroll 8
-        for (u32 s = 0; s < 64; ++s) {
-            if (s >= tl) break;
-            const u64 bit = (v >> sq[s]) & 1ull;
+        for (u32 k = 0; k < 64; ++k) {
+            if (k >= tl) break;
+            const u64 bit = (v >> s.q[k]) & 1ull;
             const u64 msk = 0ull - bit;
-            v ^= sE[s] & msk;
-            a ^= sD[s] & msk;
-            c |= bit << s;
+            v ^= s.E[k] & msk;
+            a ^= s.D[k] & msk;
+            c |= bit << k;
         }
         u64 epart = 0;
         if (off < rb) {
             c |= 1ull << off;
-            epart = v & ~low_mask64((int)sq[off] + 1);
+            epart = v & ~low_mask64((int)s.q[off] + 1);
         }
         p.info[pos] = make_ulonglong2(a, (u64)ph);
-        const u64 lo = c << b0;
-        const u64 hi = b0 ? (c >> (64 - b0)) : 0ull;
+        const u64 clo = c << b0;
+        const u64 chi = b0 ? (c >> (64 - b0)) : 0ull;
         if (w0 == w) {
-            *tword(p.mat, p.m, ph, w) = lo | epart;
+            *tword(p.mat, p.m, ph, w) = clo | epart;
         } else {
-            *tword(p.mat, p.m, ph, w0) |= lo;
+            u64* x0 = tword(p.mat, p.m, ph, w0);
+            *x0 = ldcg(x0) | clo;
             if (w0 + 1 == w) {
-                *tword(p.mat, p.m, ph, w) = hi | epart;
+                *tword(p.mat, p.m, ph, w) = chi | epart;
             } else {
-                if (hi) *tword(p.mat, p.m, ph, w0 + 1) |= hi;
+                if (chi) {
+                    u64* x1 = tword(p.mat, p.m, ph, w0 + 1);
+                    *x1 = ldcg(x1) | chi;
+                }
                 *tword(p.mat, p.m, ph, w) = epart;
             }
         }
     }
+}
 
-    // stage raw pivot-row tails, tiles [x0/8, Wpad8/8): stage[(T*64 + t)*8 + k]
-    if (w + 1 < p.W && rb > 0) {
-        const u32 x0 = (w + 1) & ~7u;
-        const u32 span2 = (p.Wpad8 - x0) >> 1;  // 16-byte units per row
-        const u32 total = rb * span2;
-        for (u32 e = gtid; e < total; e += gsize) {
-            const u32 t = e / span2, x = x0 + 2u * (e - t * span2);
-            const u32 ph = p.perm[r + t];
-            *reinterpret_cast<ulonglong2*>(p.stage + (((size_t)(x >> 3) * 64 + t) << 3) + (x & 7u)) =
-                *reinterpret_cast<const ulonglong2*>(tword(p.mat, p.m, ph, x));
-        }
+// Raw pivot-row tails, tiles [(w+1)/8, Wpad8/8), into stage[(T*64 + t)*8 + k];
+// units [u0, u1) of 16 bytes in the flattened (t, x) order.
+__device__ __forceinline__ void stage_units(const Params& p, u32 w, u32 r, u32 rb, u32 u0, u32 u1,
+                                            u32 tid, u32 nthr) {
+    const u32 x0 = (w + 1) & ~7u;
+    const u32 span2 = (p.Wpad8 - x0) >> 1;
+    for (u32 e = u0 + tid; e < u1; e += nthr) {
+        const u32 t = e / span2, x = x0 + 2u * (e - t * span2);
+        const u32 ph = ldcg(p.perm + r + t);
+        *reinterpret_cast<ulonglong2*>(p.stage + (((size_t)(x >> 3) * 64 + t) << 3) + (x & 7u)) =
+            ldcg(reinterpret_cast<const ulonglong2*>(tword(p.mat, p.m, ph, x)));
     }
 }
 
-// ---------------------------------------------------------------------------
-// trailing_update
-// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 stage_total(const Params& p, u32 w, u32 rb) {
+    if (w + 1 >= p.W || rb == 0) return 0;
+    const u32 x0 = (w + 1) & ~7u;
+    return rb * ((p.Wpad8 - x0) >> 1);
+}
+
+__global__ void __launch_bounds__(kApplyThreads) panel_apply_kernel(Params p, u32 w) {
+    __shared__ ApplyShared s;
+    const StepState st = *p.state;
+    const u32 r = st.r, rb = st.rb;
+    if (r >= p.m) return;
+    apply_load(p, s, rb);
+    __syncthreads();
+    const u32 gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 gsize = gridDim.x * blockDim.x;
+    apply_rows(p, s, w, r, rb, r, p.m, gtid, gsize);
+    stage_units(p, w, r, rb, 0, stage_total(p, w, rb), gtid, gsize);
+}
+
+// ===========================================================================
+// Phase 3: trailing update
+// ===========================================================================
 // Shared-memory table layout (conflict-free for the row-pair rotation):
 //   entry e of table g, 16-byte chunk ch  ->  byte
 //   ((g >> 1) * 256 + e) * 128 + (g & 1) * 64 + ch * 16
@@ -523,7 +611,7 @@ __device__ __forceinline__ void build_tables(const Params& p, unsigned char* sme
     for (int b = 0; b < 8; ++b) {
         const u32 t = 8u * g + b;
         ulonglong2 v = make_ulonglong2(0ull, 0ull);
-        if (t < rb) v = *reinterpret_cast<const ulonglong2*>(st + ((size_t)t << 3));
+        if (t < rb) v = ldcg(reinterpret_cast<const ulonglong2*>(st + ((size_t)t << 3)));
         if (x <= w) v.x = 0ull;
         if (x + 1u <= w) v.y = 0ull;
         R[b] = v;
@@ -544,8 +632,101 @@ __device__ __forceinline__ void build_tables(const Params& p, unsigned char* sme
     }
 }
 
-__device__ __forceinline__ ulonglong2 ldg_info(const ulonglong2* info, u32 pos, bool valid) {
-    return valid ? __ldg(info + pos) : make_ulonglong2(0ull, 0ull);
+__device__ __forceinline__ ulonglong2 ld_info(const ulonglong2* info, u32 pos, bool valid) {
+    return valid ? ldcg(info + pos) : make_ulonglong2(0ull, 0ull);
+}
+
+// Rows [row0, row0+cnt) (offsets from r) of tile `tile`; tables must already
+// be built. The tile holding word w+1 also writes the look-ahead panel buffer.
+__device__ __forceinline__ void trail_rows(const Params& p, const unsigned char* smem, u32 w,
+                                           u32 r, u32 tile, u32 row0, u32 cnt) {
+    const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
+    const u32 cap_word = w + 1;
+    const bool capture = (cap_word >> 3) == tile;
+    const bool cap_lane = capture && ((cap_word & 7u) >> 1) == ch;
+    const bool cap_hi = (cap_word & 1u) != 0;
+    const u32 lane_row = wid * 8u + rg;
+    u64* tbase = p.mat + (((size_t)tile * p.m) << 3) + 2u * ch;
+    const u32 rend = row0 + cnt;
+    const u32 nit = (cnt + kRowsPerIter - 1) / kRowsPerIter;
+
+    // software pipeline: rows of iteration i+1 and records of i+2 in flight
+    ulonglong2 infC[kUnroll], infN[kUnroll], valC[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+        const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 4);
+        infC[k] = ld_info(p.info, r + ri, ri < rend);
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+        const u32 ri = row0 + kRowsPerIter + lane_row + (u32)k * (kTrailThreads / 4);
+        infN[k] = ld_info(p.info, r + ri, ri < rend);
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+        const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 4);
+        valC[k] = make_ulonglong2(0ull, 0ull);
+        if (ri < rend && (infC[k].x != 0ull || capture))
+            valC[k] = ldcg(reinterpret_cast<const ulonglong2*>(tbase + ((size_t)infC[k].y << 3)));
+    }
+    for (u32 it = 0; it < nit; ++it) {
+        const u32 base = row0 + it * kRowsPerIter;
+        ulonglong2 valN[kUnroll], infNN[kUnroll];
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            const u32 ri = base + kRowsPerIter + lane_row + (u32)k * (kTrailThreads / 4);
+            valN[k] = make_ulonglong2(0ull, 0ull);
+            if (ri < rend && (infN[k].x != 0ull || capture))
+                valN[k] = ldcg(reinterpret_cast<const ulonglong2*>(tbase + ((size_t)infN[k].y << 3)));
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            const u32 ri = base + 2 * kRowsPerIter + lane_row + (u32)k * (kTrailThreads / 4);
+            infNN[k] = ld_info(p.info, r + ri, ri < rend);
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            const u32 ri = base + lane_row + (u32)k * (kTrailThreads / 4);
+            const u64 d = infC[k].x;
+            if (d != 0ull) {
+#pragma unroll
+                for (u32 gi = 0; gi < kTables; ++gi) {
+                    const u32 g = gi ^ par;
+                    const u32 e = (u32)(d >> (8u * g)) & 0xffu;
+                    xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
+                }
+                *reinterpret_cast<ulonglong2*>(tbase + ((size_t)infC[k].y << 3)) = valC[k];
+            }
+            if (cap_lane && ri < rend) p.pb[r + ri] = cap_hi ? valC[k].y : valC[k].x;
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            infC[k] = infN[k];
+            infN[k] = infNN[k];
+            valC[k] = valN[k];
+        }
+    }
+}
+
+// Linear share [beg, end) of the (tile, row) work of step w over tiles
+// [tile_lo, tile_hi), rows r..m-1; tables rebuilt per tile segment.
+__device__ __forceinline__ void trail_share(const Params& p, unsigned char* smem, u32 w, u32 r,
+                                            u32 rb, u32 tile_lo, u64 beg, u64 end) {
+    const u32 nrows = p.m - r;
+    u64 u = beg;
+    while (u < end) {
+        const u32 tile = tile_lo + (u32)(u / nrows);
+        const u32 row0 = (u32)(u % nrows);
+        const u32 cnt = (u32)min((u64)(nrows - row0), end - u);
+        if (rb > 0) {
+            __syncthreads();
+            build_tables(p, smem, tile, w, rb);
+            __syncthreads();
+        }
+        trail_rows(p, smem, w, r, tile, row0, cnt);
+        u += cnt;
+    }
 }
 
 __global__ void __launch_bounds__(kTrailThreads, 1) trailing_update_kernel(Params p, u32 w) {
@@ -555,91 +736,9 @@ __global__ void __launch_bounds__(kTrailThreads, 1) trailing_update_kernel(Param
     if (r >= p.m || w + 1 >= p.W) return;
     const u32 tile0 = (w + 1) >> 3;
     const u32 ntiles = (p.Wpad8 >> 3) - tile0;
-    const u32 nrows = p.m - r;
-    const u64 total = (u64)ntiles * nrows;
-    const u64 beg = total * blockIdx.x / gridDim.x;
-    const u64 end = total * (blockIdx.x + 1) / gridDim.x;
-
-    const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
-    const u32 cap_word = w + 1;  // next panel word
-    const u32 lane_row = wid * 8u + rg;  // + k * (kTrailThreads/4)
-
-    u64 u = beg;
-    while (u < end) {
-        const u32 tile = tile0 + (u32)(u / nrows);
-        const u32 row0 = (u32)(u % nrows);
-        const u32 cnt = (u32)min((u64)(nrows - row0), end - u);
-        const bool capture = (cap_word >> 3) == tile;
-        const bool cap_lane = capture && ((cap_word & 7u) >> 1) == ch;
-        const bool cap_hi = (cap_word & 1u) != 0;
-        if (rb > 0) {
-            __syncthreads();
-            build_tables(p, smem, tile, w, rb);
-            __syncthreads();
-        }
-        u64* tbase = p.mat + (((size_t)tile * p.m) << 3) + 2u * ch;
-        const u32 rend = row0 + cnt;
-        const u32 nit = (cnt + kRowsPerIter - 1) / kRowsPerIter;
-
-        // software pipeline: rows of iteration i+1 and records of i+2 in flight
-        ulonglong2 infC[kUnroll], infN[kUnroll], valC[kUnroll];
-#pragma unroll
-        for (int k = 0; k < kUnroll; ++k) {
-            const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 4);
-            infC[k] = ldg_info(p.info, r + ri, ri < rend);
-        }
-#pragma unroll
-        for (int k = 0; k < kUnroll; ++k) {
-            const u32 ri = row0 + kRowsPerIter + lane_row + (u32)k * (kTrailThreads / 4);
-            infN[k] = ldg_info(p.info, r + ri, ri < rend);
-        }
-#pragma unroll
-        for (int k = 0; k < kUnroll; ++k) {
-            const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 4);
-            valC[k] = make_ulonglong2(0ull, 0ull);
-            if (ri < rend && (infC[k].x != 0ull || capture))
-                valC[k] = *reinterpret_cast<const ulonglong2*>(tbase + ((size_t)infC[k].y << 3));
-        }
-        for (u32 it = 0; it < nit; ++it) {
-            const u32 base = row0 + it * kRowsPerIter;
-            ulonglong2 valN[kUnroll], infNN[kUnroll];
-#pragma unroll
-            for (int k = 0; k < kUnroll; ++k) {
-                const u32 ri = base + kRowsPerIter + lane_row + (u32)k * (kTrailThreads / 4);
-                valN[k] = make_ulonglong2(0ull, 0ull);
-                if (ri < rend && (infN[k].x != 0ull || capture))
-                    valN[k] = *reinterpret_cast<const ulonglong2*>(tbase + ((size_t)infN[k].y << 3));
-            }
-#pragma unroll
-            for (int k = 0; k < kUnroll; ++k) {
-                const u32 ri = base + 2 * kRowsPerIter + lane_row + (u32)k * (kTrailThreads / 4);
-                infNN[k] = ldg_info(p.info, r + ri, ri < rend);
-            }
-#pragma unroll
-            for (int k = 0; k < kUnroll; ++k) {
-                const u32 ri = base + lane_row + (u32)k * (kTrailThreads / 4);
-                const u64 d = infC[k].x;
-                if (d != 0ull) {
-#pragma unroll
-                    for (u32 gi = 0; gi < kTables; ++gi) {
-                        const u32 g = gi ^ par;
-                        const u32 e = (u32)(d >> (8u * g)) & 0xffu;
-                        xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
-                    }
-                    *reinterpret_cast<ulonglong2*>(tbase + ((size_t)infC[k].y << 3)) = valC[k];
-                }
-                if (cap_lane && ri < rend) p.pb[r + ri] = cap_hi ? valC[k].y : valC[k].x;
-            }
-#pragma unroll
-            for (int k = 0; k < kUnroll; ++k) {
-                infC[k] = infN[k];
-                infN[k] = infNN[k];
-                valC[k] = valN[k];
-            }
-        }
-        u += cnt;
-    }
+    const u64 total = (u64)ntiles * (p.m - r);
+    trail_share(p, smem, w, r, rb, tile0, total * blockIdx.x / gridDim.x,
+                total * (blockIdx.x + 1) / gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,114 @@
+// ple_persistent.cuh -- persistent cooperative driver of the B200 PLE.
+//
+// One launch factors the whole matrix. CTA 0 is the panel CTA: it runs
+// panel_factor_body for step w+1 as soon as every worker has finished the
+// look-ahead tile (the 64-byte tile holding word w+1) of step w, i.e. while
+// the workers are still streaming the rest of step w's trailing update.
+// CTAs 1..G-1 are workers: per step they
+//   apply   their row slab (multipliers, d, compressed words),
+//   stage   their share of the raw pivot-row tails (after all of step w-1),
+//   update  the look-ahead tile for their row slab, signal the panel CTA,
+//   update  their linear share of the remaining tiles.
+// Cross-CTA ordering uses release/acquire counters in SyncState; every wait
+// has a watchdog so a bug turns into an error code, not a hung GPU. The grid
+// is launched cooperatively, so all CTAs are co-resident.
+#pragma once
+
+#include "ple_kernels.cuh"
+
+namespace gf2cu {
+
+__device__ __forceinline__ bool cta_wait(SyncState* sy, const u32* ctr, u32 target, u32& s_ok) {
+    if (threadIdx.x == 0) s_ok = spin_geq(ctr, target, &sy->error) ? 1u : 0u;
+    __syncthreads();
+    return s_ok != 0;
+}
+
+__device__ __forceinline__ void cta_arrive(u32* ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_add(ctr, 1u);
+    }
+}
+
+__device__ __forceinline__ void stamp(const Params& p, u32 w, u32 k) {
+    if (p.phase_ns && threadIdx.x == 0) p.phase_ns[(size_t)w * 8 + k] = globaltimer();
+}
+
+__global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params p, u32 nsteps) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ PanelShared psh;
+    __shared__ ApplyShared ash;
+    __shared__ u32 s_ok;
+    SyncState* sy = p.sync;
+    const u32 nworkers = gridDim.x - 1;
+
+    if (blockIdx.x == 0) {
+        // ------------------------------------------------------ panel CTA
+        for (u32 w = 0; w < nsteps; ++w) {
+            if (w > 0 && !cta_wait(sy, &sy->cap_count, nworkers * w, s_ok)) return;
+            stamp(p, w, 0);
+            panel_factor_body(p, w, psh, blockDim.x);
+            stamp(p, w, 1);
+            const bool done = psh.r >= p.m;
+            cta_arrive(&sy->panel_done);
+            if (done) return;
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- workers
+    const u32 wk = blockIdx.x - 1;
+    for (u32 w = 0; w < nsteps; ++w) {
+        if (!cta_wait(sy, &sy->panel_done, w + 1, s_ok)) return;
+        const volatile StepState* vs = p.state;
+        const u32 r = vs->r, rb = vs->rb;
+        if (r >= p.m) return;
+        Params q = p;
+        q.info = p.info + (size_t)(w & 1u) * p.m;
+        const u32 nrows = p.m - r;
+        const u32 slab = (nrows + nworkers - 1) / nworkers;
+        const u32 lo = min(p.m, r + wk * slab), hi = min(p.m, lo + slab);
+
+        if (wk == 0) stamp(p, w, 2);
+        // apply: own slab
+        apply_load(q, ash, rb);
+        __syncthreads();
+        apply_rows(q, ash, w, r, rb, lo, hi, threadIdx.x, blockDim.x);
+
+        // stage: after every worker finished step w-1 (pivot tails final)
+        if (w > 0 && !cta_wait(sy, &sy->t_count, nworkers * w, s_ok)) return;
+        const u32 stot = stage_total(q, w, rb);
+        stage_units(q, w, r, rb, (u32)((u64)stot * wk / nworkers), (u32)((u64)stot * (wk + 1) / nworkers),
+                    threadIdx.x, blockDim.x);
+        cta_arrive(&sy->st_count);
+        if (!cta_wait(sy, &sy->st_count, nworkers * (w + 1), s_ok)) return;
+
+        if (wk == 0) stamp(p, w, 3);
+        const u32 tile0 = (w + 1) >> 3;
+        if (w + 1 < p.W) {
+            // look-ahead tile: own slab, then release the panel CTA
+            if (hi > lo) {
+                if (rb > 0) {
+                    build_tables(q, smem, tile0, w, rb);
+                    __syncthreads();
+                }
+                trail_rows(q, smem, w, r, tile0, lo - r, hi - lo);
+            }
+            cta_arrive(&sy->cap_count);
+            if (wk == 0) stamp(p, w, 4);
+            // remaining tiles: linear share
+            const u32 nt = (p.Wpad8 >> 3) - tile0 - 1;
+            const u64 total = (u64)nt * nrows;
+            trail_share(q, smem, w, r, rb, tile0 + 1, total * wk / nworkers,
+                        total * (wk + 1) / nworkers);
+        } else {
+            cta_arrive(&sy->cap_count);
+        }
+        cta_arrive(&sy->t_count);
+        if (wk == 0) stamp(p, w, 5);
+    }
+}
+
+}  // namespace gf2cu

@@ -48,6 +48,7 @@ class PleConfig:
     device: int = 0
     stream: Optional[int] = None   # cudaStream_t as an int (e.g. torch stream.cuda_stream)
     time_kernels: bool = False
+    multi_kernel: bool = False     # one launch per phase (cross-check driver)
 
     def to_c(self) -> gf2cu_cfg:
         c = gf2cu_cfg()
@@ -57,7 +58,8 @@ class PleConfig:
         c.table_count = max(1, int(self.table_count))
         c.device = int(self.device)
         c.stream = C.c_void_p(self.stream) if self.stream else None
-        c.flags = _lib.FLAG_TIME_KERNELS if self.time_kernels else 0
+        c.flags = (_lib.FLAG_TIME_KERNELS if self.time_kernels else 0) | \
+            (_lib.FLAG_MULTI_KERNEL if self.multi_kernel else 0)
         return c
 
 

@@ -98,3 +98,25 @@ def test_dropin_cpp_binary():
 def test_smoke_entry():
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("multi", [False, True])
+@pytest.mark.parametrize("m,n,gen", [(3000, 3000, "dense"), (2048, 2048, "p256"), (1500, 4000, "ctr"),
+                                     (4000, 1500, "ctr"), (2500, 2500, "dup")])
+def test_drivers_agree(m, n, gen, multi):
+    """Both drivers (persistent cooperative / one launch per phase) are bit-exact."""
+    if gen == "dense":
+        a = O.fill_random(m, n, 0.5, 5)
+    elif gen == "p256":
+        a = O.fill_random(m, n, 1 / 256, 5)
+    elif gen == "ctr":
+        a = O.fill_ctr(m, n, 5)
+    else:
+        a = O.fill_ctr(m, n, 6)
+        a[100:900] = a[1000:1800]  # rank deficiency: pivotless columns, window misses
+    ref = a.copy()
+    want = O.ple(ref, m, n)
+    bm = G.BitMatrix(m, n, a.copy())
+    got = G.block_iterative_ple(bm, G.PleConfig(multi_kernel=multi))
+    assert got.stats["driver"] == (0 if multi else 1)
+    assert_same(ref, want, bm, got, what=f"{gen} {m}x{n} multi={multi}")
