@@ -100,15 +100,27 @@ class RowPermutation:
                 a[[i, j]] = a[[j, i]]
 
 
-@dataclass
 class PleOutcome:
-    """ple.hpp:45-51."""
-    rank: int = 0
-    processed: int = 0
-    p: RowPermutation = field(default_factory=RowPermutation)
-    q: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.uint64))
-    col_swaps: List[ColSwap] = field(default_factory=list)
-    stats: Optional[dict] = None
+    """ple.hpp:45-51. `col_swaps` is materialised lazily from the (k, 3)
+    array `col_swaps_array` (the canonical {j, q[j], j} list)."""
+
+    def __init__(self, rank: int = 0, processed: int = 0, p: Optional[RowPermutation] = None,
+                 q: Optional[np.ndarray] = None, col_swaps_array: Optional[np.ndarray] = None,
+                 stats: Optional[dict] = None):
+        self.rank = rank
+        self.processed = processed
+        self.p = p if p is not None else RowPermutation()
+        self.q = q if q is not None else np.zeros(0, dtype=np.uint64)
+        self.col_swaps_array = (col_swaps_array if col_swaps_array is not None
+                                else np.zeros((0, 3), dtype=np.uint64))
+        self.stats = stats
+        self._cs = None
+
+    @property
+    def col_swaps(self) -> List[ColSwap]:
+        if self._cs is None:
+            self._cs = [ColSwap(int(a), int(b), int(c)) for a, b, c in self.col_swaps_array]
+        return self._cs
 
 
 class MatrixView:
@@ -328,12 +340,10 @@ def host_checksum(words: np.ndarray, ncols: int) -> int:
 # ----------------------------------------------------------------- the path
 def _outcome(rank, swaps, q, cs, ncs, m, st) -> PleOutcome:
     r = int(rank.value)
-    out = PleOutcome(rank=r, processed=m)
-    out.p = RowPermutation(np.array(swaps[:r], dtype=np.uint64))
-    out.q = np.array(q[:r], dtype=np.uint64)
-    out.col_swaps = [ColSwap(int(cs[i].a), int(cs[i].b), int(cs[i].from_row)) for i in range(int(ncs.value))]
-    out.stats = {f: getattr(st, f) for f, _ in gf2cu_stats._fields_}
-    return out
+    return PleOutcome(rank=r, processed=m, p=RowPermutation(swaps[:r].astype(np.uint64)),
+                      q=q[:r].astype(np.uint64),
+                      col_swaps_array=cs[: int(ncs.value)].astype(np.uint64),
+                      stats={f: getattr(st, f) for f, _ in gf2cu_stats._fields_})
 
 
 def block_iterative_ple(a, cfg: Optional[PleConfig] = None) -> PleOutcome:
@@ -351,17 +361,20 @@ def block_iterative_ple(a, cfg: Optional[PleConfig] = None) -> PleOutcome:
         view = a.view() if isinstance(a, BitMatrix) else a
         m, n = view.nrows(), view.ncols()
     cap = max(1, min(m, n))
-    swaps = (C.c_size_t * cap)()
-    q = (C.c_size_t * cap)()
-    cs = (gf2cu_colswap * cap)()
+    swaps = np.empty(cap, dtype=np.uintp)
+    q = np.empty(cap, dtype=np.uintp)
+    cs = np.empty((cap, 3), dtype=np.uintp)  # gf2cu_colswap = 3 x size_t
     rank = C.c_size_t()
     ncs = C.c_size_t()
     st = gf2cu_stats()
+    szp = C.POINTER(C.c_size_t)
+    sp, qp = swaps.ctypes.data_as(szp), q.ctypes.data_as(szp)
+    cp = C.cast(cs.ctypes.data, C.POINTER(gf2cu_colswap))
     if isinstance(a, DeviceMatrix):
-        check(L.gf2cu_ple_device(h, C.byref(c), swaps, q, C.byref(rank), cs, C.byref(ncs), C.byref(st)))
+        check(L.gf2cu_ple_device(h, C.byref(c), sp, qp, C.byref(rank), cp, C.byref(ncs), C.byref(st)))
     else:
         v = view._c()
-        check(L.gf2cu_ple(C.byref(v), C.byref(c), swaps, q, C.byref(rank), cs, C.byref(ncs), C.byref(st)))
+        check(L.gf2cu_ple(C.byref(v), C.byref(c), sp, qp, C.byref(rank), cp, C.byref(ncs), C.byref(st)))
     return _outcome(rank, swaps, q, cs, ncs, m, st)
 
 
