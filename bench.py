@@ -251,18 +251,23 @@ def gpu_arm(args, rank, world, local_rank):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     tot_bytes = 0.0
-    trail_ms = 0.0
-    launches = 0
+    trail_ms = 0.0      # device-timestamped trailing-update phases (inside the kernel)
+    kern_ms = 0.0       # CUDA-event duration of the persistent PLE kernel
+    launches = 0        # persistent-kernel launches (one per PLE)
     kernel_launches = 0
+    panel_ms = apply_ms = 0.0
     for _ in range(args.steps):
         work.copy_from(pristine, stream=sptr)
         out = G.block_iterative_ple(work, cfg_t)
         st = out.stats
         tot_bytes += st["alg_bytes"]
         trail_ms += st["trailing_ms"]
-        launches += st["trailing_launches"]
-        # tile + init + untile, and per step panel + apply (+ trailing)
-        kernel_launches += 3 + 2 * st["steps"] + st["trailing_launches"]
+        kern_ms += st["kernel_ms"]
+        panel_ms += st["panel_ms"]
+        apply_ms += st["coef_ms"]
+        launches += 1
+        # tile + init + persistent PLE + untile per step
+        kernel_launches += 4
     ev1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -290,7 +295,7 @@ def gpu_arm(args, rank, world, local_rank):
     e2e_parity = (o2.rank == out.rank)
 
     # ---- max over ranks ----
-    vals = torch.tensor([dev_ms, tot_bytes, e2e_s, e2e_bytes, trail_ms, float(launches)],
+    vals = torch.tensor([dev_ms, tot_bytes, e2e_s, e2e_bytes, kern_ms, float(launches)],
                         dtype=torch.float64, device="cuda")
     if dist is not None:
         allv = [torch.zeros_like(vals) for _ in range(world)]
@@ -313,17 +318,23 @@ def gpu_arm(args, rank, world, local_rank):
     e2e_value = e2e_sum_bytes / e2e_max_s / 1e9
     peak, peak_kind = load_peaks()
     per_launch_bytes = tot_bytes / max(1, launches)
-    per_launch_ms = trail_ms / max(1, launches)
+    per_launch_ms = kern_ms / max(1, launches)
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else None
     traffic_ratio = load_traffic()
     roofline = {
-        "kernel": "trailing_update_kernel", "bound": "hbm",
+        "kernel": "ple_persistent_kernel", "bound": "hbm",
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": (round(per_launch_bytes * traffic_ratio) if traffic_ratio else None),
-        "alg_bytes_per_launch": round(per_launch_bytes), "avg_launch_ms": round(per_launch_ms, 5),
-        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
-        "share_of_step": round(trail_ms / max(1e-9, dev_ms), 4),
+        "alg_bytes_per_launch": round(per_launch_bytes), "avg_launch_ms": round(per_launch_ms, 4),
+        "peak_source": (f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+                        else "fallback 6.65 TB/s"),
+        "share_of_step": round(kern_ms / max(1e-9, dev_ms), 4),
+        "phases_ms_per_launch": {"trailing_sweep": round(trail_ms / max(1, launches), 3),
+                                 "panel_factor_overlapped": round(panel_ms / max(1, launches), 3),
+                                 "apply_stage_barriers": round(apply_ms / max(1, launches), 3)},
+        "trailing_sweep_GBps": round(per_launch_bytes / (trail_ms / max(1, launches) * 1e-3) / 1e9, 1)
+        if trail_ms > 0 else None,
     }
 
     cpu = None
