@@ -138,7 +138,7 @@ gf2cu_status ensure_ws(gf2cu_matrix* a) {
     CU_TRY(cudaMalloc(&w.pb, std::max<size_t>(1, m) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.info, 2 * std::max<size_t>(1, m) * sizeof(ulonglong2)));
     CU_TRY(cudaMalloc(&w.sync, sizeof(gf2cu::SyncState)));
-    CU_TRY(cudaMalloc(&w.phase_ns, (8 * (a->W + 1) + 8 + 64 * 5 + 3 * 160) * sizeof(u64)));
+    CU_TRY(cudaMalloc(&w.phase_ns, (8 * (a->W + 1) + 8 + 2 * 64 * 5 + 3 * 160) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.stage, 64 * wpad8(a->W) * sizeof(u64)));
     CU_TRY(cudaMemset(w.stage, 0, 64 * wpad8(a->W) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.state, sizeof(gf2cu::StepState)));
@@ -354,9 +354,6 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
                     }
                     std::vector<u64> dbg(64 * 5);
                     cudaMemcpy(dbg.data(), ws.phase_ns + 8 * W + 8, dbg.size() * 8, cudaMemcpyDeviceToHost);
-                    std::vector<u64> wkt(3 * 160);
-                    cudaMemcpy(wkt.data(), ws.phase_ns + 8 * W + 8 + 64 * 5, wkt.size() * 8, cudaMemcpyDeviceToHost);
-                    for (int k = 0; k < 3 * 160; ++k) std::fprintf(f, "#W %d %llu\n", k, wkt[k]);
                     for (int j = 0; j < 64; ++j)
                         std::fprintf(f, "# %d %llu %llu %llu %llu %llu\n", j, dbg[5 * j], dbg[5 * j + 1],
                                      dbg[5 * j + 2], dbg[5 * j + 3], dbg[5 * j + 4]);
