@@ -217,7 +217,11 @@ def gpu_arm(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = local_rank
-    stream = torch.cuda.current_stream()
+    # an explicit stream: the library calls, the CUDA events and every torch op
+    # of the timed region are ordered on it (the legacy default stream is not
+    # ordered with the library's non-blocking streams)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
     m = n = args.n
     dist = None

@@ -135,6 +135,55 @@ gf2cu_status gf2cu_ple_device(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swa
                               gf2cu_stats* stats);
 
 /* ------------------------------------------------------------------ */
+/* Row-sharded multi-GPU PLE (one process per GPU, host-driven steps)   */
+/* ------------------------------------------------------------------ */
+/* Global row g lives on rank (g / block) % nranks, local index
+ * (g / (block * nranks)) * block + g % block. Each rank holds its rows plus
+ * the replicated position state; the orchestration (collectives) is done by
+ * the caller, see paper_1111_6549_b200/shard.py and DESIGN.md section 8.
+ * All calls are asynchronous on `stream` except gf2cu_shard_panel (returns
+ * the status words) and gf2cu_shard_finish / download. Buffers passed as
+ * device pointers (pos_words, pack) are caller-owned device memory. */
+typedef struct gf2cu_shard gf2cu_shard;
+
+#define GF2CU_SHARD_STATUS_WORDS(nranks) (8 + 2 * (nranks))
+
+gf2cu_status gf2cu_shard_create(size_t m, size_t n, int rank, int nranks, size_t block, int device,
+                                gf2cu_shard** out);
+gf2cu_status gf2cu_shard_destroy(gf2cu_shard* s);
+/* m_local rows on this rank; pack_words = u64 capacity the pack buffer needs. */
+gf2cu_status gf2cu_shard_info(const gf2cu_shard* s, size_t* m_local, size_t* pack_words);
+/* Local rows in local order, host_stride words apart. */
+gf2cu_status gf2cu_shard_upload(gf2cu_shard* s, const uint64_t* host, size_t host_stride,
+                                void* stream);
+gf2cu_status gf2cu_shard_download(const gf2cu_shard* s, uint64_t* host, size_t host_stride,
+                                  void* stream);
+/* Start a factorization: tile-major working copy, replicated state reset. */
+gf2cu_status gf2cu_shard_begin(gf2cu_shard* s, void* stream);
+/* pos_words[lo, hi) := 0 then this rank's active rows' panel words at their
+ * positions (the caller all-reduces (sum) that range across ranks). */
+gf2cu_status gf2cu_shard_gather(gf2cu_shard* s, uint64_t* pos_words, size_t lo, size_t hi,
+                                void* stream);
+/* Panel factorization of step w from the all-reduced pos_words; window_only
+ * = 1 aborts on a window miss (status[0] = 1, nothing changed). status_out
+ * receives GF2CU_SHARD_STATUS_WORDS(nranks) words: [0] miss, [1] rb, [2] r,
+ * [8 + 2o], [9 + 2o] = low/high half of rank o's pivot bitmask. */
+gf2cu_status gf2cu_shard_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, int window_only,
+                               uint32_t* status_out, void* stream);
+/* Apply step w to the local rows; packs this rank's pivot tails into pack. */
+gf2cu_status gf2cu_shard_apply(gf2cu_shard* s, size_t w, uint64_t* pack, void* stream);
+/* Stage owner rank's packed pivot tails (bitmask mask) for step w. */
+gf2cu_status gf2cu_shard_unpack(gf2cu_shard* s, size_t w, uint64_t mask, const uint64_t* pack,
+                                void* stream);
+/* Trailing update of step w on the local rows. */
+gf2cu_status gf2cu_shard_trailing(gf2cu_shard* s, size_t w, void* stream);
+/* End: local rows back to row-major (gf2cu_shard_download reads them), and the
+ * replicated outcome: swaps/q (capacity min(m,n)), rank, and perm[m] =
+ * global row id at each final position (the caller assembles rows). */
+gf2cu_status gf2cu_shard_finish(gf2cu_shard* s, size_t* swaps, size_t* q, size_t* rank,
+                                uint32_t* perm, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* Host-side input generators (bench/test inputs; not the hot path)     */
 /* ------------------------------------------------------------------ */
 /* gf2::fill_random (bit_matrix.hpp:459-486), mt19937_64-driven. */

@@ -104,6 +104,18 @@ SYMBOLS = {
     "gf2cu_matrix_checksum": (C.c_int, [_mp, _u64p, C.c_void_p]),
     "gf2cu_ple_device": (C.c_int, [_mp, C.POINTER(gf2cu_cfg), _szp, _szp, _szp,
                                    C.POINTER(gf2cu_colswap), _szp, C.POINTER(gf2cu_stats)]),
+    "gf2cu_shard_create": (C.c_int, [_sz, _sz, C.c_int, C.c_int, _sz, C.c_int, C.POINTER(_mp)]),
+    "gf2cu_shard_destroy": (C.c_int, [_mp]),
+    "gf2cu_shard_info": (C.c_int, [_mp, _szp, _szp]),
+    "gf2cu_shard_upload": (C.c_int, [_mp, _u64p, _sz, C.c_void_p]),
+    "gf2cu_shard_download": (C.c_int, [_mp, _u64p, _sz, C.c_void_p]),
+    "gf2cu_shard_begin": (C.c_int, [_mp, C.c_void_p]),
+    "gf2cu_shard_gather": (C.c_int, [_mp, _u64p, _sz, _sz, C.c_void_p]),
+    "gf2cu_shard_panel": (C.c_int, [_mp, _sz, _u64p, C.c_int, C.POINTER(C.c_uint32), C.c_void_p]),
+    "gf2cu_shard_apply": (C.c_int, [_mp, _sz, _u64p, C.c_void_p]),
+    "gf2cu_shard_unpack": (C.c_int, [_mp, _sz, C.c_uint64, _u64p, C.c_void_p]),
+    "gf2cu_shard_trailing": (C.c_int, [_mp, _sz, C.c_void_p]),
+    "gf2cu_shard_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),
     "gf2cu_fill_random": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_double, C.c_uint64]),
     "gf2cu_fill_ctr": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_uint64]),
 }

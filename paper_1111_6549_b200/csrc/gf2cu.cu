@@ -20,6 +20,7 @@
 #include "gf2cu.h"
 #include "ple_kernels.cuh"
 #include "ple_persistent.cuh"
+#include "ple_shard.cuh"
 
 using gf2cu::u32;
 using gf2cu::u64;
@@ -657,6 +658,317 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
         }
     }
     return st;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- sharded
+struct gf2cu_shard {
+    size_t m = 0, n = 0, W = 0, Wp = 0, Wpad8 = 0, m_loc = 0, block = 0;
+    int rank = 0, nranks = 1, device = 0;
+    // local
+    u64* data = nullptr;  // row-major (upload / download)
+    u64* mat = nullptr;   // tile-major working copy
+    u64* pbl = nullptr;
+    ulonglong2* info = nullptr;
+    unsigned char* retired = nullptr;
+    gf2cu::StepState* lstate = nullptr;
+    u64* stage = nullptr;
+    // replicated
+    u32* perm = nullptr;
+    u32* inv = nullptr;
+    gf2cu::StepState* gstate = nullptr;
+    gf2cu::PanelOut* pout = nullptr;
+    u32* swaps = nullptr;
+    u32* qcol = nullptr;
+    u32* rhist = nullptr;
+    u32* rbhist = nullptr;
+    u32* status = nullptr;
+    cudaStream_t own = nullptr;
+};
+
+namespace {
+
+cudaStream_t shard_stream(gf2cu_shard* s, void* st) {
+    return st ? reinterpret_cast<cudaStream_t>(st) : s->own;
+}
+
+gf2cu::ShardParams shard_params(gf2cu_shard* s) {
+    gf2cu::ShardParams p{};
+    p.mat = s->mat;
+    p.pbl = s->pbl;
+    p.info = s->info;
+    p.retired = s->retired;
+    p.lstate = s->lstate;
+    p.perm = s->perm;
+    p.inv = s->inv;
+    p.gstate = s->gstate;
+    p.pout = s->pout;
+    p.m_loc = (u32)s->m_loc;
+    p.m = (u32)s->m;
+    p.n = (u32)s->n;
+    p.W = (u32)s->W;
+    p.Wpad8 = (u32)s->Wpad8;
+    p.rank = (u32)s->rank;
+    p.nranks = (u32)s->nranks;
+    p.block = (u32)s->block;
+    return p;
+}
+
+size_t shard_local_rows(size_t m, size_t rank, size_t nranks, size_t block) {
+    size_t cnt = 0;
+    const size_t nblocks = (m + block - 1) / block;
+    for (size_t b = rank; b < nblocks; b += nranks) cnt += std::min(block, m - b * block);
+    return cnt;
+}
+
+}  // namespace
+
+extern "C" {
+
+gf2cu_status gf2cu_shard_create(size_t m, size_t n, int rank, int nranks, size_t block, int device,
+                                gf2cu_shard** out) {
+    if (!out) return fail(GF2CU_EINVAL, "out is null");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks || block == 0)
+        return fail(GF2CU_EINVAL, "bad rank / nranks / block");
+    if (m == 0 || n == 0 || m >= (1ull << 31) || n >= (1ull << 31))
+        return fail(GF2CU_EINVAL, "dimensions must be in [1, 2^31)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(GF2CU_ENODEVICE, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(GF2CU_EINVAL, "bad device ordinal");
+    DeviceGuard g(device);
+    auto* s = new (std::nothrow) gf2cu_shard;
+    if (!s) return fail(GF2CU_ENOMEM, "host allocation failed");
+    s->m = m;
+    s->n = n;
+    s->W = words_of(n);
+    s->Wp = padded_stride(n);
+    s->Wpad8 = wpad8(s->W);
+    s->rank = rank;
+    s->nranks = nranks;
+    s->block = block;
+    s->device = device;
+    s->m_loc = shard_local_rows(m, rank, nranks, block);
+    const size_t ml = std::max<size_t>(1, s->m_loc), mn = std::max<size_t>(1, std::min(m, n));
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](auto** ptr, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(ptr), bytes);
+    };
+    alloc(&s->data, ml * s->Wp * 8);
+    alloc(&s->mat, ml * s->Wpad8 * 8);
+    alloc(&s->pbl, ml * 8);
+    alloc(&s->info, ml * sizeof(ulonglong2));
+    alloc(&s->retired, ml);
+    alloc(&s->lstate, sizeof(gf2cu::StepState));
+    alloc(&s->stage, 64 * s->Wpad8 * 8);
+    alloc(&s->perm, m * 4);
+    alloc(&s->inv, m * 4);
+    alloc(&s->gstate, sizeof(gf2cu::StepState));
+    alloc(&s->pout, sizeof(gf2cu::PanelOut));
+    alloc(&s->swaps, mn * 4);
+    alloc(&s->qcol, mn * 4);
+    alloc(&s->rhist, (s->W + 1) * 4);
+    alloc(&s->rbhist, (s->W + 1) * 4);
+    alloc(&s->status, (8 + 2 * (size_t)nranks) * 4);
+    if (e == cudaSuccess) e = cudaMemset(s->data, 0, ml * s->Wp * 8);
+    if (e == cudaSuccess) e = cudaMemset(s->stage, 0, 64 * s->Wpad8 * 8);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        gf2cu_shard_destroy(s);
+        return cuda_fail(e, "gf2cu_shard_create");
+    }
+    *out = s;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_destroy(gf2cu_shard* s) {
+    if (!s) return GF2CU_OK;
+    DeviceGuard g(s->device);
+    for (void* p : {(void*)s->data, (void*)s->mat, (void*)s->pbl, (void*)s->info, (void*)s->retired,
+                    (void*)s->lstate, (void*)s->stage, (void*)s->perm, (void*)s->inv,
+                    (void*)s->gstate, (void*)s->pout, (void*)s->swaps, (void*)s->qcol,
+                    (void*)s->rhist, (void*)s->rbhist, (void*)s->status})
+        cudaFree(p);
+    if (s->own) cudaStreamDestroy(s->own);
+    delete s;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_info(const gf2cu_shard* s, size_t* m_local, size_t* pack_words) {
+    if (!s) return fail(GF2CU_EINVAL, "null shard");
+    if (m_local) *m_local = s->m_loc;
+    if (pack_words) *pack_words = 64 * s->Wpad8;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_upload(gf2cu_shard* s, const uint64_t* host, size_t host_stride,
+                                void* stream) {
+    if (!s || (!host && s->m_loc)) return fail(GF2CU_EINVAL, "null argument");
+    if (host_stride < s->W) return fail(GF2CU_EINVAL, "host stride smaller than the row");
+    if (!s->m_loc) return GF2CU_OK;
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    CU_TRY(cudaMemcpy2DAsync(s->data, s->Wp * 8, host, host_stride * 8, s->W * 8, s->m_loc,
+                             cudaMemcpyHostToDevice, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_download(const gf2cu_shard* s, uint64_t* host, size_t host_stride,
+                                  void* stream) {
+    if (!s || (!host && s->m_loc)) return fail(GF2CU_EINVAL, "null argument");
+    if (host_stride < s->W) return fail(GF2CU_EINVAL, "host stride smaller than the row");
+    if (!s->m_loc) return GF2CU_OK;
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(const_cast<gf2cu_shard*>(s), stream);
+    CU_TRY(cudaMemcpy2DAsync(host, host_stride * 8, s->data, s->Wp * 8, s->W * 8, s->m_loc,
+                             cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_begin(gf2cu_shard* s, void* stream) {
+    if (!s) return fail(GF2CU_EINVAL, "null shard");
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    const int sms = num_sms(s->device);
+    if (s->m_loc)
+        gf2cu::tile_kernel<<<sms * 8, 256, 0, st>>>(s->data, s->mat, (u32)s->m_loc, (u32)s->Wp,
+                                                   (u32)s->Wpad8);
+    gf2cu::shard_init_kernel<<<sms * 4, 256, 0, st>>>(shard_params(s), s->perm, s->inv, s->gstate);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_gather(gf2cu_shard* s, uint64_t* pos_words, size_t lo, size_t hi,
+                                void* stream) {
+    if (!s || !pos_words || lo > hi || hi > s->m) return fail(GF2CU_EINVAL, "bad gather range");
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    if (hi == lo) return GF2CU_OK;
+    CU_TRY(cudaMemsetAsync(pos_words + lo, 0, (hi - lo) * 8, st));
+    if (s->m_loc)
+        gf2cu::shard_gather_kernel<<<num_sms(s->device) * 4, 256, 0, st>>>(
+            shard_params(s), reinterpret_cast<u64*>(pos_words), (u32)lo, (u32)hi);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, int window_only,
+                               uint32_t* status_out, void* stream) {
+    if (!s || !pos_words || !status_out || w >= s->W) return fail(GF2CU_EINVAL, "bad panel call");
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    gf2cu::Params p{};
+    p.pb = reinterpret_cast<u64*>(pos_words);
+    p.perm = s->perm;
+    p.inv = s->inv;
+    p.state = s->gstate;
+    p.pout = s->pout;
+    p.swaps = s->swaps;
+    p.qcol = s->qcol;
+    p.rhist = s->rhist;
+    p.rbhist = s->rbhist;
+    p.status = s->status;
+    p.window_only = window_only ? 1u : 0u;
+    p.nranks = (u32)s->nranks;
+    p.block = (u32)s->block;
+    p.m = (u32)s->m;
+    p.n = (u32)s->n;
+    p.W = (u32)s->W;
+    p.Wpad8 = (u32)s->Wpad8;
+    gf2cu::panel_factor_kernel<<<1, gf2cu::kPanelThreads, 0, st>>>(p, (u32)w);
+    CU_TRY(cudaGetLastError());
+    CU_TRY(cudaMemcpyAsync(status_out, s->status, (8 + 2 * (size_t)s->nranks) * 4,
+                           cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_apply(gf2cu_shard* s, size_t w, uint64_t* pack, void* stream) {
+    if (!s || !pack || w >= s->W) return fail(GF2CU_EINVAL, "bad apply call");
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    CU_TRY(cudaMemsetAsync(&s->lstate->r, 0xff, 4, st));
+    if (s->m_loc) {
+        gf2cu::ShardParams p = shard_params(s);
+        p.pack = reinterpret_cast<u64*>(pack);
+        gf2cu::shard_apply_kernel<<<num_sms(s->device) * 4, gf2cu::kApplyThreads, 0, st>>>(p, (u32)w);
+    }
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_unpack(gf2cu_shard* s, size_t w, uint64_t mask, const uint64_t* pack,
+                                void* stream) {
+    if (!s || !pack || w >= s->W) return fail(GF2CU_EINVAL, "bad unpack call");
+    if (!mask || w + 1 >= s->W) return GF2CU_OK;
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    gf2cu::shard_unpack_kernel<<<num_sms(s->device) * 4, 256, 0, st>>>(
+        reinterpret_cast<const u64*>(pack), mask, s->stage, (u32)w, (u32)s->Wpad8);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_trailing(gf2cu_shard* s, size_t w, void* stream) {
+    if (!s || w >= s->W) return fail(GF2CU_EINVAL, "bad trailing call");
+    if (!s->m_loc || w + 1 >= s->W) return GF2CU_OK;
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    static bool attr[64] = {false};
+    if (s->device < 64 && !attr[s->device]) {
+        CU_TRY(cudaFuncSetAttribute(gf2cu::trailing_update_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    gf2cu::kTableBytes));
+        attr[s->device] = true;
+    }
+    gf2cu::Params p{};
+    p.mat = s->mat;
+    p.pb = s->pbl;
+    p.info = s->info;
+    p.stage = s->stage;
+    p.state = s->lstate;
+    p.m = (u32)s->m_loc;
+    p.n = (u32)s->n;
+    p.W = (u32)s->W;
+    p.Wpad8 = (u32)s->Wpad8;
+    gf2cu::trailing_update_kernel<<<num_sms(s->device), gf2cu::kTrailThreads, gf2cu::kTableBytes,
+                                    st>>>(p, (u32)w);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_finish(gf2cu_shard* s, size_t* swaps, size_t* q, size_t* rank,
+                                uint32_t* perm, void* stream) {
+    if (!s || !rank || !perm || ((!swaps || !q) && std::min(s->m, s->n) > 0))
+        return fail(GF2CU_EINVAL, "null argument");
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    if (s->m_loc)
+        gf2cu::untile_kernel<<<num_sms(s->device) * 8, 256, 0, st>>>(s->mat, s->data, nullptr,
+                                                                    (u32)s->m_loc, (u32)s->Wp,
+                                                                    (u32)s->Wpad8);
+    CU_TRY(cudaGetLastError());
+    gf2cu::StepState fin{};
+    CU_TRY(cudaMemcpyAsync(&fin, s->gstate, sizeof(fin), cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaMemcpyAsync(perm, s->perm, s->m * 4, cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(s->m, s->n));
+    std::vector<u32> sw(rk), qq(rk);
+    if (rk) {
+        CU_TRY(cudaMemcpyAsync(sw.data(), s->swaps, rk * 4, cudaMemcpyDeviceToHost, st));
+        CU_TRY(cudaMemcpyAsync(qq.data(), s->qcol, rk * 4, cudaMemcpyDeviceToHost, st));
+        CU_TRY(cudaStreamSynchronize(st));
+    }
+    for (size_t i = 0; i < rk; ++i) {
+        swaps[i] = sw[i];
+        q[i] = qq[i];
+    }
+    *rank = rk;
+    return GF2CU_OK;
 }
 
 gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t stride, double density,

@@ -85,8 +85,19 @@ struct Params {
     volatile u32* host_r;  // mapped pinned mirror of (r + rb), may be null
     SyncState* sync;
     u64* phase_ns;   // per-step phase timestamps (persistent driver), may be null
+    // sharded driver only (null / 0 otherwise)
+    u32* inv;        // global row -> position (kept in step with perm)
+    u32* status;     // panel status words (see kPanelStatus*)
+    u32 window_only; // 1: abort on a window miss instead of scanning
+    u32 nranks, block;  // row distribution: row g lives on rank (g / block) % nranks
     u32 m, n, W, Wpad8;
 };
+
+// Panel status words written when Params::status is set.
+constexpr int kStatusMiss = 0;   // 1 = aborted on a window miss (window_only)
+constexpr int kStatusRb = 1;     // pivots found
+constexpr int kStatusR = 2;      // pivots before this step
+constexpr int kStatusOwners = 8; // 2 words per rank: bitmask of pivots t owned
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ u64 low_mask64(int k) {
@@ -324,6 +335,11 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             *p.host_r = r;
             __threadfence_system();
         }
+        if (threadIdx.x == 0 && p.status) {
+            p.status[kStatusMiss] = 0u;
+            p.status[kStatusRb] = 0u;
+            p.status[kStatusR] = r;
+        }
         __syncthreads();
         return 0;
     }
@@ -352,6 +368,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 6] = globaltimer();
         int t = 0;
         int out_next = nwin < nrem ? 0 : 64;
+        bool aborted = false;
         for (int j = 0; j < jmax && (u32)t < nrem; ++j) {
             const int par = j & 1;
             // candidates: live rows (position >= t) holding column j
@@ -391,6 +408,12 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             } else {
                 // ---- window miss: the remaining rows decide ----
                 if (j < out_next) continue;  // no row outside has this column
+                if (p.window_only) {
+                    // sharded driver: the host gathers the whole panel column
+                    // and runs the step again (nothing global was written)
+                    aborted = true;
+                    break;
+                }
                 if (me == 0) {
                     sh.cmd = 0;
                     sh.t = t;
@@ -414,6 +437,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 if (me == (u32)t) {
                     p.pb[r + P] = sh.wraw[org];
                     p.perm[r + P] = sh.wphys[org];
+                    if (p.inv) p.inv[sh.wphys[org]] = r + P;
                     sh.oraw[t] = sh.o_raw;
                     sh.ophys[t] = sh.o_phys;
                 }
@@ -445,16 +469,42 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         }
         if (me == 0) {
             sh.cmd = 1;
-            sh.t = t;
+            sh.t = aborted ? -1 : t;
         }
         named_bar(1, nthr);  // release the helpers
-        if (inwin) {
+        if (inwin && !aborted) {
             p.pb[r + me] = rw;
             p.perm[r + me] = ph;
+            if (p.inv) p.inv[ph] = r + me;
         }
     }
     __syncthreads();
+    if (sh.t < 0) {
+        // aborted: state stays {r, 0}, so running the step again is exact
+        if (threadIdx.x == 0 && p.status) {
+            p.status[kStatusMiss] = 1u;
+            p.status[kStatusRb] = 0u;
+            p.status[kStatusR] = r;
+        }
+        __syncthreads();
+        return 0;
+    }
     const u32 t = (u32)sh.t;
+    if (p.status) {
+        // sharded driver: which rank owns each pivot row
+        for (u32 k = threadIdx.x; k < 2u * p.nranks; k += nthr) p.status[kStatusOwners + k] = 0u;
+        __syncthreads();
+        for (u32 k = threadIdx.x; k < t; k += nthr) {
+            const u32 g = p.perm[r + k];
+            const u32 o = (g / p.block) % p.nranks;
+            atomicOr(&p.status[kStatusOwners + 2 * o + (k >> 5)], 1u << (k & 31));
+        }
+        if (threadIdx.x == 0) {
+            p.status[kStatusMiss] = 0u;
+            p.status[kStatusRb] = t;
+            p.status[kStatusR] = r;
+        }
+    }
     for (u32 k = threadIdx.x; k < t; k += nthr) {
         p.pout->E[k] = sh.E[k];
         p.pout->D[k] = sh.D[k];

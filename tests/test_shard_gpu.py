@@ -1,0 +1,90 @@
+"""GPU: the row-sharded driver with the DEVICE engine (gf2cu_shard_* C ABI),
+bit-exact vs the oracle. world_size 1 over NCCL, and world_size 2/3 as
+processes sharing the one GPU with gloo collectives on CUDA tensors (the
+per-rank kernels never wait on each other; all coordination is host-side
+collectives, so this is safe on one device)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _make(case):
+    if case == "dense":
+        return O.fill_random(700, 900, 0.5, 11), 700, 900
+    if case == "sparse":
+        return O.fill_random(600, 600, 1 / 64, 12), 600, 600
+    if case == "deficient":
+        return O.mul(O.fill_ctr(500, 300, 13), 300, O.fill_ctr(300, 640, 14), 640), 500, 640
+    if case == "big":
+        return O.fill_ctr(4096, 4096, 15), 4096, 4096
+    raise ValueError(case)
+
+
+def _worker(rank, world, port, backend, case, block, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
+    dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+    try:
+        from paper_1111_6549_b200.shard import sharded_block_iterative_ple
+        a, m, n = _make(case)
+        res, full = sharded_block_iterative_ple(a, m, n, block=block)
+        q.put((rank, res.rank, res.swaps, res.q, full))
+    except Exception as e:  # report instead of leaving the peer hanging
+        import traceback
+        q.put((rank, "error", traceback.format_exc(), None, None))
+        os._exit(1)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,backend,case,block", [
+    (1, "nccl", "dense", 256), (1, "nccl", "big", 256), (2, "gloo", "dense", 64),
+    (2, "gloo", "sparse", 32), (3, "gloo", "deficient", 16), (2, "gloo", "big", 256)])
+def test_sharded_device_engine(world, backend, case, block):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, case, block, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = []
+    try:
+        for _ in range(world):
+            o = q.get(timeout=240)
+            assert o[1] != "error", o[2]
+            outs.append(o)
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for p in procs:
+        assert p.exitcode == 0
+    a, m, n = _make(case)
+    ref = a.copy()
+    want = O.ple(ref, m, n)
+    for (rk, rank, swaps, qq, full) in outs:
+        assert rank == want.rank
+        assert np.array_equal(swaps, want.swaps.astype(np.uint64))
+        assert np.array_equal(qq, want.q.astype(np.uint64))
+        assert np.array_equal(full, ref), f"rank {rk}"
