@@ -378,20 +378,130 @@ def gpu_arm(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def weak_n(world: int) -> int:
+    """Per-GPU work fixed as N grows: total work ~ n^3, so n = 65536 * N^(1/3)
+    (N = 8 -> 131072, BASELINE config 5's large case)."""
+    return int(round(N_DEFAULT * world ** (1.0 / 3.0) / 64.0)) * 64
+
+
+def q_to_bytes(m, n, q):
+    W = (n + 63) // 64
+    q = np.asarray(q, dtype=np.int64)
+    rh, rbh, r = [], [], 0
+    for w in range(W):
+        rb = int(np.count_nonzero((q >= 64 * w) & (q < 64 * w + 64)))
+        rh.append(r)
+        rbh.append(rb)
+        r += rb
+    return alg_bytes_from_history(m, n, rh, rbh)
+
+
+def gpu_sharded_arm(args, rank, world, local_rank):
+    """N > 1: the row-sharded PLE (paper_1111_6549_b200/shard.py), one process
+    per GPU over NCCL, on the weak-scaling size n = 65536 * N^(1/3)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1111_6549_b200 import shard as S
+
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    n = args.n if args.n != N_DEFAULT else weak_n(world)
+    m = n
+    eng = S.GpuShardEngine(m, n, rank, world, block=256, device=local_rank)
+
+    def one():
+        eng.fill_ctr(SEED)
+        return S.run_sharded(eng, dist)
+
+    res = None
+    for _ in range(args.warmup):
+        res = one()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with eng.stream_ctx():
+        ev0.record()
+        for _ in range(args.steps):
+            res = one()
+        ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    bytes_per_step = float(q_to_bytes(m, n, res.q))
+    # e2e: each rank's rows in from pinned host memory, L\E rows back out
+    Wd = (n + 63) // 64
+    host_in = torch.empty((max(1, eng.m_local), Wd), dtype=torch.int64, pin_memory=True)
+    eng.fill_ctr(SEED)
+    eng.download(host_in.numpy().view(np.uint64))
+    t_e2e = 0.0
+    e2e_steps = max(1, min(args.steps, 2))
+    for _ in range(e2e_steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.upload(host_in.numpy().view(np.uint64)[: eng.m_local])
+        out2 = S.run_sharded(eng, dist)  # finish() downloads this rank's rows
+        torch.cuda.synchronize()
+        t_e2e += time.perf_counter() - t0
+        assert out2.rank == res.rank
+    vals = torch.tensor([dev_ms, t_e2e], dtype=torch.float64, device="cuda")
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    max_ms, e2e_max_s = float(vals[0]), float(vals[1])
+    if rank == 0:
+        value = bytes_per_step * args.steps / (max_ms * 1e-3) / 1e9
+        peak, peak_kind = load_peaks()
+        per_gpu = value / world
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"block_iterative_ple {m}x{n} row-sharded over {world} GPUs "
+                                   f"(weak scaling: n = 65536*N^(1/3); N=8 is BASELINE config 5's 131072^2)",
+                       "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "rank": int(res.rank),
+                       "panel_bits": 64, "parallelism": f"row-sharded x{world} (block-cyclic 256-row blocks, NCCL)",
+                       "l2": "per-GPU shard > 126 MB L2"},
+            "e2e": {"value": round(bytes_per_step * e2e_steps / e2e_max_s / 1e9, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": int(m * Wd * 8), "d2h_bytes_per_step": int(m * Wd * 8),
+                    "steps": e2e_steps},
+            "roofline": {"kernel": "sharded step sequence (per GPU)", "bound": "hbm",
+                         "achieved": round(per_gpu, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(per_gpu / peak, 4), "traffic": None,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+            "cpu_baseline": None,
+            "clocks": clk,
+            "gpu_launches": None,
+        }))
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--size", dest="n", type=int, default=N_DEFAULT)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded PLE even at N=1 (testing)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent single-GPU replicas instead of the row-sharded PLE")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         reference_arm(args, rank)
+        return
+    if (world > 1 and not args.replicas) or args.sharded:
+        gpu_sharded_arm(args, rank, world, local_rank)
         return
     gpu_arm(args, rank, world, local_rank)
 

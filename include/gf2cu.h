@@ -158,6 +158,8 @@ gf2cu_status gf2cu_shard_upload(gf2cu_shard* s, const uint64_t* host, size_t hos
                                 void* stream);
 gf2cu_status gf2cu_shard_download(const gf2cu_shard* s, uint64_t* host, size_t host_stride,
                                   void* stream);
+/* Device-side ctr generator for this rank's rows. */
+gf2cu_status gf2cu_shard_fill_ctr(gf2cu_shard* s, uint64_t seed, void* stream);
 /* Start a factorization: tile-major working copy, replicated state reset. */
 gf2cu_status gf2cu_shard_begin(gf2cu_shard* s, void* stream);
 /* pos_words[lo, hi) := 0 then this rank's active rows' panel words at their

@@ -110,6 +110,7 @@ SYMBOLS = {
     "gf2cu_shard_upload": (C.c_int, [_mp, _u64p, _sz, C.c_void_p]),
     "gf2cu_shard_download": (C.c_int, [_mp, _u64p, _sz, C.c_void_p]),
     "gf2cu_shard_begin": (C.c_int, [_mp, C.c_void_p]),
+    "gf2cu_shard_fill_ctr": (C.c_int, [_mp, C.c_uint64, C.c_void_p]),
     "gf2cu_shard_gather": (C.c_int, [_mp, _u64p, _sz, _sz, C.c_void_p]),
     "gf2cu_shard_panel": (C.c_int, [_mp, _sz, _u64p, C.c_int, C.POINTER(C.c_uint32), C.c_void_p]),
     "gf2cu_shard_apply": (C.c_int, [_mp, _sz, _u64p, C.c_void_p]),

@@ -829,6 +829,18 @@ gf2cu_status gf2cu_shard_download(const gf2cu_shard* s, uint64_t* host, size_t h
     return GF2CU_OK;
 }
 
+gf2cu_status gf2cu_shard_fill_ctr(gf2cu_shard* s, uint64_t seed, void* stream) {
+    if (!s) return fail(GF2CU_EINVAL, "null shard");
+    if (!s->m_loc) return GF2CU_OK;
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    gf2cu::shard_fill_ctr_kernel<<<num_sms(s->device) * 8, 256, 0, st>>>(
+        s->data, (u32)s->m_loc, (u32)s->n, (u32)s->Wp, (u32)s->rank, (u32)s->nranks,
+        (u32)s->block, seed);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
 gf2cu_status gf2cu_shard_begin(gf2cu_shard* s, void* stream) {
     if (!s) return fail(GF2CU_EINVAL, "null shard");
     DeviceGuard g(s->device);
@@ -895,6 +907,8 @@ gf2cu_status gf2cu_shard_apply(gf2cu_shard* s, size_t w, uint64_t* pack, void* s
     if (s->m_loc) {
         gf2cu::ShardParams p = shard_params(s);
         p.pack = reinterpret_cast<u64*>(pack);
+        if (w + 1 < s->W)
+            gf2cu::shard_pack_kernel<<<num_sms(s->device) * 4, 256, 0, st>>>(p, (u32)w);
         gf2cu::shard_apply_kernel<<<num_sms(s->device) * 4, gf2cu::kApplyThreads, 0, st>>>(p, (u32)w);
     }
     CU_TRY(cudaGetLastError());

@@ -73,7 +73,6 @@ __global__ void shard_gather_kernel(ShardParams s, u64* posw, u32 lo, u32 hi) {
 __global__ void __launch_bounds__(kApplyThreads) shard_apply_kernel(ShardParams s, u32 w) {
     __shared__ u64 sE[64], sD[64];
     __shared__ u32 sq[64];
-    __shared__ unsigned long long own;
     const u32 r = s.gstate->r, rb = s.gstate->rb;
     for (u32 k = threadIdx.x; k < 64; k += blockDim.x) {
         const bool v = k < rb;
@@ -81,14 +80,7 @@ __global__ void __launch_bounds__(kApplyThreads) shard_apply_kernel(ShardParams 
         sD[k] = v ? s.pout->D[k] : 0ull;
         sq[k] = v ? s.pout->qb[k] : 0u;
     }
-    if (threadIdx.x == 0) own = 0ull;
     __syncthreads();
-    for (u32 k = threadIdx.x; k < rb; k += blockDim.x)
-        if (shard_owner(s.perm[r + k], s.nranks, s.block) == s.rank) atomicOr(&own, 1ull << k);
-    __syncthreads();
-    const u64 ownmask = own;
-    const u32 x0 = (w + 1) & ~7u;
-    const u32 tailw = s.Wpad8 > x0 ? s.Wpad8 - x0 : 0u;
     const u32 w0 = r >> 6, b0 = r & 63;
     const u32 stride = gridDim.x * blockDim.x;
     u32 lo = 0xffffffffu;
@@ -116,10 +108,6 @@ __global__ void __launch_bounds__(kApplyThreads) shard_apply_kernel(ShardParams 
             c |= 1ull << off;
             epart = v & ~low_mask64((int)sq[off] + 1);
             s.retired[l] = 1;
-            // pack the raw tail (words [x0, Wpad8)) before this step changes it
-            const u32 slot = __popcll(ownmask & ((1ull << off) - 1ull));
-            u64* dst = s.pack + (size_t)slot * tailw;
-            for (u32 x = x0; x < s.Wpad8; ++x) dst[x - x0] = *tword(s.mat, s.m_loc, l, x);
         }
         s.info[l] = make_ulonglong2(a, (u64)l);
         const u64 clo = c << b0;
@@ -140,6 +128,46 @@ __global__ void __launch_bounds__(kApplyThreads) shard_apply_kernel(ShardParams 
     for (int o = 16; o > 0; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     if ((threadIdx.x & 31) == 0 && lo != 0xffffffffu) atomicMin(&s.lstate->r, lo);
     if (blockIdx.x == 0 && threadIdx.x == 0) s.lstate->rb = rb;
+}
+
+// Pack this rank's pivot rows' raw tails (words [x0, Wpad8)), slot = rank of
+// t among the owned pivots; runs before shard_apply_kernel touches the rows.
+__global__ void shard_pack_kernel(ShardParams s, u32 w) {
+    const u32 r = s.gstate->r, rb = s.gstate->rb;
+    const u32 x0 = (w + 1) & ~7u;
+    const u32 tailw = s.Wpad8 > x0 ? s.Wpad8 - x0 : 0u;
+    const u64 total = (u64)rb * tailw;
+    for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u32 t = (u32)(e / tailw), x = x0 + (u32)(e - (u64)t * tailw);
+        const u32 g = s.perm[r + t];
+        if (shard_owner(g, s.nranks, s.block) != s.rank) continue;
+        u32 slot = 0;
+        for (u32 k = 0; k < t; ++k) slot += shard_owner(s.perm[r + k], s.nranks, s.block) == s.rank;
+        s.pack[(size_t)slot * tailw + (x - x0)] =
+            *tword(s.mat, s.m_loc, shard_local(g, s.nranks, s.block), x);
+    }
+}
+
+// The ctr generator for this rank's rows (row-major local
+// buffer, stride Wp): the words of global row g, bit-identical to fill_ctr.
+__global__ void shard_fill_ctr_kernel(u64* data, u32 m_loc, u32 n, u32 Wp, u32 rank, u32 nranks,
+                                      u32 block, u64 seed) {
+    const u32 W = (n + 63u) >> 6;
+    const u64 total = (u64)m_loc * Wp;
+    const u64 base = seed << 32;
+    const u64 lastmask = (n & 63u) ? ((1ull << (n & 63u)) - 1ull) : ~0ull;
+    for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u32 l = (u32)(e / Wp), x = (u32)(e - (u64)l * Wp);
+        const u64 g = shard_global(l, rank, nranks, block);
+        u64 v = 0ull;
+        if (x < W) {
+            v = fmix64(base + (g * W + x + 1ull) * 0x9e3779b97f4a7c15ull);
+            if (x == W - 1u) v &= lastmask;
+        }
+        data[e] = v;
+    }
 }
 
 // Scatter owner o's packed pivot tails (its pivots in increasing t order,

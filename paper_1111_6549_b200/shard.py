@@ -204,10 +204,17 @@ class GpuShardEngine:
     def _p(t):
         return C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_uint64))
 
+    def download(self, out: np.ndarray):
+        check(self.L.gf2cu_shard_download(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                          out.shape[1], self._s()))
+
     def upload(self, words: np.ndarray):
         words = np.ascontiguousarray(words, dtype=np.uint64)
         check(self.L.gf2cu_shard_upload(self.h, words.ctypes.data_as(C.POINTER(C.c_uint64)),
                                         words.shape[1] if words.ndim == 2 else 1, self._s()))
+
+    def fill_ctr(self, seed: int):
+        check(self.L.gf2cu_shard_fill_ctr(self.h, C.c_uint64(seed), self._s()))
 
     def begin(self):
         check(self.L.gf2cu_shard_begin(self.h, self._s()))
