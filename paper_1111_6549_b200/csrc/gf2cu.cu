@@ -53,6 +53,7 @@ struct Workspace {
     size_t m = 0, Wp = 0, W = 0;
     u32* perm = nullptr;
     u64* pb = nullptr;
+    u64* pb2 = nullptr;  // look-ahead next-word capture
     ulonglong2* info = nullptr;
     u64* stage = nullptr;
     gf2cu::StepState* state = nullptr;
@@ -72,6 +73,7 @@ struct Workspace {
 void free_ws(Workspace& w) {
     cudaFree(w.perm);
     cudaFree(w.pb);
+    cudaFree(w.pb2);
     cudaFree(w.info);
     cudaFree(w.stage);
     cudaFree(w.state);
@@ -137,6 +139,7 @@ gf2cu_status ensure_ws(gf2cu_matrix* a) {
     w.W = a->W;
     CU_TRY(cudaMalloc(&w.perm, std::max<size_t>(1, m) * sizeof(u32)));
     CU_TRY(cudaMalloc(&w.pb, std::max<size_t>(1, m) * sizeof(u64)));
+    CU_TRY(cudaMalloc(&w.pb2, std::max<size_t>(1, m) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.info, 2 * std::max<size_t>(1, m) * sizeof(ulonglong2)));
     CU_TRY(cudaMalloc(&w.sync, sizeof(gf2cu::SyncState)));
     CU_TRY(cudaMalloc(&w.phase_ns, (8 * (a->W + 1) + 8 + 2 * 64 * 5 + 3 * 160) * sizeof(u64)));
@@ -184,6 +187,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     p.mat = a->alt;
     p.perm = ws.perm;
     p.pb = ws.pb;
+    p.pb2 = (cfg && (cfg->flags & GF2CU_FLAG_MULTI_KERNEL)) ? nullptr : ws.pb2;
     p.info = ws.info;
     p.stage = ws.stage;
     p.state = ws.state;

@@ -74,6 +74,7 @@ struct Params {
     u64* mat;        // tile-major, Wpad8/8 tiles x m rows x 8 words
     u32* perm;       // position -> physical row
     u64* pb;         // panel word per position (current step)
+    u64* pb2;        // next word (w+1) per position, pre-step (look-ahead), may be null
     ulonglong2* info;  // per position: {d, physical row}
     u64* stage;      // tile-major raw pivot rows: tiles x 64 rows x 8 words
     StepState* state;
@@ -205,6 +206,7 @@ __global__ void ple_init_kernel(Params p) {
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
         p.perm[i] = i;
         p.pb[i] = *tword(p.mat, p.m, i, 0);
+        if (p.pb2 && p.W > 1) p.pb2[i] = *tword(p.mat, p.m, i, 1);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         p.state->r = 0;
@@ -233,9 +235,29 @@ struct PanelShared {
     int t, j;
     u64 warp_best[32];
     u64 best;  // (first column << 32) | offset
-    u64 o_red, o_acc, o_raw;
+    u64 o_red, o_acc, o_raw, o_raw2;
     u32 o_phys;
     u32 r;
+    // look-ahead (persistent driver): next step's window words computed here
+    u64 nraw[kWin];     // panel words of the next window (word w+1 after step w)
+    u64 piv2[64];       // pre-step word w+1 of each pivot row
+    u64 opb2[64];       // ... of pivots taken from outside the window
+    u64 dacc[kWin];     // per window slot: d (its combination) and origin
+    u32 dorg[kWin];
+    int cap_ok;
+};
+
+// Look-ahead mode of panel_factor_body (persistent driver): the step's r is
+// tracked by the caller, the window words come from sh.nraw (computed at the
+// end of the previous step), and everything that reads the previous step's
+// look-ahead capture (scans, the writeback, the next window) first waits until
+// all workers have finished it (cap_count >= cap_target).
+struct LookAhead {
+    u32 r;
+    bool have_window;
+    const u32* cap_ctr;
+    u32 cap_target;
+    u32* err;
 };
 
 // All `nthr` threads: scan positions r + [nwin, nrem) reducing each raw panel
@@ -316,11 +338,27 @@ __device__ __forceinline__ bool swap_elim(Col128& x, u64 tm, u64 pl, u64 ph, int
 // of raw pivot rows); per pivot they exchange one ballot and one candidate
 // row per warp through shared memory behind a single 128-thread named
 // barrier. The other warps serve window-miss scans. Returns rb in all threads.
-__device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nthr) {
+// Wait (one thread, result broadcast through sh.cap_ok) until the workers
+// finished the previous step's look-ahead capture.
+__device__ __forceinline__ void la_wait_cap(const LookAhead* la, PanelShared& sh, int bar_id,
+                                            int bar_cnt) {
+    if (!la || sh.cap_ok) return;
+    if (threadIdx.x == 0)
+        sh.cap_ok = spin_geq(la->cap_ctr, la->cap_target, la->err) ? 1 : -1;
+    named_bar(bar_id, bar_cnt);
+}
+
+__device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nthr,
+                                 const LookAhead* la = nullptr) {
     if (threadIdx.x == 0) {
-        const volatile StepState* vs = p.state;
-        sh.r = vs->r + vs->rb;
+        if (la) {
+            sh.r = la->r;
+        } else {
+            const volatile StepState* vs = p.state;
+            sh.r = vs->r + vs->rb;
+        }
         sh.t = 0;
+        sh.cap_ok = la ? (la->cap_target == 0 ? 1 : 0) : 1;
     }
     __syncthreads();
     const u32 r = sh.r;
@@ -360,7 +398,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         u64 red = 0ull, acc = 0ull;
         u32 org = me;  // window offset of the row this slot holds
         if (inwin) {
-            red = ldcg(p.pb + r + me);
+            red = (la && la->have_window) ? sh.nraw[me] : ldcg(p.pb + r + me);
             sh.wraw[me] = red;
             sh.wphys[me] = ldcg(p.perm + r + me);
         }
@@ -414,6 +452,11 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                     aborted = true;
                     break;
                 }
+                la_wait_cap(la, sh, 3, kWin);  // pb of the outside rows is the capture
+                if (la && sh.cap_ok < 0) {
+                    aborted = true;
+                    break;
+                }
                 if (me == 0) {
                     sh.cmd = 0;
                     sh.t = t;
@@ -435,6 +478,11 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 pacc = sh.o_acc;
                 porg = 0x80000000u | (u32)t;
                 if (me == (u32)t) {
+                    if (p.pb2 && w + 1 < p.W) {
+                        // next-word capture follows the displaced window row
+                        sh.opb2[t] = ldcg(p.pb2 + r + P);
+                        p.pb2[r + P] = ldcg(p.pb2 + r + org);
+                    }
                     p.pb[r + P] = sh.wraw[org];
                     p.perm[r + P] = sh.wphys[org];
                     if (p.inv) p.inv[sh.wphys[org]] = r + P;
@@ -458,8 +506,14 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             ++t;
         }
         if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 7] = globaltimer();
-        // the permuted window: raw panel word and physical row per position
+        sh.dacc[me] = acc;
+        sh.dorg[me] = org;
+        // the writeback below may only land after the workers are done with
+        // the previous step (apply, staging and its look-ahead capture)
         named_bar(3, kWin);
+        if (!aborted) la_wait_cap(la, sh, 3, kWin);
+        if (la && sh.cap_ok < 0) aborted = true;
+        // the permuted window: raw panel word and physical row per position
         u64 rw = 0ull;
         u32 ph = 0u;
         if (inwin) {
@@ -521,6 +575,44 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         }
     }
     __syncthreads();
+    if (la && w + 1 < p.W && r + t < p.m) {
+        // ---- next window: word w+1 after step w, for positions
+        //      [r + t, r + t + 128), from the pre-step capture pb2 ----
+        const u32 r1 = r + t;
+        const u32 nwin1 = min((u32)kWin, p.m - r1);
+        // pre-step word w+1 of each pivot row
+        for (u32 k = threadIdx.x; k < t; k += nthr) {
+            const u32 o = sh.dorg[k];
+            sh.piv2[k] = (o & 0x80000000u) ? sh.opb2[o & 63u] : ldcg(p.pb2 + r + o);
+        }
+        __syncthreads();
+        for (u32 k = threadIdx.x; k < nwin1; k += nthr) {
+            const u32 q = r1 + k;  // position
+            u64 d, pre;
+            if (q - r < nwin) {
+                d = sh.dacc[q - r];
+                pre = ldcg(p.pb2 + r + sh.dorg[q - r]);
+            } else {
+                // a row entering the window: its combination for step w
+                u64 v = ldcg(p.pb + q);
+                d = 0ull;
+                for (u32 s2 = 0; s2 < t; ++s2) {
+                    const u64 msk = 0ull - ((v >> sh.q[s2]) & 1ull);
+                    v ^= sh.E[s2] & msk;
+                    d ^= sh.D[s2] & msk;
+                }
+                pre = ldcg(p.pb2 + q);
+            }
+            u64 x = pre;
+#pragma unroll 8
+            for (u32 s2 = 0; s2 < 64; ++s2) {
+                if (s2 >= t) break;
+                x ^= sh.piv2[s2] & (0ull - ((d >> s2) & 1ull));
+            }
+            sh.nraw[k] = x;
+        }
+        __syncthreads();
+    }
     return t;
 }
 
@@ -693,9 +785,15 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
     const u32 cap_word = w + 1;
-    const bool capture = (cap_word >> 3) == tile;
-    const bool cap_lane = capture && ((cap_word & 7u) >> 1) == ch;
+    const bool capture1 = (cap_word >> 3) == tile;
+    const bool cap_lane = capture1 && ((cap_word & 7u) >> 1) == ch;
     const bool cap_hi = (cap_word & 1u) != 0;
+    // look-ahead driver: word w+2 as well (the panel CTA's next-window input)
+    const u32 cap2_word = w + 2;
+    const bool capture2 = p.pb2 != nullptr && cap2_word < p.W && (cap2_word >> 3) == tile;
+    const bool cap2_lane = capture2 && ((cap2_word & 7u) >> 1) == ch;
+    const bool cap2_hi = (cap2_word & 1u) != 0;
+    const bool capture = capture1 || capture2;
     const u32 lane_row = wid * 8u + rg;
     u64* tbase = p.mat + (((size_t)tile * p.m) << 3) + 2u * ch;
     const u32 rend = row0 + cnt;
@@ -749,6 +847,7 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
                 *reinterpret_cast<ulonglong2*>(tbase + ((size_t)infC[k].y << 3)) = valC[k];
             }
             if (cap_lane && ri < rend) p.pb[r + ri] = cap_hi ? valC[k].y : valC[k].x;
+            if (cap2_lane && ri < rend) p.pb2[r + ri] = cap2_hi ? valC[k].y : valC[k].x;
         }
 #pragma unroll
         for (int k = 0; k < kUnroll; ++k) {

@@ -46,14 +46,21 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
 
     if (blockIdx.x == 0) {
         // ------------------------------------------------------ panel CTA
+        // Look-ahead: step w+1's window words are computed at the end of step
+        // w, so the next factorization starts at once; only its scans and its
+        // writeback wait for the workers' look-ahead capture of step w.
+        LookAhead la{0u, false, &sy->cap_count, 0u, &sy->error};
         for (u32 w = 0; w < nsteps; ++w) {
-            if (w > 0 && !cta_wait(sy, &sy->cap_count, nworkers * w, s_ok)) return;
+            la.cap_target = nworkers * w;
             stamp(p, w, 0);
-            panel_factor_body(p, w, psh, blockDim.x);
+            const u32 rb = panel_factor_body(p, w, psh, blockDim.x, &la);
             stamp(p, w, 1);
-            const bool done = psh.r >= p.m;
+            if (*(volatile u32*)&sy->error) return;
+            const bool done = la.r >= p.m;
             cta_arrive(&sy->panel_done);
             if (done) return;
+            la.r += rb;
+            la.have_window = true;
         }
         return;
     }
@@ -62,8 +69,9 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
     const u32 wk = blockIdx.x - 1;
     for (u32 w = 0; w < nsteps; ++w) {
         if (!cta_wait(sy, &sy->panel_done, w + 1, s_ok)) return;
-        const volatile StepState* vs = p.state;
-        const u32 r = vs->r, rb = vs->rb;
+        // this step's r / rb (the shared state word may already belong to the
+        // next step: the panel CTA runs ahead)
+        const u32 r = *(volatile u32*)&p.rhist[w], rb = *(volatile u32*)&p.rbhist[w];
         if (r >= p.m) return;
         Params q = p;
         q.info = p.info + (size_t)(w & 1u) * p.m;
@@ -88,20 +96,25 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         if (wk == 0) stamp(p, w, 3);
         const u32 tile0 = (w + 1) >> 3;
         if (w + 1 < p.W) {
-            // look-ahead tile: own slab, then release the panel CTA
+            // look-ahead tiles (those holding words w+1 and w+2): own slab,
+            // then release the panel CTA
+            const u32 tcap = (w + 2 < p.W) ? ((w + 2) >> 3) : tile0;
             if (hi > lo) {
-                if (rb > 0) {
-                    build_tables(q, smem, tile0, w, rb);
-                    __syncthreads();
+                for (u32 tt = tile0; tt <= tcap; ++tt) {
+                    if (rb > 0) {
+                        __syncthreads();
+                        build_tables(q, smem, tt, w, rb);
+                        __syncthreads();
+                    }
+                    trail_rows(q, smem, w, r, tt, lo - r, hi - lo);
                 }
-                trail_rows(q, smem, w, r, tile0, lo - r, hi - lo);
             }
             cta_arrive(&sy->cap_count);
             if (wk == 0) stamp(p, w, 4);
             // remaining tiles: linear share
-            const u32 nt = (p.Wpad8 >> 3) - tile0 - 1;
+            const u32 nt = (p.Wpad8 >> 3) - tcap - 1;
             const u64 total = (u64)nt * nrows;
-            trail_share(q, smem, w, r, rb, tile0 + 1, total * wk / nworkers,
+            trail_share(q, smem, w, r, rb, tcap + 1, total * wk / nworkers,
                         total * (wk + 1) / nworkers);
         } else {
             cta_arrive(&sy->cap_count);
