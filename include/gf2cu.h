@@ -135,6 +135,33 @@ gf2cu_status gf2cu_ple_device(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swa
                               gf2cu_stats* stats);
 
 /* ------------------------------------------------------------------ */
+/* Echelon forms and the upper-triangular solve     */
+/* ------------------------------------------------------------------ */
+/* Replaces gf2::rref_from_ple(MatrixView a, const PleOutcome& out, bool full,
+ * const MulConfig&) (ple.hpp:318-329). `a` holds the in-place result of a
+ * full PLE (block_iterative_ple / recursive_ple, processed == nrows) whose
+ * pivot columns are q[0..rank); the outcome's col_swaps are implied by q
+ * (any compression-swap list of that PLE undoes to the same matrix). On
+ * return the top `rank` rows hold the row echelon form (reduced if full),
+ * the rows below are zero. GF2CU_EINVAL if q is not strictly increasing
+ * inside the matrix or rank exceeds min(m, n) (check_pivots, ple.hpp:299). */
+gf2cu_status gf2cu_rref_from_ple(const gf2cu_view* a, const size_t* q, size_t rank, int full,
+                                 const gf2cu_cfg* cfg);
+gf2cu_status gf2cu_rref_from_ple_device(gf2cu_matrix* a, const size_t* q, size_t rank, int full,
+                                        void* stream);
+/* Replaces gf2::echelonize(a, EchelonStrategy::ple_iterative, full, cfg)
+ * (m4ri.hpp:88-98): block_iterative_ple followed by rref_from_ple, the matrix
+ * resident on the device in between. *rank = the rank. */
+gf2cu_status gf2cu_echelonize(const gf2cu_view* a, int full, const gf2cu_cfg* cfg, size_t* rank);
+gf2cu_status gf2cu_echelonize_device(gf2cu_matrix* a, int full, const gf2cu_cfg* cfg, size_t* rank);
+/* Replaces gf2::trsm_upper_left_unit(ConstMatrixView u, MatrixView b,
+ * const MulConfig&) (multiply.hpp:314-335): b <- u^-1 b for the unit upper
+ * triangle of the r x r view u (bits strictly above the diagonal read, the
+ * rest ignored); b is r x ncols. GF2CU_EINVAL on a dimension mismatch. */
+gf2cu_status gf2cu_trsm_upper_left_unit(const gf2cu_view* u, const gf2cu_view* b,
+                                        const gf2cu_cfg* cfg);
+
+/* ------------------------------------------------------------------ */
 /* Row-sharded multi-GPU PLE (one process per GPU, host-driven steps)   */
 /* ------------------------------------------------------------------ */
 /* Global row g lives on rank (g / block) % nranks, local index

@@ -82,14 +82,79 @@ gf2::PleOutcome block_iterative_ple(View a, const Cfg& cfg = {}, const DeviceOpt
     return out;
 }
 
-// echelonize(a, EchelonStrategy::ple_iterative, full) (m4ri.hpp:95-98) with the
-// decomposition on the B200 and the reference's rref_from_ple on the host.
+namespace detail {
+
+template <class View>
+gf2cu_view to_view(View a) {
+    gf2cu_view v;
+    v.data = a.nrows() ? a.row_words(0) : nullptr;
+    v.stride = a.stride();
+    v.col_off = a.col_offset();
+    v.nrows = a.nrows();
+    v.ncols = a.ncols();
+    return v;
+}
+
+template <class Cfg>
+gf2cu_cfg to_cfg(const Cfg& cfg, const DeviceOptions& dev) {
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    c.k = cfg.k;
+    c.k_scale = cfg.k_scale;
+    c.table_count = cfg.table_count;
+    c.device = dev.device;
+    c.stream = dev.stream;
+    return c;
+}
+
+}  // namespace detail
+
+// rref_from_ple (ple.hpp:318-329) on the B200: `a` holds the in-place result
+// `out` describes (a complete decomposition, out.processed == a.nrows()); the
+// top out.rank rows become the echelon form (reduced if `full`), rows below
+// zero. Throws std::invalid_argument for a corrupt outcome (check_pivots).
+template <class View = gf2::MatrixView>
+void rref_from_ple(View a, const gf2::PleOutcome& out, bool full = true,
+                   const DeviceOptions& dev = {}) {
+    if (out.processed != a.nrows())
+        throw std::invalid_argument("rref_from_ple on the device needs processed == nrows");
+    if (out.q.size() != out.rank) throw std::invalid_argument("rank disagrees with pivot list");
+    gf2cu_view v = detail::to_view(a);
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    c.device = dev.device;
+    c.stream = dev.stream;
+    std::vector<std::size_t> q(out.q.begin(), out.q.end());
+    detail::throw_status(gf2cu_rref_from_ple(&v, q.data(), out.rank, full ? 1 : 0, &c));
+}
+
+// echelonize(a, EchelonStrategy::ple_iterative, full) (m4ri.hpp:95-98): the
+// decomposition and rref_from_ple both on the B200, one upload and download.
 template <class View = gf2::MatrixView, class Cfg = gf2::PleConfig>
 std::size_t echelonize_ple_iterative(View a, bool full = true, const Cfg& cfg = {},
                                      const DeviceOptions& dev = {}) {
-    gf2::PleOutcome out = block_iterative_ple(a, cfg, dev);
-    gf2::rref_from_ple(a, out, full, cfg.mul);
-    return out.rank;
+    gf2cu_view v = detail::to_view(a);
+    gf2cu_cfg c = detail::to_cfg(cfg, dev);
+    std::size_t rank = 0;
+    detail::throw_status(gf2cu_echelonize(&v, full ? 1 : 0, &c, &rank));
+    return rank;
+}
+
+// trsm_upper_left_unit (multiply.hpp:314-335) on the B200: b <- u^-1 b.
+template <class CView = gf2::ConstMatrixView, class View = gf2::MatrixView>
+void trsm_upper_left_unit(CView u, View b, const DeviceOptions& dev = {}) {
+    gf2cu_view uv;
+    uv.data = const_cast<uint64_t*>(u.nrows() ? u.row_words(0) : nullptr);
+    uv.stride = u.stride();
+    uv.col_off = u.col_offset();
+    uv.nrows = u.nrows();
+    uv.ncols = u.ncols();
+    gf2cu_view bv = detail::to_view(b);
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    c.device = dev.device;
+    c.stream = dev.stream;
+    detail::throw_status(gf2cu_trsm_upper_left_unit(&uv, &bv, &c));
 }
 
 }  // namespace b200

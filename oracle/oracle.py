@@ -55,6 +55,10 @@ def lib():
         L.orc_undo_col_swaps.restype = None
         L.orc_mul.argtypes = [_u64p, _sz, _sz, _sz, _u64p, _sz, _sz, _u64p, _sz]
         L.orc_mul.restype = None
+        L.orc_echelonize.argtypes = [_u64p, _sz, _sz, _sz, C.c_int]
+        L.orc_echelonize.restype = _sz
+        L.orc_trsm_upper.argtypes = [_u64p, _sz, _sz, _u64p, _sz, _sz]
+        L.orc_trsm_upper.restype = None
         _lib = L
     return _lib
 
@@ -89,6 +93,10 @@ def ref():
         R.ref_rref_from_ple.restype = C.c_int
         R.ref_reconstructs.argtypes = [_u64p, _u64p, _sz, _sz, _sz, _sz, _szp, _szp, _szp, _sz]
         R.ref_reconstructs.restype = C.c_int
+        R.ref_echelonize.argtypes = [_u64p, _sz, _sz, _sz, C.c_int, C.c_int]
+        R.ref_echelonize.restype = C.c_longlong
+        R.ref_trsm_upper_left_unit.argtypes = [_u64p, _sz, _sz, _u64p, _sz, _sz]
+        R.ref_trsm_upper_left_unit.restype = C.c_int
         _ref = R
     return _ref
 
@@ -251,3 +259,29 @@ def ref_reconstructs(orig: np.ndarray, dec: np.ndarray, m: int, n: int, out: Out
     if rc < 0:
         raise RuntimeError("reference reconstruction threw")
     return rc == 1
+
+
+def echelonize(a: np.ndarray, m: int, n: int, full: bool = True) -> int:
+    """orc_echelonize: naive_echelonize restated (ple.hpp:362-380), in place."""
+    return int(lib().orc_echelonize(_u64(a), m, n, a.shape[1], int(full)))
+
+
+def trsm_upper(u: np.ndarray, r: int, b: np.ndarray, n: int) -> None:
+    """orc_trsm_upper: b <- u^-1 b (multiply.hpp:314-335 restated), in place."""
+    lib().orc_trsm_upper(_u64(u), r, u.shape[1], _u64(b), n, b.shape[1])
+
+
+STRATEGIES = {"naive": 0, "m4ri": 1, "ple_iterative": 2, "ple_recursive": 3}
+
+
+def ref_echelonize(a: np.ndarray, m: int, n: int, strategy: str = "ple_iterative",
+                   full: bool = True) -> int:
+    rc = ref().ref_echelonize(_u64(a), m, n, a.shape[1], STRATEGIES[strategy], int(full))
+    if rc < 0:
+        raise RuntimeError("reference echelonize threw")
+    return int(rc)
+
+
+def ref_trsm_upper_left_unit(u: np.ndarray, r: int, b: np.ndarray, n: int) -> None:
+    if ref().ref_trsm_upper_left_unit(_u64(u), r, u.shape[1], _u64(b), n, b.shape[1]) != 0:
+        raise RuntimeError("reference trsm_upper_left_unit threw")

@@ -280,3 +280,60 @@ void orc_mul(const word* A, size_t m, size_t l, size_t sa, const word* B, size_t
             }
     }
 }
+
+/* naive_echelonize (ple.hpp:362-380): word-at-a-time Gauss-Jordan. Per
+ * column c the pivot is the first row >= r holding a 1, swapped to row r;
+ * then every other row (full) or every lower row (!full) with bit c gets the
+ * pivot row added from column c on (row_add_from, bit_matrix.hpp:273-279).
+ * The reduced form is unique, and the !full form is the PLE's E factor with
+ * zero rows below (same pivot choice and elimination as orc_ple). Returns
+ * the rank. */
+size_t orc_echelonize(word* A, size_t m, size_t n, size_t stride, int full) {
+    const size_t W = (n + 63) / 64;
+    size_t r = 0;
+    for (size_t c = 0; c < n && r < m; ++c) {
+        const size_t wc = c >> 6;
+        const word bc = (word)1 << (c & 63);
+        size_t p = r;
+        while (p < m && !(A[p * stride + wc] & bc)) ++p;
+        if (p == m) continue;
+        if (p != r) {
+            word* x = A + r * stride;
+            word* y = A + p * stride;
+            for (size_t w = 0; w < W; ++w) {
+                const word t = x[w];
+                x[w] = y[w];
+                y[w] = t;
+            }
+        }
+        const word* prow = A + r * stride;
+        const word first = prow[wc] & ~low_mask(c & 63); /* columns >= c */
+        for (size_t i = full ? 0 : r + 1; i < m; ++i) {
+            if (i == r) continue;
+            word* row = A + i * stride;
+            if (!(row[wc] & bc)) continue;
+            row[wc] ^= first;
+            for (size_t w = wc + 1; w < W; ++w) row[w] ^= prow[w];
+        }
+        ++r;
+    }
+    return r;
+}
+
+/* trsm_upper_left_unit (multiply.hpp:314-335) as plain back substitution:
+ * B <- U^-1 B for the unit upper triangle of the r x r matrix U (only bits
+ * strictly above the diagonal read). Row i (bottom-up) receives every row
+ * j > i of the already-solved B with U[i][j] = 1 (the <= 64 branch at
+ * :322-331 for any r). */
+void orc_trsm_upper(const word* U, size_t r, size_t su, word* B, size_t n, size_t sb) {
+    const size_t W = (n + 63) / 64;
+    for (size_t i = r; i-- > 0;) {
+        word* bi = B + i * sb;
+        const word* ui = U + i * su;
+        for (size_t j = i + 1; j < r; ++j)
+            if ((ui[j >> 6] >> (j & 63)) & 1) {
+                const word* bj = B + j * sb;
+                for (size_t w = 0; w < W; ++w) bi[w] ^= bj[w];
+            }
+    }
+}

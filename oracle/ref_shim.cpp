@@ -175,6 +175,32 @@ int ref_rref_from_ple(std::uint64_t* words, std::size_t m, std::size_t n, std::s
     }
 }
 
+// gf2::echelonize(a, strategy, full) (m4ri.hpp:88-105); strategy 0 naive,
+// 1 m4ri, 2 ple_iterative, 3 ple_recursive. Returns the rank or -1.
+long long ref_echelonize(std::uint64_t* words, std::size_t m, std::size_t n, std::size_t stride,
+                         int strategy, int full) {
+    try {
+        const gf2::EchelonStrategy s = strategy == 0   ? gf2::EchelonStrategy::naive
+                                       : strategy == 1 ? gf2::EchelonStrategy::m4ri
+                                       : strategy == 2 ? gf2::EchelonStrategy::ple_iterative
+                                                       : gf2::EchelonStrategy::ple_recursive;
+        return (long long)gf2::echelonize(view_of(words, m, n, stride), s, full != 0);
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// gf2::trsm_upper_left_unit (multiply.hpp:314-335): b <- u^-1 b.
+int ref_trsm_upper_left_unit(const std::uint64_t* u, std::size_t r, std::size_t su,
+                             std::uint64_t* b, std::size_t n, std::size_t sb) {
+    try {
+        gf2::trsm_upper_left_unit(gf2::ConstMatrixView(u, su, 0, r, r), view_of(b, r, n, sb));
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // P*L*E reconstruction check (test_ple.cpp:38-50 / acceptance_main.cpp:97-108):
 // returns 1 when P*L*E equals `orig` on the first `processed` (= m) rows.
 int ref_reconstructs(const std::uint64_t* orig, const std::uint64_t* decomposed, std::size_t m,

@@ -16,14 +16,20 @@ from .ple import (  # noqa: F401
     RowPermutation,
     block_iterative_ple,
     device_count,
+    echelonize,
+    extract_e,
+    extract_l,
     fill_ctr,
     fill_random,
     host_checksum,
+    rref_from_ple,
+    trsm_upper_left_unit,
     words_per_row,
 )
 
 __all__ = [
     "BitMatrix", "ColSwap", "DeviceMatrix", "MatrixView", "PleConfig", "PleOutcome",
     "RowPermutation", "block_iterative_ple", "device_count", "fill_ctr", "fill_random",
-    "host_checksum", "words_per_row", "build", "load",
+    "host_checksum", "words_per_row", "build", "load", "echelonize", "extract_e", "extract_l",
+    "rref_from_ple", "trsm_upper_left_unit",
 ]

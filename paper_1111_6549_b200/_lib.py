@@ -104,6 +104,12 @@ SYMBOLS = {
     "gf2cu_matrix_checksum": (C.c_int, [_mp, _u64p, C.c_void_p]),
     "gf2cu_ple_device": (C.c_int, [_mp, C.POINTER(gf2cu_cfg), _szp, _szp, _szp,
                                    C.POINTER(gf2cu_colswap), _szp, C.POINTER(gf2cu_stats)]),
+    "gf2cu_rref_from_ple": (C.c_int, [C.POINTER(gf2cu_view), _szp, _sz, C.c_int, C.POINTER(gf2cu_cfg)]),
+    "gf2cu_rref_from_ple_device": (C.c_int, [_mp, _szp, _sz, C.c_int, C.c_void_p]),
+    "gf2cu_echelonize": (C.c_int, [C.POINTER(gf2cu_view), C.c_int, C.POINTER(gf2cu_cfg), _szp]),
+    "gf2cu_echelonize_device": (C.c_int, [_mp, C.c_int, C.POINTER(gf2cu_cfg), _szp]),
+    "gf2cu_trsm_upper_left_unit": (C.c_int, [C.POINTER(gf2cu_view), C.POINTER(gf2cu_view),
+                                             C.POINTER(gf2cu_cfg)]),
     "gf2cu_shard_create": (C.c_int, [_sz, _sz, C.c_int, C.c_int, _sz, C.c_int, C.POINTER(_mp)]),
     "gf2cu_shard_destroy": (C.c_int, [_mp]),
     "gf2cu_shard_info": (C.c_int, [_mp, _szp, _szp]),

@@ -21,6 +21,7 @@
 #include "ple_kernels.cuh"
 #include "ple_persistent.cuh"
 #include "ple_shard.cuh"
+#include "rref_kernels.cuh"
 
 using gf2cu::u32;
 using gf2cu::u64;
@@ -115,12 +116,48 @@ int num_sms(int dev) {
 
 }  // namespace
 
+namespace {
+
+// Device buffers of the reduced-echelon / upper-triangular solve, grown on
+// demand and kept with the matrix handle.
+struct RrefWs {
+    u64* U = nullptr;     size_t U_words = 0;
+    u64* N = nullptr;     size_t N_words = 0;
+    u64* src = nullptr;   size_t src_words = 0;  // trsm operands (row-major)
+    u32* idx = nullptr;   size_t idx_words = 0;  // q | np | usrc | nsrc | npos0
+    u64* npmask = nullptr; size_t npmask_words = 0;
+};
+
+void free_rref(RrefWs& w) {
+    cudaFree(w.U);
+    cudaFree(w.N);
+    cudaFree(w.src);
+    cudaFree(w.idx);
+    cudaFree(w.npmask);
+    w = RrefWs{};
+}
+
+template <class T>
+cudaError_t grow(T** ptr, size_t* have, size_t need) {
+    need = std::max<size_t>(need, 1);
+    if (*have >= need) return cudaSuccess;
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    *have = 0;
+    cudaError_t e = cudaMalloc(ptr, need * sizeof(T));
+    if (e == cudaSuccess) *have = need;
+    return e;
+}
+
+}  // namespace
+
 struct gf2cu_matrix {
     size_t m = 0, n = 0, W = 0, Wp = 0;
     int device = 0;
     u64* data = nullptr;
     u64* alt = nullptr;  // tile-major working copy used by the factorization
     Workspace ws;
+    RrefWs rw;
     cudaStream_t own = nullptr;
 };
 
@@ -407,6 +444,223 @@ void write_bits(u64* row, size_t lo, size_t count, u64 bits) {
     }
 }
 
+// check_pivots (ple.hpp:299-307): q strictly increasing, inside the matrix.
+gf2cu_status check_pivots(const size_t* q, size_t rank, size_t m, size_t n) {
+    if (rank > std::min(m, n)) return fail(GF2CU_EINVAL, "rank exceeds the matrix dimensions");
+    if (rank && !q) return fail(GF2CU_EINVAL, "null pivot list");
+    for (size_t j = 0; j < rank; ++j)
+        if (q[j] >= n || (j > 0 && q[j] <= q[j - 1]))
+            return fail(GF2CU_EINVAL, "pivot columns are not strictly increasing");
+    return GF2CU_OK;
+}
+
+// X = U^-1 N over the prepared RrefParams (U, N filled): bottom-up 64-row
+// blocks, in-block solve then the Gray-table update of the rows above.
+gf2cu_status solve_upper(gf2cu_matrix* a, const gf2cu::RrefParams& p, cudaStream_t s) {
+    static bool attr_set[64] = {false};
+    if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
+        CU_TRY(cudaFuncSetAttribute(gf2cu::rref_update_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, gf2cu::kTableBytes));
+        attr_set[a->device] = true;
+    }
+    const int sms = num_sms(a->device);
+    const u32 nblk = p.R / 64;
+    const u32 solve_grid = (p.Wn + 7) / 8;
+    for (u32 J = nblk; J-- > 0;) {
+        gf2cu::rref_block_solve_kernel<<<solve_grid, 256, 0, s>>>(p, J);
+        if (J > 0) {
+            const u64 units = (u64)(p.WnPad8 / 8) * 64u * J;
+            const int grid = (int)std::min<u64>((u64)sms, std::max<u64>(1, units / 256));
+            gf2cu::rref_update_kernel<<<grid, gf2cu::kTrailThreads, gf2cu::kTableBytes, s>>>(p, J);
+        }
+    }
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+// rref_from_ple (ple.hpp:318-329) on the device copy in place: a->data must
+// hold the in-place PLE result whose pivot columns are q[0..rank).
+gf2cu_status run_rref(gf2cu_matrix* a, const size_t* q, size_t rank, bool full, cudaStream_t s) {
+    const size_t m = a->m, n = a->n, W = a->W;
+    gf2cu_status st = check_pivots(q, rank, m, n);
+    if (st != GF2CU_OK) return st;
+    if (m == 0 || n == 0) return GF2CU_OK;
+    RrefWs& rw = a->rw;
+    const int sms = num_sms(a->device);
+    const size_t r = rank, ncn = n - r;
+    const size_t R = (r + 63) / 64 * 64, Wu = R / 64, Wn = (ncn + 63) / 64;
+    const size_t WnPad8 = (Wn + 7) / 8 * 8;
+    // host-side index arrays: q | np | usrc | nsrc | npos0, and npmask
+    std::vector<u32> idx(r + ncn + Wu + Wn + W);
+    std::vector<u64> npmask(W, 0ull);
+    u32* hq = idx.data();
+    u32* hnp = hq + r;
+    u32* husrc = hnp + ncn;
+    u32* hnsrc = husrc + Wu;
+    u32* hnpos0 = hnsrc + Wn;
+    {
+        size_t j = 0, k = 0;
+        for (size_t c = 0; c < n; ++c) {
+            if (j < r && q[j] == c) {
+                hq[j++] = (u32)c;
+            } else {
+                hnp[k++] = (u32)c;
+                npmask[c >> 6] |= 1ull << (c & 63);
+            }
+        }
+        size_t before = 0;
+        for (size_t y = 0; y < W; ++y) {
+            hnpos0[y] = (u32)before;
+            before += (size_t)__builtin_popcountll(npmask[y]);
+        }
+        auto contiguous = [](const u32* cols, size_t k0, size_t cnt) -> u32 {
+            return cols[k0 + cnt - 1] - cols[k0] == cnt - 1 ? cols[k0] : gf2cu::kNone;
+        };
+        for (size_t x = 0; x < Wu; ++x)
+            husrc[x] = 64 * x < r ? contiguous(hq, 64 * x, std::min<size_t>(64, r - 64 * x)) : 0u;
+        for (size_t x = 0; x < Wn; ++x) hnsrc[x] = contiguous(hnp, 64 * x, std::min<size_t>(64, ncn - 64 * x));
+    }
+    CU_TRY(grow(&rw.idx, &rw.idx_words, idx.size()));
+    CU_TRY(grow(&rw.npmask, &rw.npmask_words, W));
+    CU_TRY(cudaMemcpyAsync(rw.idx, idx.data(), idx.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+    CU_TRY(cudaMemcpyAsync(rw.npmask, npmask.data(), W * sizeof(u64), cudaMemcpyHostToDevice, s));
+    const u32* dq = rw.idx;
+    if (!full) {
+        gf2cu::rref_echelon_kernel<<<sms * 8, 256, 0, s>>>(a->data, dq, (u32)m, (u32)W, (u32)a->Wp, (u32)r);
+        CU_TRY(cudaGetLastError());
+        return GF2CU_OK;
+    }
+    gf2cu::RrefParams p{};
+    p.a = a->data;
+    p.out = a->data;
+    p.q = dq;
+    p.np = dq + r;
+    p.usrc = dq + r + ncn;
+    p.nsrc = p.usrc + Wu;
+    p.npos0 = p.nsrc + Wn;
+    p.npmask = rw.npmask;
+    p.m = (u32)m;
+    p.n = (u32)n;
+    p.W = (u32)W;
+    p.Wp = (u32)a->Wp;
+    p.Wa = (u32)W;
+    p.Wpa = (u32)a->Wp;
+    p.r = (u32)r;
+    p.R = (u32)R;
+    p.Wu = (u32)Wu;
+    p.Wn = (u32)Wn;
+    p.WnPad8 = (u32)WnPad8;
+    p.ncn = (u32)ncn;
+    if (r > 0 && ncn > 0) {
+        CU_TRY(grow(&rw.U, &rw.U_words, Wu * R));
+        CU_TRY(grow(&rw.N, &rw.N_words, WnPad8 * R));
+        CU_TRY(cudaMemsetAsync(rw.U, 0, Wu * R * sizeof(u64), s));
+        CU_TRY(cudaMemsetAsync(rw.N, 0, WnPad8 * R * sizeof(u64), s));
+        p.U = rw.U;
+        p.N = rw.N;
+        gf2cu::rref_gather_kernel<<<sms * 8, 256, 0, s>>>(p, 1);
+        CU_TRY(cudaGetLastError());
+        st = solve_upper(a, p, s);
+        if (st != GF2CU_OK) return st;
+    }
+    gf2cu::rref_scatter_kernel<<<sms * 8, 256, 0, s>>>(p);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+// Host view <-> the per-thread cached device matrix of its shape: upload,
+// body(matrix, stream), download, with unaligned windows packed host-side.
+template <class Body>
+gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* stats, Body&& body) {
+    const size_t m = v->nrows, n = v->ncols;
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    if (cfg) c = *cfg;
+    // One cached device matrix per host thread: repeated calls on the same
+    // shape reuse HBM buffers and workspace instead of re-allocating.
+    struct Cache {
+        gf2cu_matrix* a = nullptr;
+        ~Cache() { gf2cu_matrix_destroy(a); }
+    };
+    thread_local Cache cache;
+    if (cache.a && (cache.a->m != m || cache.a->n != n || cache.a->device != c.device)) {
+        gf2cu_matrix_destroy(cache.a);
+        cache.a = nullptr;
+    }
+    gf2cu_status st;
+    if (!cache.a) {
+        st = gf2cu_matrix_create(m, n, c.device, &cache.a);
+        if (st != GF2CU_OK) return st;
+    }
+    gf2cu_matrix* a = cache.a;
+    DeviceGuard g(c.device);
+    cudaStream_t s = pick_stream(a, c.stream);
+    const size_t W = a->W;
+    std::vector<u64> packed;
+    const bool aligned = (v->col_off & 63) == 0 && (n & 63) == 0;
+    cudaError_t e = cudaSuccess;
+    if (aligned) {
+        e = cudaMemcpy2DAsync(a->data, a->Wp * 8, v->data + (v->col_off >> 6), v->stride * 8, W * 8,
+                              m, cudaMemcpyHostToDevice, s);
+    } else {
+        packed.assign(m * W, 0ull);
+        for (size_t i = 0; i < m; ++i) {
+            const u64* row = reinterpret_cast<const u64*>(v->data) + i * v->stride;
+            for (size_t x = 0; x < W; ++x) {
+                const size_t take = std::min<size_t>(64, n - 64 * x);
+                packed[i * W + x] = read_bits(row, v->col_off + 64 * x, take);
+            }
+        }
+        e = cudaMemcpy2DAsync(a->data, a->Wp * 8, packed.data(), W * 8, W * 8, m,
+                              cudaMemcpyHostToDevice, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "upload");
+    c.stream = s;
+    st = body(a, c);
+    if (st == GF2CU_OK) {
+        if (aligned) {
+            e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6), v->stride * 8, a->data, a->Wp * 8,
+                                  W * 8, m, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        } else {
+            e = cudaMemcpy2DAsync(packed.data(), W * 8, a->data, a->Wp * 8, W * 8, m,
+                                  cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e == cudaSuccess)
+                for (size_t i = 0; i < m; ++i) {
+                    u64* row = reinterpret_cast<u64*>(v->data) + i * v->stride;
+                    for (size_t x = 0; x < W; ++x) {
+                        const size_t take = std::min<size_t>(64, n - 64 * x);
+                        write_bits(row, v->col_off + 64 * x, take, packed[i * W + x]);
+                    }
+                }
+        }
+        if (e != cudaSuccess) st = cuda_fail(e, "download");
+        if (stats) {
+            stats->h2d_bytes = double(m) * W * 8;
+            stats->d2h_bytes = double(m) * W * 8;
+        }
+    }
+    return st;
+}
+
+gf2cu_status check_view(const gf2cu_view* v) {
+    if (!v) return fail(GF2CU_EINVAL, "null argument");
+    if (v->nrows && v->ncols && !v->data) return fail(GF2CU_EINVAL, "null data");
+    if (v->nrows && v->ncols && v->stride * 64 < v->col_off + v->ncols)
+        return fail(GF2CU_ERANGE, "view window exceeds its row stride");
+    return GF2CU_OK;
+}
+
+// PLE then rref_from_ple on the device copy (echelonize, m4ri.hpp:95-98).
+gf2cu_status run_echelonize(gf2cu_matrix* a, const gf2cu_cfg* cfg, bool full, size_t* rank) {
+    const size_t mn = std::min(a->m, a->n);
+    std::vector<size_t> sw(std::max<size_t>(1, mn)), q(std::max<size_t>(1, mn));
+    gf2cu_status st = run_ple(a, cfg, sw.data(), q.data(), rank, nullptr, nullptr, nullptr);
+    if (st != GF2CU_OK) return st;
+    return run_rref(a, q.data(), *rank, full, pick_stream(a, cfg ? cfg->stream : nullptr));
+}
+
 }  // namespace
 
 extern "C" {
@@ -476,6 +730,7 @@ gf2cu_status gf2cu_matrix_destroy(gf2cu_matrix* a) {
     cudaFree(a->data);
     cudaFree(a->alt);
     free_ws(a->ws);
+    free_rref(a->rw);
     if (a->own) cudaStreamDestroy(a->own);
     delete a;
     return GF2CU_OK;
@@ -581,12 +836,11 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
                        size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
                        gf2cu_stats* stats) {
     if (!v || !rank) return fail(GF2CU_EINVAL, "null argument");
+    gf2cu_status st = check_view(v);
+    if (st != GF2CU_OK) return st;
     const size_t m = v->nrows, n = v->ncols;
-    if (m && n && !v->data) return fail(GF2CU_EINVAL, "null data");
-    if (m && n && v->stride * 64 < v->col_off + n)
-        return fail(GF2CU_ERANGE, "view window exceeds its row stride");
     if ((!swaps || !q) && std::min(m, n) > 0) return fail(GF2CU_EINVAL, "null outputs");
-    gf2cu_status st = check_cfg(cfg);
+    st = check_cfg(cfg);
     if (st != GF2CU_OK) return st;
     if (m == 0 || n == 0) {
         *rank = 0;
@@ -594,74 +848,111 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
         if (stats) std::memset(stats, 0, sizeof(*stats));
         return GF2CU_OK;
     }
-    gf2cu_cfg c;
-    gf2cu_default_config(&c);
-    if (cfg) c = *cfg;
-    // One cached device matrix per host thread: repeated calls on the same
-    // shape reuse HBM buffers and workspace instead of re-allocating.
-    struct Cache {
-        gf2cu_matrix* a = nullptr;
-        ~Cache() { gf2cu_matrix_destroy(a); }
-    };
-    thread_local Cache cache;
-    if (cache.a && (cache.a->m != m || cache.a->n != n || cache.a->device != c.device)) {
-        gf2cu_matrix_destroy(cache.a);
-        cache.a = nullptr;
-    }
-    if (!cache.a) {
-        st = gf2cu_matrix_create(m, n, c.device, &cache.a);
-        if (st != GF2CU_OK) return st;
-    }
-    gf2cu_matrix* a = cache.a;
-    DeviceGuard g(c.device);
-    cudaStream_t s = pick_stream(a, c.stream);
-    const size_t W = a->W;
-    std::vector<u64> packed;
-    const bool aligned = (v->col_off & 63) == 0 && (n & 63) == 0;
-    cudaError_t e = cudaSuccess;
-    if (aligned) {
-        e = cudaMemcpy2DAsync(a->data, a->Wp * 8, v->data + (v->col_off >> 6), v->stride * 8, W * 8,
-                              m, cudaMemcpyHostToDevice, s);
-    } else {
-        packed.assign(m * W, 0ull);
-        for (size_t i = 0; i < m; ++i) {
-            const u64* row = reinterpret_cast<const u64*>(v->data) + i * v->stride;
-            for (size_t x = 0; x < W; ++x) {
-                const size_t take = std::min<size_t>(64, n - 64 * x);
-                packed[i * W + x] = read_bits(row, v->col_off + 64 * x, take);
-            }
-        }
-        e = cudaMemcpy2DAsync(a->data, a->Wp * 8, packed.data(), W * 8, W * 8, m,
-                              cudaMemcpyHostToDevice, s);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "upload");
-    c.stream = s;
-    st = run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats);
-    if (st == GF2CU_OK) {
-        if (aligned) {
-            e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6), v->stride * 8, a->data, a->Wp * 8,
-                                  W * 8, m, cudaMemcpyDeviceToHost, s);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        } else {
-            e = cudaMemcpy2DAsync(packed.data(), W * 8, a->data, a->Wp * 8, W * 8, m,
-                                  cudaMemcpyDeviceToHost, s);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-            if (e == cudaSuccess)
-                for (size_t i = 0; i < m; ++i) {
-                    u64* row = reinterpret_cast<u64*>(v->data) + i * v->stride;
-                    for (size_t x = 0; x < W; ++x) {
-                        const size_t take = std::min<size_t>(64, n - 64 * x);
-                        write_bits(row, v->col_off + 64 * x, take, packed[i * W + x]);
-                    }
-                }
-        }
-        if (e != cudaSuccess) st = cuda_fail(e, "download");
-        if (stats) {
-            stats->h2d_bytes = double(m) * W * 8;
-            stats->d2h_bytes = double(m) * W * 8;
-        }
-    }
+    return with_view(v, cfg, stats, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
+        return run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats);
+    });
+}
+
+gf2cu_status gf2cu_rref_from_ple_device(gf2cu_matrix* a, const size_t* q, size_t rank, int full,
+                                        void* stream) {
+    if (!a) return fail(GF2CU_EINVAL, "null matrix");
+    DeviceGuard g(a->device);
+    cudaStream_t s = pick_stream(a, stream);
+    gf2cu_status st = run_rref(a, q, rank, full != 0, s);
+    if (st == GF2CU_OK) CU_TRY(cudaStreamSynchronize(s));
     return st;
+}
+
+gf2cu_status gf2cu_rref_from_ple(const gf2cu_view* v, const size_t* q, size_t rank, int full,
+                                 const gf2cu_cfg* cfg) {
+    gf2cu_status st = check_view(v);
+    if (st != GF2CU_OK) return st;
+    st = check_pivots(q, rank, v->nrows, v->ncols);
+    if (st != GF2CU_OK || v->nrows == 0 || v->ncols == 0) return st;
+    return with_view(v, cfg, nullptr, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
+        return run_rref(a, q, rank, full != 0, pick_stream(a, c.stream));
+    });
+}
+
+gf2cu_status gf2cu_echelonize_device(gf2cu_matrix* a, int full, const gf2cu_cfg* cfg, size_t* rank) {
+    if (!a || !rank) return fail(GF2CU_EINVAL, "null argument");
+    gf2cu_status st = check_cfg(cfg);
+    if (st != GF2CU_OK) return st;
+    DeviceGuard g(a->device);
+    st = run_echelonize(a, cfg, full != 0, rank);
+    if (st == GF2CU_OK) CU_TRY(cudaStreamSynchronize(pick_stream(a, cfg ? cfg->stream : nullptr)));
+    return st;
+}
+
+gf2cu_status gf2cu_echelonize(const gf2cu_view* v, int full, const gf2cu_cfg* cfg, size_t* rank) {
+    if (!rank) return fail(GF2CU_EINVAL, "null argument");
+    gf2cu_status st = check_view(v);
+    if (st != GF2CU_OK) return st;
+    st = check_cfg(cfg);
+    if (st != GF2CU_OK) return st;
+    *rank = 0;
+    if (v->nrows == 0 || v->ncols == 0) return GF2CU_OK;
+    return with_view(v, cfg, nullptr, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
+        return run_echelonize(a, &c, full != 0, rank);
+    });
+}
+
+// trsm_upper_left_unit (multiply.hpp:314-335): B <- U^-1 B, U unit upper
+// triangular r x r (only bits strictly above the diagonal read), B r x n.
+gf2cu_status gf2cu_trsm_upper_left_unit(const gf2cu_view* u, const gf2cu_view* b,
+                                        const gf2cu_cfg* cfg) {
+    gf2cu_status st = check_view(u);
+    if (st == GF2CU_OK) st = check_view(b);
+    if (st != GF2CU_OK) return st;
+    const size_t r = u->nrows;
+    if (u->ncols != r || b->nrows != r) return fail(GF2CU_EINVAL, "trsm: dimension mismatch");
+    if (r <= 1 || b->ncols == 0) return GF2CU_OK;
+    const size_t Wa = words_of(r);
+    // U packed row-major (r x Wa) on the host, staged next to B's device copy
+    std::vector<u64> hu(r * Wa);
+    for (size_t i = 0; i < r; ++i) {
+        const u64* row = reinterpret_cast<const u64*>(u->data) + i * u->stride;
+        for (size_t x = 0; x < Wa; ++x)
+            hu[i * Wa + x] = read_bits(row, u->col_off + 64 * x, std::min<size_t>(64, r - 64 * x));
+    }
+    return with_view(b, cfg, nullptr, [&](gf2cu_matrix* a, const gf2cu_cfg& c) -> gf2cu_status {
+        cudaStream_t s = pick_stream(a, c.stream);
+        RrefWs& rw = a->rw;
+        const size_t n = a->n, R = (r + 63) / 64 * 64, Wu = R / 64, Wn = a->W;
+        const size_t WnPad8 = (Wn + 7) / 8 * 8;
+        CU_TRY(grow(&rw.src, &rw.src_words, r * Wa));
+        CU_TRY(grow(&rw.U, &rw.U_words, Wu * R));
+        CU_TRY(grow(&rw.N, &rw.N_words, WnPad8 * R));
+        CU_TRY(cudaMemcpyAsync(rw.src, hu.data(), hu.size() * sizeof(u64), cudaMemcpyHostToDevice, s));
+        CU_TRY(cudaMemsetAsync(rw.U, 0, Wu * R * sizeof(u64), s));
+        CU_TRY(cudaMemsetAsync(rw.N, 0, WnPad8 * R * sizeof(u64), s));
+        gf2cu::RrefParams p{};
+        p.a = rw.src;
+        p.b = a->data;
+        p.out = a->data;
+        p.U = rw.U;
+        p.N = rw.N;
+        p.m = (u32)r;
+        p.n = (u32)n;
+        p.W = (u32)a->W;
+        p.Wp = (u32)a->Wp;
+        p.Wa = (u32)Wa;
+        p.Wpa = (u32)Wa;
+        p.r = (u32)r;
+        p.R = (u32)R;
+        p.Wu = (u32)Wu;
+        p.Wn = (u32)Wn;
+        p.WnPad8 = (u32)WnPad8;
+        p.ncn = (u32)n;
+        const int sms = num_sms(a->device);
+        gf2cu::rref_gather_kernel<<<sms * 8, 256, 0, s>>>(p, 0);
+        CU_TRY(cudaGetLastError());
+        gf2cu_status st2 = solve_upper(a, p, s);
+        if (st2 != GF2CU_OK) return st2;
+        gf2cu::trsm_store_kernel<<<sms * 8, 256, 0, s>>>(p);
+        CU_TRY(cudaGetLastError());
+        return GF2CU_OK;
+    });
 }
 
 }  // extern "C"

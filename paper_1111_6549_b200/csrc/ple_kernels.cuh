@@ -734,28 +734,26 @@ __device__ __forceinline__ void xor2(ulonglong2& a, const ulonglong2& b) {
     a.y ^= b.y;
 }
 
-// Build the 8 Gray-code tables for tile `tile` from the staged raw pivot rows
-// (rows t >= rb and words <= w read as zero). Thread layout (512):
-// ch = tid&3, g&1 = (tid>>2)&1, s_lo = (tid>>3)&3, g>>1 = (tid>>5)&3,
-// s_hi = (tid>>7)&3; each thread walks entries gray(16 s + k), k = 0..15,
-// with its 8 source chunks in registers: one XOR per entry
-// (make_table, gray_code.hpp:105-112).
-__device__ __forceinline__ void build_tables(const Params& p, unsigned char* smem, u32 tile,
-                                             u32 w, u32 rb) {
+// Build the 8 Gray-code tables of one 64-byte column tile from 64 source rows
+// (row t at src + 8 t; rows t >= rb and the tile's first `zlim` words read as
+// zero). Thread layout (512): ch = tid&3, g&1 = (tid>>2)&1, s_lo = (tid>>3)&3,
+// g>>1 = (tid>>5)&3, s_hi = (tid>>7)&3; each thread walks entries
+// gray(16 s + k), k = 0..15, with its 8 source chunks in registers: one XOR
+// per entry (make_table, gray_code.hpp:105-112).
+__device__ __forceinline__ void gray_tables(unsigned char* smem, const u64* src, u32 rb, u32 zlim) {
     const u32 tid = threadIdx.x;
     const u32 ch = tid & 3u;
     const u32 g = (((tid >> 5) & 3u) << 1) | ((tid >> 2) & 1u);
     const u32 s = (((tid >> 7) & 3u) << 2) | ((tid >> 3) & 3u);
-    const u32 x = tile * 8u + 2u * ch;
-    const u64* st = p.stage + (((size_t)tile * 64) << 3) + 2u * ch;
+    const u64* st = src + 2u * ch;
     ulonglong2 R[8];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
         const u32 t = 8u * g + b;
         ulonglong2 v = make_ulonglong2(0ull, 0ull);
         if (t < rb) v = ldcg(reinterpret_cast<const ulonglong2*>(st + ((size_t)t << 3)));
-        if (x <= w) v.x = 0ull;
-        if (x + 1u <= w) v.y = 0ull;
+        if (2u * ch < zlim) v.x = 0ull;
+        if (2u * ch + 1u < zlim) v.y = 0ull;
         R[b] = v;
     }
     const u32 i0 = 16u * s;
@@ -772,6 +770,15 @@ __device__ __forceinline__ void build_tables(const Params& p, unsigned char* sme
         const u32 i = i0 + k;
         *reinterpret_cast<ulonglong2*>(smem + tab_off(g, i ^ (i >> 1), ch)) = acc;
     }
+}
+
+// Tables of step w for tile `tile` from the staged raw pivot rows (words <= w
+// read as zero: the panel and everything left of it are not updated).
+__device__ __forceinline__ void build_tables(const Params& p, unsigned char* smem, u32 tile,
+                                             u32 w, u32 rb) {
+    const u32 x0 = tile * 8u;
+    const u32 zlim = w + 1u > x0 ? min(w + 1u - x0, 8u) : 0u;
+    gray_tables(smem, p.stage + (((size_t)tile * 64) << 3), rb, zlim);
 }
 
 __device__ __forceinline__ ulonglong2 ld_info(const ulonglong2* info, u32 pos, bool valid) {

@@ -378,5 +378,95 @@ def block_iterative_ple(a, cfg: Optional[PleConfig] = None) -> PleOutcome:
     return _outcome(rank, swaps, q, cs, ncs, m, st)
 
 
+def _host_view(a) -> MatrixView:
+    return a.view() if isinstance(a, BitMatrix) else a
+
+
+def _pivots(out: PleOutcome, nrows: int) -> np.ndarray:
+    if out.processed != nrows:
+        raise ValueError("rref_from_ple on the device needs a complete decomposition "
+                         "(processed == nrows)")
+    return np.ascontiguousarray(np.asarray(out.q[: out.rank], dtype=np.uintp))
+
+
+def rref_from_ple(a, out: PleOutcome, full: bool = True, cfg: Optional[PleConfig] = None) -> None:
+    """gf2::rref_from_ple (ple.hpp:318-329) on the B200, in place: the top
+    ``out.rank`` rows become the row echelon form of the original matrix
+    (reduced when ``full``), the rows below zero. ``a`` holds the in-place
+    result that ``out`` describes (host view or ``DeviceMatrix``)."""
+    L = _lib.load()
+    szp = C.POINTER(C.c_size_t)
+    if isinstance(a, DeviceMatrix):
+        q = _pivots(out, a.m)
+        stream = cfg.stream if cfg is not None else None
+        check(L.gf2cu_rref_from_ple_device(a.handle, q.ctypes.data_as(szp), out.rank, int(full),
+                                           C.c_void_p(stream) if stream else None))
+        return
+    view = _host_view(a)
+    q = _pivots(out, view.nrows())
+    c = (cfg or PleConfig()).to_c()
+    v = view._c()
+    check(L.gf2cu_rref_from_ple(C.byref(v), q.ctypes.data_as(szp), out.rank, int(full), C.byref(c)))
+
+
+def extract_e(a, out: PleOutcome) -> BitMatrix:
+    """gf2::extract_e (ple.hpp:344-352): the rank x ncols echelon factor,
+    computed on the device from a copy (``a`` is not modified)."""
+    view = _host_view(a)
+    m, n = view.nrows(), view.ncols()
+    work = BitMatrix(m, n)
+    W = words_per_row(n)
+    flat = view.words.reshape(-1)
+    if view.col_off % 64 == 0 and n % 64 == 0:
+        for i in range(m):
+            s0 = i * view.stride + view.col_off // 64
+            work.words[i, :] = flat[s0:s0 + W]
+    else:
+        for i in range(m):
+            for j in range(n):
+                if view.get(i, j):
+                    work.set(i, j, True)
+    rref_from_ple(work, out, full=False)
+    return BitMatrix(out.rank, n, work.words[: out.rank].copy())
+
+
+def extract_l(a, out: PleOutcome) -> BitMatrix:
+    """gf2::extract_l (ple.hpp:332-341): the processed x rank unit lower
+    factor (a host-side reshuffle of the stored multipliers)."""
+    view = _host_view(a)
+    l = BitMatrix(out.processed, out.rank)
+    for i in range(out.processed):
+        for j in range(min(i, out.rank)):
+            if view.get(i, j):
+                l.set(i, j, True)
+        if i < out.rank:
+            l.set(i, i, True)
+    return l
+
+
+def echelonize(a, full: bool = True, cfg: Optional[PleConfig] = None) -> int:
+    """gf2::echelonize(a, EchelonStrategy::ple_iterative, full) (m4ri.hpp:88-98):
+    block_iterative_ple + rref_from_ple with the matrix resident on the
+    device in between. Returns the rank."""
+    L = _lib.load()
+    c = (cfg or PleConfig()).to_c()
+    rank = C.c_size_t()
+    if isinstance(a, DeviceMatrix):
+        check(L.gf2cu_echelonize_device(a.handle, int(full), C.byref(c), C.byref(rank)))
+    else:
+        v = _host_view(a)._c()
+        check(L.gf2cu_echelonize(C.byref(v), int(full), C.byref(c), C.byref(rank)))
+    return int(rank.value)
+
+
+def trsm_upper_left_unit(u, b, cfg: Optional[PleConfig] = None) -> None:
+    """gf2::trsm_upper_left_unit (multiply.hpp:314-335) on the B200:
+    b <- u^-1 b for the unit upper triangle of the square u."""
+    L = _lib.load()
+    c = (cfg or PleConfig()).to_c()
+    uv, bv = _host_view(u)._c(), _host_view(b)._c()
+    check(L.gf2cu_trsm_upper_left_unit(C.byref(uv), C.byref(bv), C.byref(c)))
+
+
 def device_count() -> int:
     return int(_lib.load().gf2cu_device_count())

@@ -70,14 +70,58 @@ int main() {
         CHECK(want.q == got.q && want.p.swaps == got.p.swaps, "sub-view outcome differs");
         ++cases;
     }
-    // echelonize(ple_iterative) facade
-    for (int rep = 0; rep < 20; ++rep) {
-        BitMatrix a(90, 110);
+    // echelonize(ple_iterative) facade, reduced and not, PLE + RREF on the device
+    for (int rep = 0; rep < 40; ++rep) {
+        const std::size_t m = 1 + rng() % 400, n = 1 + rng() % 400;
+        BitMatrix a(m, n);
         fill_random(a.view(), rep % 2 ? 0.5 : 0.1, 500 + rep);
+        const bool full = rep % 4 != 3;
         BitMatrix x = a, y = a;
-        const std::size_t r1 = echelonize(x.view(), EchelonStrategy::ple_iterative, true);
-        const std::size_t r2 = gf2::b200::echelonize_ple_iterative(y.view(), true);
-        CHECK(r1 == r2 && x == y, "echelonize differs (case %d)", rep);
+        const std::size_t r1 = echelonize(x.view(), EchelonStrategy::ple_iterative, full);
+        const std::size_t r2 = gf2::b200::echelonize_ple_iterative(y.view(), full);
+        CHECK(r1 == r2 && x == y, "echelonize differs (case %d, %zux%zu, full %d)", rep, m, n, full);
+        ++cases;
+    }
+    // rref_from_ple on the device from the reference's own outcome
+    for (int rep = 0; rep < 30; ++rep) {
+        const std::size_t m = 1 + rng() % 300, n = 1 + rng() % 300;
+        BitMatrix a(m, n);
+        fill_random(a.view(), rep % 3 ? 0.5 : 0.05, 900 + rep);
+        PleOutcome out = gf2::block_iterative_ple(a.view());
+        BitMatrix x = a, y = a;
+        const bool full = rep % 2 == 0;
+        rref_from_ple(x.view(), out, full);
+        gf2::b200::rref_from_ple(y.view(), out, full);
+        CHECK(x == y, "rref_from_ple differs (case %d, full %d)", rep, full);
+        ++cases;
+    }
+    // corrupt outcome -> std::invalid_argument, as check_pivots (test_ple.cpp:305-314)
+    {
+        BitMatrix a = BitMatrix(10, 10);
+        fill_random(a.view(), 0.5, 5);
+        PleOutcome out = gf2::b200::block_iterative_ple(a.view());
+        if (out.rank >= 2) {
+            std::swap(out.q[0], out.q[1]);
+            bool threw = false;
+            try {
+                gf2::b200::rref_from_ple(a.view(), out, true);
+            } catch (const std::invalid_argument&) {
+                threw = true;
+            }
+            CHECK(threw, "corrupt outcome accepted");
+            ++cases;
+        }
+    }
+    // trsm_upper_left_unit
+    for (int rep = 0; rep < 20; ++rep) {
+        const std::size_t r = 1 + rng() % 300, n = 1 + rng() % 300;
+        BitMatrix u(r, r), b(r, n);
+        fill_random(u.view(), 0.5, 1300 + rep);
+        fill_random(b.view(), 0.5, 1400 + rep);
+        BitMatrix b1 = b, b2 = b;
+        trsm_upper_left_unit(u.cview(), b1.view());
+        gf2::b200::trsm_upper_left_unit(u.cview(), b2.view());
+        CHECK(b1 == b2, "trsm differs (case %d, r %zu n %zu)", rep, r, n);
         ++cases;
     }
     std::printf("%d cases, %d failures\n", cases, failures);
