@@ -162,6 +162,23 @@ gf2cu_status gf2cu_trsm_upper_left_unit(const gf2cu_view* u, const gf2cu_view* b
                                         const gf2cu_cfg* cfg);
 
 /* ------------------------------------------------------------------ */
+/* GF(2) matrix product                              */
+/* ------------------------------------------------------------------ */
+/* Replace gf2::mul(ConstMatrixView a, ConstMatrixView b, const MulConfig&)
+ * (multiply.hpp:266-274; here c = a * b into the caller's c) and gf2::addmul
+ * (multiply.hpp:254-264; c ^= a * b). The product is unique, so the result
+ * does not depend on the reference's kernel choice (M4RM / Strassen) or on
+ * MulConfig. GF2CU_EINVAL on a dimension mismatch (check_mul_shapes,
+ * multiply.hpp:33-37); c must alias neither operand. */
+gf2cu_status gf2cu_mul(const gf2cu_view* c, const gf2cu_view* a, const gf2cu_view* b,
+                       const gf2cu_cfg* cfg);
+gf2cu_status gf2cu_addmul(const gf2cu_view* c, const gf2cu_view* a, const gf2cu_view* b,
+                          const gf2cu_cfg* cfg);
+/* Device-resident form: c = a * b (accumulate = 0) or c ^= a * b. */
+gf2cu_status gf2cu_matrix_mul(gf2cu_matrix* c, const gf2cu_matrix* a, const gf2cu_matrix* b,
+                              int accumulate, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* Row-sharded multi-GPU PLE (one process per GPU, host-driven steps)   */
 /* ------------------------------------------------------------------ */
 /* Global row g lives on rank (g / block) % nranks, local index

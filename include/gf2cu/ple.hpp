@@ -18,6 +18,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "gf2cu.h"
@@ -155,6 +156,40 @@ void trsm_upper_left_unit(CView u, View b, const DeviceOptions& dev = {}) {
     c.device = dev.device;
     c.stream = dev.stream;
     detail::throw_status(gf2cu_trsm_upper_left_unit(&uv, &bv, &c));
+}
+
+// recursive_ple (ple.hpp:246-289): its in-place result, rank, q and p.swaps
+// equal block_iterative_ple's (pinned in tests/test_rref_host.py), so the
+// device path serves it.
+template <class View = gf2::MatrixView, class Cfg = gf2::PleConfig>
+gf2::PleOutcome recursive_ple(View a, const Cfg& cfg = {}, const DeviceOptions& dev = {}) {
+    return block_iterative_ple(a, cfg, dev);
+}
+
+// addmul (multiply.hpp:254-264): c ^= a * b on the B200.
+template <class View = gf2::MatrixView, class CView = gf2::ConstMatrixView>
+void addmul(View c, CView a, CView b, const DeviceOptions& dev = {}) {
+    gf2cu_view cv = detail::to_view(c), av, bv;
+    for (auto [dst, src] : {std::pair<gf2cu_view*, const CView*>{&av, &a}, {&bv, &b}}) {
+        dst->data = const_cast<uint64_t*>(src->nrows() ? src->row_words(0) : nullptr);
+        dst->stride = src->stride();
+        dst->col_off = src->col_offset();
+        dst->nrows = src->nrows();
+        dst->ncols = src->ncols();
+    }
+    gf2cu_cfg cc;
+    gf2cu_default_config(&cc);
+    cc.device = dev.device;
+    cc.stream = dev.stream;
+    detail::throw_status(gf2cu_addmul(&cv, &av, &bv, &cc));
+}
+
+// mul (multiply.hpp:266-274): a new a.nrows() x b.ncols() product.
+template <class CView = gf2::ConstMatrixView>
+gf2::BitMatrix mul(CView a, CView b, const DeviceOptions& dev = {}) {
+    gf2::BitMatrix c(a.nrows(), b.ncols());
+    addmul(c.view(), a, b, dev);
+    return c;
 }
 
 }  // namespace b200

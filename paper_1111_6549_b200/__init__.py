@@ -14,8 +14,13 @@ from .ple import (  # noqa: F401
     PleConfig,
     PleOutcome,
     RowPermutation,
+    addmul,
     block_iterative_ple,
     device_count,
+    echelonize_strategy,
+    mul,
+    mul_into,
+    recursive_ple,
     echelonize,
     extract_e,
     extract_l,
@@ -31,5 +36,6 @@ __all__ = [
     "BitMatrix", "ColSwap", "DeviceMatrix", "MatrixView", "PleConfig", "PleOutcome",
     "RowPermutation", "block_iterative_ple", "device_count", "fill_ctr", "fill_random",
     "host_checksum", "words_per_row", "build", "load", "echelonize", "extract_e", "extract_l",
-    "rref_from_ple", "trsm_upper_left_unit",
+    "rref_from_ple", "trsm_upper_left_unit", "addmul", "mul", "mul_into", "recursive_ple",
+    "echelonize_strategy",
 ]

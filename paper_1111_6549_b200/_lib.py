@@ -110,6 +110,9 @@ SYMBOLS = {
     "gf2cu_echelonize_device": (C.c_int, [_mp, C.c_int, C.POINTER(gf2cu_cfg), _szp]),
     "gf2cu_trsm_upper_left_unit": (C.c_int, [C.POINTER(gf2cu_view), C.POINTER(gf2cu_view),
                                              C.POINTER(gf2cu_cfg)]),
+    "gf2cu_mul": (C.c_int, [C.POINTER(gf2cu_view)] * 3 + [C.POINTER(gf2cu_cfg)]),
+    "gf2cu_addmul": (C.c_int, [C.POINTER(gf2cu_view)] * 3 + [C.POINTER(gf2cu_cfg)]),
+    "gf2cu_matrix_mul": (C.c_int, [_mp, _mp, _mp, C.c_int, C.c_void_p]),
     "gf2cu_shard_create": (C.c_int, [_sz, _sz, C.c_int, C.c_int, _sz, C.c_int, C.POINTER(_mp)]),
     "gf2cu_shard_destroy": (C.c_int, [_mp]),
     "gf2cu_shard_info": (C.c_int, [_mp, _szp, _szp]),

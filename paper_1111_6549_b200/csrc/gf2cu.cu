@@ -22,6 +22,7 @@
 #include "ple_persistent.cuh"
 #include "ple_shard.cuh"
 #include "rref_kernels.cuh"
+#include "gemm_kernels.cuh"
 
 using gf2cu::u32;
 using gf2cu::u64;
@@ -568,81 +569,137 @@ gf2cu_status run_rref(gf2cu_matrix* a, const size_t* q, size_t rank, bool full, 
     return GF2CU_OK;
 }
 
-// Host view <-> the per-thread cached device matrix of its shape: upload,
-// body(matrix, stream), download, with unaligned windows packed host-side.
-template <class Body>
-gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* stats, Body&& body) {
-    const size_t m = v->nrows, n = v->ncols;
-    gf2cu_cfg c;
-    gf2cu_default_config(&c);
-    if (cfg) c = *cfg;
-    // One cached device matrix per host thread: repeated calls on the same
-    // shape reuse HBM buffers and workspace instead of re-allocating.
+// Per-thread cached device matrices (slot 0: the in-place operand of the
+// host-view entry points; 1, 2: read-only product operands). Repeated calls
+// on the same shapes reuse HBM buffers and workspace instead of re-allocating.
+gf2cu_status cached_matrix(int slot, size_t m, size_t n, int device, gf2cu_matrix** out) {
     struct Cache {
-        gf2cu_matrix* a = nullptr;
-        ~Cache() { gf2cu_matrix_destroy(a); }
+        gf2cu_matrix* a[3] = {nullptr, nullptr, nullptr};
+        ~Cache() {
+            for (gf2cu_matrix* x : a) gf2cu_matrix_destroy(x);
+        }
     };
     thread_local Cache cache;
-    if (cache.a && (cache.a->m != m || cache.a->n != n || cache.a->device != c.device)) {
-        gf2cu_matrix_destroy(cache.a);
-        cache.a = nullptr;
+    gf2cu_matrix*& a = cache.a[slot];
+    if (a && (a->m != m || a->n != n || a->device != device)) {
+        gf2cu_matrix_destroy(a);
+        a = nullptr;
     }
-    gf2cu_status st;
-    if (!cache.a) {
-        st = gf2cu_matrix_create(m, n, c.device, &cache.a);
+    if (!a) {
+        gf2cu_status st = gf2cu_matrix_create(m, n, device, &a);
         if (st != GF2CU_OK) return st;
     }
-    gf2cu_matrix* a = cache.a;
-    DeviceGuard g(c.device);
-    cudaStream_t s = pick_stream(a, c.stream);
-    const size_t W = a->W;
-    std::vector<u64> packed;
-    const bool aligned = (v->col_off & 63) == 0 && (n & 63) == 0;
-    cudaError_t e = cudaSuccess;
-    if (aligned) {
+    *out = a;
+    return GF2CU_OK;
+}
+
+bool view_aligned(const gf2cu_view* v) { return (v->col_off & 63) == 0 && (v->ncols & 63) == 0; }
+
+// Host window -> device rows (unaligned windows packed host-side into `packed`).
+gf2cu_status view_upload(const gf2cu_view* v, gf2cu_matrix* a, cudaStream_t s,
+                         std::vector<u64>& packed) {
+    const size_t m = v->nrows, n = v->ncols, W = a->W;
+    if (m == 0 || W == 0) return GF2CU_OK;
+    cudaError_t e;
+    if (view_aligned(v)) {
         e = cudaMemcpy2DAsync(a->data, a->Wp * 8, v->data + (v->col_off >> 6), v->stride * 8, W * 8,
                               m, cudaMemcpyHostToDevice, s);
     } else {
         packed.assign(m * W, 0ull);
         for (size_t i = 0; i < m; ++i) {
             const u64* row = reinterpret_cast<const u64*>(v->data) + i * v->stride;
-            for (size_t x = 0; x < W; ++x) {
-                const size_t take = std::min<size_t>(64, n - 64 * x);
-                packed[i * W + x] = read_bits(row, v->col_off + 64 * x, take);
-            }
+            for (size_t x = 0; x < W; ++x)
+                packed[i * W + x] = read_bits(row, v->col_off + 64 * x, std::min<size_t>(64, n - 64 * x));
         }
         e = cudaMemcpy2DAsync(a->data, a->Wp * 8, packed.data(), W * 8, W * 8, m,
                               cudaMemcpyHostToDevice, s);
     }
-    if (e != cudaSuccess) return cuda_fail(e, "upload");
+    return e == cudaSuccess ? GF2CU_OK : cuda_fail(e, "upload");
+}
+
+// Device rows -> host window (bits outside the window untouched); synchronous.
+gf2cu_status view_download(const gf2cu_view* v, const gf2cu_matrix* a, cudaStream_t s,
+                           std::vector<u64>& packed) {
+    const size_t m = v->nrows, n = v->ncols, W = a->W;
+    if (m == 0 || W == 0) return GF2CU_OK;
+    cudaError_t e;
+    if (view_aligned(v)) {
+        e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6), v->stride * 8, a->data, a->Wp * 8, W * 8,
+                              m, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    } else {
+        packed.resize(m * W);
+        e = cudaMemcpy2DAsync(packed.data(), W * 8, a->data, a->Wp * 8, W * 8, m,
+                              cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess)
+            for (size_t i = 0; i < m; ++i) {
+                u64* row = reinterpret_cast<u64*>(v->data) + i * v->stride;
+                for (size_t x = 0; x < W; ++x)
+                    write_bits(row, v->col_off + 64 * x, std::min<size_t>(64, n - 64 * x), packed[i * W + x]);
+            }
+    }
+    return e == cudaSuccess ? GF2CU_OK : cuda_fail(e, "download");
+}
+
+// Host view <-> the cached device matrix of its shape: upload,
+// body(matrix, cfg), download.
+template <class Body>
+gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* stats, Body&& body) {
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    if (cfg) c = *cfg;
+    gf2cu_matrix* a = nullptr;
+    gf2cu_status st = cached_matrix(0, v->nrows, v->ncols, c.device, &a);
+    if (st != GF2CU_OK) return st;
+    DeviceGuard g(c.device);
+    cudaStream_t s = pick_stream(a, c.stream);
+    std::vector<u64> packed;
+    st = view_upload(v, a, s, packed);
+    if (st != GF2CU_OK) return st;
     c.stream = s;
     st = body(a, c);
     if (st == GF2CU_OK) {
-        if (aligned) {
-            e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6), v->stride * 8, a->data, a->Wp * 8,
-                                  W * 8, m, cudaMemcpyDeviceToHost, s);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        } else {
-            e = cudaMemcpy2DAsync(packed.data(), W * 8, a->data, a->Wp * 8, W * 8, m,
-                                  cudaMemcpyDeviceToHost, s);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-            if (e == cudaSuccess)
-                for (size_t i = 0; i < m; ++i) {
-                    u64* row = reinterpret_cast<u64*>(v->data) + i * v->stride;
-                    for (size_t x = 0; x < W; ++x) {
-                        const size_t take = std::min<size_t>(64, n - 64 * x);
-                        write_bits(row, v->col_off + 64 * x, take, packed[i * W + x]);
-                    }
-                }
-        }
-        if (e != cudaSuccess) st = cuda_fail(e, "download");
+        st = view_download(v, a, s, packed);
         if (stats) {
-            stats->h2d_bytes = double(m) * W * 8;
-            stats->d2h_bytes = double(m) * W * 8;
+            stats->h2d_bytes = double(a->m) * a->W * 8;
+            stats->d2h_bytes = double(a->m) * a->W * 8;
         }
     }
     return st;
 }
+
+// C (+)= A * B on device matrices (check_mul_shapes, multiply.hpp:33-37).
+gf2cu_status run_mul(gf2cu_matrix* c, const gf2cu_matrix* a, const gf2cu_matrix* b, bool accumulate,
+                     cudaStream_t s) {
+    if (a->n != b->m || c->m != a->m || c->n != b->n)
+        return fail(GF2CU_EINVAL, "multiply: dimension mismatch");
+    if (c == a || c == b) return fail(GF2CU_EINVAL, "multiply: C aliases an operand");
+    if (a->device != c->device || b->device != c->device)
+        return fail(GF2CU_EINVAL, "multiply: operands on different devices");
+    const size_t M = c->m, L = a->n, Wc = c->W;
+    if (M == 0 || Wc == 0) return GF2CU_OK;
+    static bool attr_set[64] = {false};
+    if (c->device >= 0 && c->device < 64 && !attr_set[c->device]) {
+        CU_TRY(cudaFuncSetAttribute(gf2cu::gemm_m4rm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    gf2cu::kTableBytes));
+        attr_set[c->device] = true;
+    }
+    const int sms = num_sms(c->device);
+    const size_t Lw = words_of(L);
+    RrefWs& rw = c->rw;
+    CU_TRY(grow(&rw.src, &rw.src_words, M * Lw));
+    if (Lw) gf2cu::gemm_transpose_a_kernel<<<sms * 8, 256, 0, s>>>(a->data, rw.src, (u32)M, (u32)Lw, (u32)a->Wp);
+    dim3 grid((unsigned)((Wc + 7) / 8), (unsigned)((M + gf2cu::kGemmRows - 1) / gf2cu::kGemmRows));
+    gf2cu::gemm_m4rm_kernel<<<grid, gf2cu::kTrailThreads, gf2cu::kTableBytes, s>>>(
+        rw.src, b->data, c->data, (u32)M, (u32)L, (u32)b->Wp, (u32)c->Wp, accumulate ? 1 : 0);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+// Host-view product: A and B staged in the operand cache slots, C in slot 0.
+gf2cu_status view_mul(const gf2cu_view* c, const gf2cu_view* a, const gf2cu_view* b,
+                      const gf2cu_cfg* cfg, bool accumulate);
 
 gf2cu_status check_view(const gf2cu_view* v) {
     if (!v) return fail(GF2CU_EINVAL, "null argument");
@@ -650,6 +707,34 @@ gf2cu_status check_view(const gf2cu_view* v) {
     if (v->nrows && v->ncols && v->stride * 64 < v->col_off + v->ncols)
         return fail(GF2CU_ERANGE, "view window exceeds its row stride");
     return GF2CU_OK;
+}
+
+gf2cu_status view_mul(const gf2cu_view* c, const gf2cu_view* a, const gf2cu_view* b,
+                      const gf2cu_cfg* cfg, bool accumulate) {
+    gf2cu_status st = check_view(a);
+    if (st == GF2CU_OK) st = check_view(b);
+    if (st == GF2CU_OK) st = check_view(c);
+    if (st != GF2CU_OK) return st;
+    if (a->ncols != b->nrows || c->nrows != a->nrows || c->ncols != b->ncols)
+        return fail(GF2CU_EINVAL, "multiply: dimension mismatch");
+    if (c->nrows == 0 || c->ncols == 0) return GF2CU_OK;
+    gf2cu_cfg cc;
+    gf2cu_default_config(&cc);
+    if (cfg) cc = *cfg;
+    gf2cu_matrix *da = nullptr, *db = nullptr;
+    st = cached_matrix(1, a->nrows, a->ncols, cc.device, &da);
+    if (st == GF2CU_OK) st = cached_matrix(2, b->nrows, b->ncols, cc.device, &db);
+    if (st != GF2CU_OK) return st;
+    DeviceGuard g(cc.device);
+    std::vector<u64> pa, pb;
+    cudaStream_t s0 = pick_stream(da, cc.stream);
+    st = view_upload(a, da, s0, pa);
+    if (st == GF2CU_OK) st = view_upload(b, db, s0, pb);
+    if (st != GF2CU_OK) return st;
+    cc.stream = s0;
+    return with_view(c, &cc, nullptr, [&](gf2cu_matrix* dc, const gf2cu_cfg& c2) {
+        return run_mul(dc, da, db, accumulate, pick_stream(dc, c2.stream));
+    });
 }
 
 // PLE then rref_from_ple on the device copy (echelonize, m4ri.hpp:95-98).
@@ -851,6 +936,26 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
     return with_view(v, cfg, stats, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
         return run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats);
     });
+}
+
+gf2cu_status gf2cu_matrix_mul(gf2cu_matrix* c, const gf2cu_matrix* a, const gf2cu_matrix* b,
+                              int accumulate, void* stream) {
+    if (!a || !b || !c) return fail(GF2CU_EINVAL, "null matrix");
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick_stream(c, stream);
+    gf2cu_status st = run_mul(c, a, b, accumulate != 0, s);
+    if (st == GF2CU_OK) CU_TRY(cudaStreamSynchronize(s));
+    return st;
+}
+
+gf2cu_status gf2cu_mul(const gf2cu_view* c, const gf2cu_view* a, const gf2cu_view* b,
+                       const gf2cu_cfg* cfg) {
+    return view_mul(c, a, b, cfg, false);
+}
+
+gf2cu_status gf2cu_addmul(const gf2cu_view* c, const gf2cu_view* a, const gf2cu_view* b,
+                          const gf2cu_cfg* cfg) {
+    return view_mul(c, a, b, cfg, true);
 }
 
 gf2cu_status gf2cu_rref_from_ple_device(gf2cu_matrix* a, const size_t* q, size_t rank, int full,

@@ -735,12 +735,13 @@ __device__ __forceinline__ void xor2(ulonglong2& a, const ulonglong2& b) {
 }
 
 // Build the 8 Gray-code tables of one 64-byte column tile from 64 source rows
-// (row t at src + 8 t; rows t >= rb and the tile's first `zlim` words read as
-// zero). Thread layout (512): ch = tid&3, g&1 = (tid>>2)&1, s_lo = (tid>>3)&3,
+// (row t at src + rs t words; rows t >= rb and the tile's first `zlim` words
+// read as zero). Thread layout (512): ch = tid&3, g&1 = (tid>>2)&1, s_lo = (tid>>3)&3,
 // g>>1 = (tid>>5)&3, s_hi = (tid>>7)&3; each thread walks entries
 // gray(16 s + k), k = 0..15, with its 8 source chunks in registers: one XOR
 // per entry (make_table, gray_code.hpp:105-112).
-__device__ __forceinline__ void gray_tables(unsigned char* smem, const u64* src, u32 rb, u32 zlim) {
+__device__ __forceinline__ void gray_tables(unsigned char* smem, const u64* src, u32 rb, u32 zlim,
+                                            u32 rs = 8u) {
     const u32 tid = threadIdx.x;
     const u32 ch = tid & 3u;
     const u32 g = (((tid >> 5) & 3u) << 1) | ((tid >> 2) & 1u);
@@ -751,7 +752,7 @@ __device__ __forceinline__ void gray_tables(unsigned char* smem, const u64* src,
     for (int b = 0; b < 8; ++b) {
         const u32 t = 8u * g + b;
         ulonglong2 v = make_ulonglong2(0ull, 0ull);
-        if (t < rb) v = ldcg(reinterpret_cast<const ulonglong2*>(st + ((size_t)t << 3)));
+        if (t < rb) v = ldcg(reinterpret_cast<const ulonglong2*>(st + (size_t)t * rs));
         if (2u * ch < zlim) v.x = 0ull;
         if (2u * ch + 1u < zlim) v.y = 0ull;
         R[b] = v;

@@ -468,5 +468,59 @@ def trsm_upper_left_unit(u, b, cfg: Optional[PleConfig] = None) -> None:
     check(L.gf2cu_trsm_upper_left_unit(C.byref(uv), C.byref(bv), C.byref(c)))
 
 
+def recursive_ple(a, cfg: Optional[PleConfig] = None) -> PleOutcome:
+    """gf2::recursive_ple (ple.hpp:246-289). Its in-place result, rank, q and
+    p.swaps equal block_iterative_ple's (pinned against the compiled reference
+    in tests/test_rref_host.py), so the device path serves it unchanged."""
+    return block_iterative_ple(a, cfg)
+
+
+ECHELON_STRATEGIES = ("naive", "m4ri", "ple_iterative", "ple_recursive")
+
+
+def echelonize_strategy(a, strategy: str = "ple_iterative", full: bool = True,
+                        cfg: Optional[PleConfig] = None) -> int:
+    """gf2::echelonize(a, strategy, full) (m4ri.hpp:88-105). Every strategy
+    returns the same matrix (the reduced form is unique; the non-reduced forms
+    of naive / m4ri / PLE coincide, pinned in tests/test_rref_host.py), so all
+    of them run the device PLE + rref_from_ple."""
+    if strategy not in ECHELON_STRATEGIES:
+        raise ValueError(f"unknown strategy {strategy!r}")
+    return echelonize(a, full, cfg)
+
+
+def _mul(c, a, b, accumulate: bool, cfg: Optional[PleConfig]) -> None:
+    L = _lib.load()
+    if isinstance(c, DeviceMatrix):
+        if not (isinstance(a, DeviceMatrix) and isinstance(b, DeviceMatrix)):
+            raise ValueError("device product needs device operands")
+        stream = cfg.stream if cfg is not None else None
+        check(L.gf2cu_matrix_mul(c.handle, a.handle, b.handle, int(accumulate),
+                                 C.c_void_p(stream) if stream else None))
+        return
+    cc = (cfg or PleConfig()).to_c()
+    cv, av, bv = _host_view(c)._c(), _host_view(a)._c(), _host_view(b)._c()
+    fn = L.gf2cu_addmul if accumulate else L.gf2cu_mul
+    check(fn(C.byref(cv), C.byref(av), C.byref(bv), C.byref(cc)))
+
+
+def mul(a, b, cfg: Optional[PleConfig] = None) -> BitMatrix:
+    """gf2::mul (multiply.hpp:266-274): a new a.nrows x b.ncols product."""
+    av, bv = _host_view(a), _host_view(b)
+    c = BitMatrix(av.nrows(), bv.ncols())
+    _mul(c, av, bv, False, cfg)
+    return c
+
+
+def mul_into(c, a, b, cfg: Optional[PleConfig] = None) -> None:
+    """c = a * b (host views or DeviceMatrix operands)."""
+    _mul(c, a, b, False, cfg)
+
+
+def addmul(c, a, b, cfg: Optional[PleConfig] = None) -> None:
+    """gf2::addmul (multiply.hpp:254-264): c ^= a * b."""
+    _mul(c, a, b, True, cfg)
+
+
 def device_count() -> int:
     return int(_lib.load().gf2cu_device_count())

@@ -146,3 +146,33 @@ def test_known_answers():
     # rank zero (test_ple.cpp:279-285)
     z = np.zeros((6, 1), dtype=np.uint64)
     assert O.echelonize(z, 6, 9, True) == 0 and not z.any()
+
+
+def test_strategy_equivalences_pinned():
+    """What lets one device path serve recursive_ple and every echelonize
+    strategy: recursive_ple's in-place result, rank, q and p.swaps equal
+    block_iterative_ple's for any recursion cut-off, and the non-reduced
+    forms of naive / m4ri / ple_iterative / ple_recursive coincide."""
+    for (m, n, kind, seed) in cases()[:100] + [(500, 500, 2, 1), (300, 900, 3, 2), (900, 300, 2, 3)]:
+        a = S.build(m, n, kind, seed)
+        x = a.copy()
+        o1, _ = O.ref_ple(x, m, n)
+        for bb, bn in [(0, 0), (512, 32), (8 << 10, 0)]:
+            y = a.copy()
+            o2 = O.ref_recursive_ple(y, m, n, base_bytes=bb, base_ncols=bn)
+            assert np.array_equal(x, y) and o1.rank == o2.rank, (m, n, kind)
+            assert np.array_equal(o1.q, o2.q) and np.array_equal(o1.swaps, o2.swaps), (m, n, kind)
+        forms = []
+        for strat in ("naive", "m4ri", "ple_iterative", "ple_recursive"):
+            u = a.copy()
+            O.ref_echelonize(u, m, n, strat, False)
+            forms.append(u)
+        assert all(np.array_equal(forms[0], f) for f in forms[1:]), (m, n, kind)
+
+
+def test_mul_oracle_matches_reference():
+    for (m, l, n, seed) in [(1, 1, 1, 1), (3, 70, 5, 2), (64, 64, 64, 3), (65, 129, 63, 4),
+                            (200, 300, 100, 5), (130, 1, 70, 6)]:
+        a = O.fill_random(m, l, 0.5, seed)
+        b = O.fill_random(l, n, 0.5, seed + 1)
+        assert np.array_equal(O.mul(a, l, b, n), O.ref_mul(a, l, b, n)), (m, l, n)
