@@ -285,12 +285,32 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         void* args[] = {&p, &nsteps};
         cudaEvent_t* E = timing ? &ws.ev[6 * (W + 1)] : nullptr;
         if (E) cudaEventRecord(E[0], s);
+        // diagnostics: per-worker sweep stamps (GF2CU_DUMP_WORKERS=<path>)
+        const char* wpath = timing ? std::getenv("GF2CU_DUMP_WORKERS") : nullptr;
+        u64* wns = nullptr;
+        const size_t wn_words = ((size_t)W + 1) * (size_t)(grid - 1) * 2;
+        if (wpath) {
+            CU_TRY(cudaMalloc(&wns, wn_words * sizeof(u64)));
+            CU_TRY(cudaMemsetAsync(wns, 0, wn_words * sizeof(u64), s));
+        }
+        p.worker_ns = wns;
         CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_persistent_kernel, dim3(grid),
                                            dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
         if (E) cudaEventRecord(E[1], s);
         gf2cu::SyncState sy{};
         CU_TRY(cudaMemcpyAsync(&sy, ws.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
         CU_TRY(cudaStreamSynchronize(s));
+        if (wns) {
+            std::vector<u64> h(wn_words);
+            cudaMemcpy(h.data(), wns, wn_words * sizeof(u64), cudaMemcpyDeviceToHost);
+            cudaFree(wns);
+            if (FILE* f = std::fopen(wpath, "wb")) {
+                const u64 hdr[2] = {(u64)W, (u64)(grid - 1)};
+                std::fwrite(hdr, sizeof(u64), 2, f);
+                std::fwrite(h.data(), sizeof(u64), h.size(), f);
+                std::fclose(f);
+            }
+        }
         if (sy.error) return fail(GF2CU_ECUDA, "persistent PLE kernel watchdog tripped");
         steps = sy.panel_done;
         if (E) cudaEventElapsedTime(&kernel_ms, E[0], E[1]);

@@ -86,6 +86,7 @@ struct Params {
     volatile u32* host_r;  // mapped pinned mirror of (r + rb), may be null
     SyncState* sync;
     u64* phase_ns;   // per-step phase timestamps (persistent driver), may be null
+    u64* worker_ns;  // diagnostics: per step x worker {rest start, rest end}, may be null
     // sharded driver only (null / 0 otherwise)
     u32* inv;        // global row -> position (kept in step with perm)
     u32* status;     // panel status words (see kPanelStatus*)

@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
             }
             cta_arrive(&sy->cap_count);
             if (wk == 0) stamp(p, w, 4);
+            if (p.worker_ns && threadIdx.x == 0)
+                p.worker_ns[((size_t)w * nworkers + wk) * 2] = globaltimer();
             // remaining tiles: linear share
             const u32 nt = (p.Wpad8 >> 3) - tcap - 1;
             const u64 total = (u64)nt * nrows;
@@ -118,6 +120,14 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
                         total * (wk + 1) / nworkers);
         } else {
             cta_arrive(&sy->cap_count);
+        }
+        if (p.worker_ns && threadIdx.x == 0) {
+            p.worker_ns[((size_t)w * nworkers + wk) * 2 + 1] = globaltimer();
+            if (w == 0) {
+                u32 smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                p.worker_ns[((size_t)nsteps * nworkers + wk) * 2] = smid;
+            }
         }
         cta_arrive(&sy->t_count);
         if (wk == 0) stamp(p, w, 5);

@@ -124,6 +124,32 @@ int main() {
         CHECK(b1 == b2, "trsm differs (case %d, r %zu n %zu)", rep, r, n);
         ++cases;
     }
+    // recursive_ple (same outputs as the iterative PLE), mul / addmul
+    for (int rep = 0; rep < 20; ++rep) {
+        const std::size_t m = 1 + rng() % 400, n = 1 + rng() % 400;
+        BitMatrix a(m, n);
+        fill_random(a.view(), rep % 2 ? 0.5 : 0.05, 1700 + rep);
+        BitMatrix x = a, y = a;
+        PleConfig cfg;
+        cfg.base_bytes = 512;
+        cfg.base_ncols = 32;
+        PleOutcome want = gf2::recursive_ple(x.view(), cfg);
+        PleOutcome got = gf2::b200::recursive_ple(y.view(), cfg);
+        CHECK(x == y && want.rank == got.rank && want.q == got.q && want.p.swaps == got.p.swaps,
+              "recursive_ple differs (case %d)", rep);
+        const std::size_t l = 1 + rng() % 300, k = 1 + rng() % 300;
+        BitMatrix u(m, l), v(l, k), c(m, k);
+        fill_random(u.view(), 0.5, 1800 + rep);
+        fill_random(v.view(), 0.3, 1900 + rep);
+        fill_random(c.view(), 0.5, 2000 + rep);
+        CHECK(gf2::mul(u.cview(), v.cview()) == gf2::b200::mul(u.cview(), v.cview()),
+              "mul differs (case %d)", rep);
+        BitMatrix c1 = c, c2 = c;
+        gf2::addmul(c1.view(), u.cview(), v.cview());
+        gf2::b200::addmul(c2.view(), u.cview(), v.cview());
+        CHECK(c1 == c2, "addmul differs (case %d)", rep);
+        cases += 3;
+    }
     std::printf("%d cases, %d failures\n", cases, failures);
     return failures ? 1 : 0;
 }
