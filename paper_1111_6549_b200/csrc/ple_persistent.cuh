@@ -80,17 +80,19 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         const u32 lo = min(p.m, r + wk * slab), hi = min(p.m, lo + slab);
 
         if (wk == 0) stamp(p, w, 2);
-        // apply: own slab
-        apply_load(q, ash, rb);
-        __syncthreads();
-        apply_rows(q, ash, w, r, rb, lo, hi, threadIdx.x, blockDim.x);
-
-        // stage: after every worker finished step w-1 (pivot tails final)
+        // stage: after every worker finished step w-1 (pivot tails final).
+        // Staging first and applying while the staging barrier propagates
+        // keeps the apply of the last worker of step w-1 off the critical
+        // path (the tables never read the words <= w that apply writes).
         if (w > 0 && !cta_wait(sy, &sy->t_count, nworkers * w, s_ok)) return;
         const u32 stot = stage_total(q, w, rb);
         stage_units(q, w, r, rb, (u32)((u64)stot * wk / nworkers), (u32)((u64)stot * (wk + 1) / nworkers),
                     threadIdx.x, blockDim.x);
         cta_arrive(&sy->st_count);
+        // apply: own slab
+        apply_load(q, ash, rb);
+        __syncthreads();
+        apply_rows(q, ash, w, r, rb, lo, hi, threadIdx.x, blockDim.x);
         if (!cta_wait(sy, &sy->st_count, nworkers * (w + 1), s_ok)) return;
 
         if (wk == 0) stamp(p, w, 3);
