@@ -69,6 +69,8 @@ struct Workspace {
     u64* hashes = nullptr;       // per-row checksum scratch
     gf2cu::SyncState* sync = nullptr;
     u64* phase_ns = nullptr;     // 8 stamps per step (persistent driver)
+    u64* ubuf = nullptr;         // persistent driver: swept pivot-row tails
+    size_t ucap = 0;
     std::vector<cudaEvent_t> ev;
 };
 
@@ -87,6 +89,7 @@ void free_ws(Workspace& w) {
     cudaFree(w.hashes);
     cudaFree(w.sync);
     cudaFree(w.phase_ns);
+    cudaFree(w.ubuf);
     if (w.host_r) cudaFreeHost(w.host_r);
     for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
     w = Workspace{};
@@ -255,6 +258,14 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     const int sms = num_sms(a->device);
     const int apply_grid = sms * 4;
     const bool multi = cfg && (cfg->flags & GF2CU_FLAG_MULTI_KERNEL);
+    if (!multi) {
+        if (!ws.ubuf) {
+            ws.ucap = std::max<size_t>(1, std::min(m, n));
+            CU_TRY(cudaMalloc(&ws.ubuf, ws.ucap * p.Wpad8 * sizeof(u64)));
+        }
+        p.ubuf = ws.ubuf;
+        p.ucap = (u32)ws.ucap;
+    }
 
     if (timing) {
         const size_t need = 6 * (W + 1) + 2;
@@ -359,7 +370,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
 
     // back to the row-major public layout, rows gathered into position order
     gf2cu::untile_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
-                                                p.Wpad8);
+                                                p.Wpad8, p.ubuf, p.ucap, ws.qcol, (u32)rk, (u32)W);
     CU_TRY(cudaGetLastError());
 
     std::vector<u32> sw(rk), qq(rk);

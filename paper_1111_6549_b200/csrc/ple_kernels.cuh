@@ -87,6 +87,11 @@ struct Params {
     SyncState* sync;
     u64* phase_ns;   // per-step phase timestamps (persistent driver), may be null
     u64* worker_ns;  // diagnostics: per step x worker {rest start, rest end}, may be null
+    // persistent driver: the pivot rows' swept tails go to ubuf (tile-major,
+    // indexed by position, ucap rows) instead of back into the matrix, so the
+    // matrix keeps their raw tails for the step's table builds (no staging)
+    u64* ubuf;
+    u32 ucap;
     // sharded driver only (null / 0 otherwise)
     u32* inv;        // global row -> position (kept in step with perm)
     u32* status;     // panel status words (see kPanelStatus*)
@@ -186,16 +191,27 @@ __global__ void tile_kernel(const u64* __restrict__ src, u64* __restrict__ dst, 
     }
 }
 
+// Back to row-major in position order. With ubuf (persistent driver), the
+// pivot row at position i < rank of step ws = q_i / 64 takes its tiles from
+// the step's first swept tile ((ws+1)/8) on from ubuf (if that step swept).
 __global__ void untile_kernel(const u64* __restrict__ src, u64* __restrict__ dst,
-                              const u32* __restrict__ perm, u32 m, u32 Wp, u32 Wpad8) {
+                              const u32* __restrict__ perm, u32 m, u32 Wp, u32 Wpad8,
+                              const u64* __restrict__ ubuf = nullptr, u32 ucap = 0u,
+                              const u32* __restrict__ qcol = nullptr, u32 rank = 0u, u32 W = 0u) {
     const u32 per_row = Wpad8 >> 1;
     const u64 total = (u64)m * per_row;
     for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (u64)gridDim.x * blockDim.x) {
         const u32 row = (u32)(e / per_row), x = 2u * (u32)(e - (u64)row * per_row);
         const u32 ph = perm ? perm[row] : row;
+        const u64* from = tword(const_cast<u64*>(src), m, ph, x);
+        if (ubuf && row < rank) {
+            const u32 ws = qcol[row] >> 6;
+            if (ws + 1u < W && (x >> 3) >= ((ws + 1u) >> 3))
+                from = tword(const_cast<u64*>(ubuf), ucap, row, x);
+        }
         *reinterpret_cast<ulonglong2*>(dst + (size_t)row * Wp + x) =
-            *reinterpret_cast<const ulonglong2*>(tword(const_cast<u64*>(src), m, ph, x));
+            *reinterpret_cast<const ulonglong2*>(from);
     }
 }
 
@@ -736,24 +752,23 @@ __device__ __forceinline__ void xor2(ulonglong2& a, const ulonglong2& b) {
 }
 
 // Build the 8 Gray-code tables of one 64-byte column tile from 64 source rows
-// (row t at src + rs t words; rows t >= rb and the tile's first `zlim` words
-// read as zero). Thread layout (512): ch = tid&3, g&1 = (tid>>2)&1, s_lo = (tid>>3)&3,
-// g>>1 = (tid>>5)&3, s_hi = (tid>>7)&3; each thread walks entries
-// gray(16 s + k), k = 0..15, with its 8 source chunks in registers: one XOR
-// per entry (make_table, gray_code.hpp:105-112).
-__device__ __forceinline__ void gray_tables(unsigned char* smem, const u64* src, u32 rb, u32 zlim,
-                                            u32 rs = 8u) {
+// (row t's chunk at rowptr(t); rows t >= rb and the tile's first `zlim`
+// words read as zero). Thread layout (512): ch = tid&3, g&1 = (tid>>2)&1,
+// s_lo = (tid>>3)&3, g>>1 = (tid>>5)&3, s_hi = (tid>>7)&3; each thread walks
+// entries gray(16 s + k), k = 0..15, with its 8 source chunks in registers:
+// one XOR per entry (make_table, gray_code.hpp:105-112).
+template <class RowPtr>
+__device__ __forceinline__ void gray_tables_rows(unsigned char* smem, RowPtr rowptr, u32 rb, u32 zlim) {
     const u32 tid = threadIdx.x;
     const u32 ch = tid & 3u;
     const u32 g = (((tid >> 5) & 3u) << 1) | ((tid >> 2) & 1u);
     const u32 s = (((tid >> 7) & 3u) << 2) | ((tid >> 3) & 3u);
-    const u64* st = src + 2u * ch;
     ulonglong2 R[8];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
         const u32 t = 8u * g + b;
         ulonglong2 v = make_ulonglong2(0ull, 0ull);
-        if (t < rb) v = ldcg(reinterpret_cast<const ulonglong2*>(st + (size_t)t * rs));
+        if (t < rb) v = ldcg(reinterpret_cast<const ulonglong2*>(rowptr(t) + 2u * ch));
         if (2u * ch < zlim) v.x = 0ull;
         if (2u * ch + 1u < zlim) v.y = 0ull;
         R[b] = v;
@@ -774,13 +789,24 @@ __device__ __forceinline__ void gray_tables(unsigned char* smem, const u64* src,
     }
 }
 
-// Tables of step w for tile `tile` from the staged raw pivot rows (words <= w
-// read as zero: the panel and everything left of it are not updated).
+// Contiguous source rows, `rs` words apart.
+__device__ __forceinline__ void gray_tables(unsigned char* smem, const u64* src, u32 rb, u32 zlim,
+                                            u32 rs = 8u) {
+    gray_tables_rows(smem, [&](u32 t) { return src + (size_t)t * rs; }, rb, zlim);
+}
+
+// Tables of step w for tile `tile` from the raw pivot rows: the staged copy,
+// or (persistent driver, piv = the step's pivot rows' physical indices) the
+// matrix itself. Words <= w read as zero: the panel and everything left of
+// it are not updated.
 __device__ __forceinline__ void build_tables(const Params& p, unsigned char* smem, u32 tile,
-                                             u32 w, u32 rb) {
+                                             u32 w, u32 rb, const u32* piv = nullptr) {
     const u32 x0 = tile * 8u;
     const u32 zlim = w + 1u > x0 ? min(w + 1u - x0, 8u) : 0u;
-    gray_tables(smem, p.stage + (((size_t)tile * 64) << 3), rb, zlim);
+    if (piv)
+        gray_tables_rows(smem, [&](u32 t) { return tword(p.mat, p.m, piv[t], x0); }, rb, zlim);
+    else
+        gray_tables(smem, p.stage + (((size_t)tile * 64) << 3), rb, zlim);
 }
 
 __device__ __forceinline__ ulonglong2 ld_info(const ulonglong2* info, u32 pos, bool valid) {
@@ -790,7 +816,7 @@ __device__ __forceinline__ ulonglong2 ld_info(const ulonglong2* info, u32 pos, b
 // Rows [row0, row0+cnt) (offsets from r) of tile `tile`; tables must already
 // be built. The tile holding word w+1 also writes the look-ahead panel buffer.
 __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char* smem, u32 w,
-                                           u32 r, u32 tile, u32 row0, u32 cnt) {
+                                           u32 r, u32 tile, u32 row0, u32 cnt, u32 npiv = 0u) {
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
     const u32 cap_word = w + 1;
@@ -824,7 +850,7 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
     for (int k = 0; k < kUnroll; ++k) {
         const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 4);
         valC[k] = make_ulonglong2(0ull, 0ull);
-        if (ri < rend && (infC[k].x != 0ull || capture))
+        if (ri < rend && (infC[k].x != 0ull || capture || ri < npiv))
             valC[k] = ldcg(reinterpret_cast<const ulonglong2*>(tbase + ((size_t)infC[k].y << 3)));
     }
     for (u32 it = 0; it < nit; ++it) {
@@ -834,7 +860,7 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
         for (int k = 0; k < kUnroll; ++k) {
             const u32 ri = base + kRowsPerIter + lane_row + (u32)k * (kTrailThreads / 4);
             valN[k] = make_ulonglong2(0ull, 0ull);
-            if (ri < rend && (infN[k].x != 0ull || capture))
+            if (ri < rend && (infN[k].x != 0ull || capture || ri < npiv))
                 valN[k] = ldcg(reinterpret_cast<const ulonglong2*>(tbase + ((size_t)infN[k].y << 3)));
         }
 #pragma unroll
@@ -846,14 +872,19 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
         for (int k = 0; k < kUnroll; ++k) {
             const u32 ri = base + lane_row + (u32)k * (kTrailThreads / 4);
             const u64 d = infC[k].x;
-            if (d != 0ull) {
+            // (pivot rows always reach ubuf, d = 0 included: U_t = raw tail)
+            if (d != 0ull || (ri < npiv && ri < rend)) {
 #pragma unroll
                 for (u32 gi = 0; gi < kTables; ++gi) {
                     const u32 g = gi ^ par;
                     const u32 e = (u32)(d >> (8u * g)) & 0xffu;
                     xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
                 }
-                *reinterpret_cast<ulonglong2*>(tbase + ((size_t)infC[k].y << 3)) = valC[k];
+                if (ri < npiv)  // a pivot row of this step: its tail goes to ubuf
+                    *reinterpret_cast<ulonglong2*>(
+                        p.ubuf + ((((size_t)tile * p.ucap + r + ri) << 3) + 2u * ch)) = valC[k];
+                else
+                    *reinterpret_cast<ulonglong2*>(tbase + ((size_t)infC[k].y << 3)) = valC[k];
             }
             if (cap_lane && ri < rend) p.pb[r + ri] = cap_hi ? valC[k].y : valC[k].x;
             if (cap2_lane && ri < rend) p.pb2[r + ri] = cap2_hi ? valC[k].y : valC[k].x;
@@ -870,7 +901,8 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
 // Linear share [beg, end) of the (tile, row) work of step w over tiles
 // [tile_lo, tile_hi), rows r..m-1; tables rebuilt per tile segment.
 __device__ __forceinline__ void trail_share(const Params& p, unsigned char* smem, u32 w, u32 r,
-                                            u32 rb, u32 tile_lo, u64 beg, u64 end) {
+                                            u32 rb, u32 tile_lo, u64 beg, u64 end,
+                                            const u32* piv = nullptr) {
     const u32 nrows = p.m - r;
     u64 u = beg;
     while (u < end) {
@@ -879,10 +911,10 @@ __device__ __forceinline__ void trail_share(const Params& p, unsigned char* smem
         const u32 cnt = (u32)min((u64)(nrows - row0), end - u);
         if (rb > 0) {
             __syncthreads();
-            build_tables(p, smem, tile, w, rb);
+            build_tables(p, smem, tile, w, rb, piv);
             __syncthreads();
         }
-        trail_rows(p, smem, w, r, tile, row0, cnt);
+        trail_rows(p, smem, w, r, tile, row0, cnt, piv ? rb : 0u);
         u += cnt;
     }
 }

@@ -6,8 +6,10 @@
 // the workers are still streaming the rest of step w's trailing update.
 // CTAs 1..G-1 are workers: per step they
 //   apply   their row slab (multipliers, d, compressed words),
-//   stage   their share of the raw pivot-row tails (after all of step w-1),
-//   update  the look-ahead tile for their row slab, signal the panel CTA,
+//   wait    until every worker finished step w-1 (the pivot rows' raw tails
+//           are then final; tables read them in place, and the pivot rows'
+//           own swept tails go to ubuf, so no staging copy is needed),
+//   update  the look-ahead tiles for their row slab, signal the panel CTA,
 //   update  their linear share of the remaining tiles.
 // Cross-CTA ordering uses release/acquire counters in SyncState; every wait
 // has a watchdog so a bug turns into an error code, not a hung GPU. The grid
@@ -41,6 +43,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
     __shared__ PanelShared psh;
     __shared__ ApplyShared ash;
     __shared__ u32 s_ok;
+    __shared__ u32 s_piv[64];  // physical rows of the step's pivots
     SyncState* sy = p.sync;
     const u32 nworkers = gridDim.x - 1;
 
@@ -80,20 +83,15 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         const u32 lo = min(p.m, r + wk * slab), hi = min(p.m, lo + slab);
 
         if (wk == 0) stamp(p, w, 2);
-        // stage: after every worker finished step w-1 (pivot tails final).
-        // Staging first and applying while the staging barrier propagates
-        // keeps the apply of the last worker of step w-1 off the critical
-        // path (the tables never read the words <= w that apply writes).
-        if (w > 0 && !cta_wait(sy, &sy->t_count, nworkers * w, s_ok)) return;
-        const u32 stot = stage_total(q, w, rb);
-        stage_units(q, w, r, rb, (u32)((u64)stot * wk / nworkers), (u32)((u64)stot * (wk + 1) / nworkers),
-                    threadIdx.x, blockDim.x);
-        cta_arrive(&sy->st_count);
         // apply: own slab
         apply_load(q, ash, rb);
         __syncthreads();
         apply_rows(q, ash, w, r, rb, lo, hi, threadIdx.x, blockDim.x);
-        if (!cta_wait(sy, &sy->st_count, nworkers * (w + 1), s_ok)) return;
+        // the pivot rows' raw tails are final once every worker finished step
+        // w-1; the tables read them in place (their own swept tails go to ubuf)
+        if (w > 0 && !cta_wait(sy, &sy->t_count, nworkers * w, s_ok)) return;
+        for (u32 k = threadIdx.x; k < rb; k += blockDim.x) s_piv[k] = ldcg(p.perm + r + k);
+        __syncthreads();
 
         if (wk == 0) stamp(p, w, 3);
         const u32 tile0 = (w + 1) >> 3;
@@ -105,10 +103,10 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
                 for (u32 tt = tile0; tt <= tcap; ++tt) {
                     if (rb > 0) {
                         __syncthreads();
-                        build_tables(q, smem, tt, w, rb);
+                        build_tables(q, smem, tt, w, rb, s_piv);
                         __syncthreads();
                     }
-                    trail_rows(q, smem, w, r, tt, lo - r, hi - lo);
+                    trail_rows(q, smem, w, r, tt, lo - r, hi - lo, rb);
                 }
             }
             cta_arrive(&sy->cap_count);
@@ -119,7 +117,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
             const u32 nt = (p.Wpad8 >> 3) - tcap - 1;
             const u64 total = (u64)nt * nrows;
             trail_share(q, smem, w, r, rb, tcap + 1, total * wk / nworkers,
-                        total * (wk + 1) / nworkers);
+                        total * (wk + 1) / nworkers, s_piv);
         } else {
             cta_arrive(&sy->cap_count);
         }
