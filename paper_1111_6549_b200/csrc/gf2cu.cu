@@ -71,6 +71,7 @@ struct Workspace {
     u64* phase_ns = nullptr;     // 8 stamps per step (persistent driver)
     u64* ubuf = nullptr;         // persistent driver: swept pivot-row tails
     size_t ucap = 0;
+    u32* apctr = nullptr;        // persistent driver: per-step pre-work chunk counters
     std::vector<cudaEvent_t> ev;
 };
 
@@ -90,6 +91,7 @@ void free_ws(Workspace& w) {
     cudaFree(w.sync);
     cudaFree(w.phase_ns);
     cudaFree(w.ubuf);
+    cudaFree(w.apctr);
     if (w.host_r) cudaFreeHost(w.host_r);
     for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
     w = Workspace{};
@@ -265,6 +267,9 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         }
         p.ubuf = ws.ubuf;
         p.ucap = (u32)ws.ucap;
+        if (!ws.apctr) CU_TRY(cudaMalloc(&ws.apctr, 2 * (W + 1) * sizeof(u32)));
+        p.ap_claim = ws.apctr;
+        p.ap_done = ws.apctr + W + 1;
     }
 
     if (timing) {
@@ -286,6 +291,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     if (!multi) {
         // ---- persistent cooperative driver: one launch for all panels ----
         CU_TRY(cudaMemsetAsync(ws.sync, 0, sizeof(gf2cu::SyncState), s));
+        CU_TRY(cudaMemsetAsync(ws.apctr, 0, 2 * (W + 1) * sizeof(u32), s));
         if (timing) CU_TRY(cudaMemsetAsync(ws.phase_ns, 0, 8 * (W + 1) * sizeof(u64), s));
         int per_sm = 0;
         CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(

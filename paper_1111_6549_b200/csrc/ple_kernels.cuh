@@ -62,9 +62,9 @@ struct PanelOut {
 // Cross-CTA counters of the persistent driver (zeroed before each launch).
 struct SyncState {
     u32 panel_done;  // steps whose panel factorization is published
-    u32 cap_count;   // worker arrivals after the look-ahead tile
+    u32 cap_count;   // worker arrivals after the look-ahead tile (unused by the persistent driver)
     u32 t_count;     // worker arrivals after the whole trailing update
-    u32 st_count;    // worker arrivals after staging
+    u32 st_count;    // worker arrivals after staging (unused by the persistent driver)
     u32 error;       // watchdog tripped
     u32 pad[3];
     u64 stamps[8];   // debug timestamps
@@ -92,6 +92,8 @@ struct Params {
     // matrix keeps their raw tails for the step's table builds (no staging)
     u64* ubuf;
     u32 ucap;
+    u32* ap_claim;   // persistent driver: per step, pre-work chunks claimed / done
+    u32* ap_done;
     // sharded driver only (null / 0 otherwise)
     u32* inv;        // global row -> position (kept in step with perm)
     u32* status;     // panel status words (see kPanelStatus*)
@@ -109,6 +111,27 @@ constexpr int kStatusOwners = 8; // 2 words per rank: bitmask of pivots t owned
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ u64 low_mask64(int k) {
     return k >= 64 ? ~0ull : ((1ull << k) - 1ull);
+}
+
+// Last 64-byte tile of step w's look-ahead sweep (the tiles holding words
+// w+1 and w+2).
+__device__ __forceinline__ u32 cap_last_tile(u32 w, u32 W) {
+    return (w + 2u < W) ? ((w + 2u) >> 3) : ((w + 1u) >> 3);
+}
+// Step w's look-ahead tiles are all among step w-1's (or untouched, w = 0):
+// every row of them is final once step w-1's look-ahead sweep is done.
+__device__ __forceinline__ bool early_cap(u32 w, u32 W) {
+    return w == 0u || cap_last_tile(w, W) <= cap_last_tile(w - 1u, W);
+}
+// Persistent driver: rows per pre-work chunk (apply + look-ahead sweep) of a
+// step with `nrows` active rows, and the chunk count. Many small chunks when
+// few rows are left (latency), up to 1024 rows when many (fewer table builds).
+__device__ __forceinline__ u32 pw_rows(u32 nrows) {
+    return min(1024u, 64u * max(1u, (nrows + 64u * 128u - 1u) / (64u * 128u)));
+}
+__device__ __forceinline__ u32 pw_chunks(u32 nrows) {
+    const u32 c = pw_rows(nrows);
+    return (nrows + c - 1u) / c;
 }
 
 __device__ __forceinline__ u64* tword(u64* mat, u32 m, u32 row, u32 x) {
@@ -152,6 +175,24 @@ __device__ __forceinline__ bool spin_geq(const u32* a, u32 target, u32* err) {
     const u64 t0 = globaltimer();
     for (;;) {
         if (ld_acquire(a) >= target) return true;
+        if (*(volatile u32*)err) return false;
+        if (globaltimer() - t0 > 4000000000ull) {
+            atomicExch(err, 1u);
+            return false;
+        }
+        __nanosleep(64);
+    }
+}
+
+// Both counters at once (their loads in flight together).
+__device__ __forceinline__ bool spin_geq2(const u32* a, u32 ta, const u32* b, u32 tb, u32* err) {
+    u32 va = ld_acquire(a), vb = ld_acquire(b);
+    if (va >= ta && vb >= tb) return true;
+    const u64 t0 = globaltimer();
+    for (;;) {
+        va = ld_acquire(a);
+        vb = ld_acquire(b);
+        if (va >= ta && vb >= tb) return true;
         if (*(volatile u32*)err) return false;
         if (globaltimer() - t0 > 4000000000ull) {
             atomicExch(err, 1u);

@@ -5,11 +5,14 @@
 // look-ahead tile (the 64-byte tile holding word w+1) of step w, i.e. while
 // the workers are still streaming the rest of step w's trailing update.
 // CTAs 1..G-1 are workers: per step they
-//   apply   their row slab (multipliers, d, compressed words),
+//   claim   pre-work chunks (apply a chunk of rows -- multipliers, d,
+//           compressed words -- then sweep them over the look-ahead tiles;
+//           the panel CTA waits on their completion count), so the workers
+//           idle at the step barrier do it and the last one finds none left,
 //   wait    until every worker finished step w-1 (the pivot rows' raw tails
 //           are then final; tables read them in place, and the pivot rows'
-//           own swept tails go to ubuf, so no staging copy is needed),
-//   update  the look-ahead tiles for their row slab, signal the panel CTA,
+//           own swept tails go to ubuf, so no staging copy is needed) and all
+//           pre-work of step w is done,
 //   update  their linear share of the remaining tiles.
 // Cross-CTA ordering uses release/acquire counters in SyncState; every wait
 // has a watchdog so a bug turns into an error code, not a hung GPU. The grid
@@ -52,9 +55,13 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         // Look-ahead: step w+1's window words are computed at the end of step
         // w, so the next factorization starts at once; only its scans and its
         // writeback wait for the workers' look-ahead capture of step w.
-        LookAhead la{0u, false, &sy->cap_count, 0u, &sy->error};
+        LookAhead la{0u, false, p.ap_done, 0u, &sy->error};
+        u32 prev_r = 0u;
         for (u32 w = 0; w < nsteps; ++w) {
-            la.cap_target = nworkers * w;
+            // step w-1's look-ahead capture = all of its pre-work chunks
+            la.cap_ctr = p.ap_done + (w > 0 ? w - 1 : 0);
+            la.cap_target = w > 0 ? pw_chunks(p.m - prev_r) : 0u;
+            prev_r = la.r;
             stamp(p, w, 0);
             const u32 rb = panel_factor_body(p, w, psh, blockDim.x, &la);
             stamp(p, w, 1);
@@ -79,47 +86,69 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         Params q = p;
         q.info = p.info + (size_t)(w & 1u) * p.m;
         const u32 nrows = p.m - r;
-        const u32 slab = (nrows + nworkers - 1) / nworkers;
-        const u32 lo = min(p.m, r + wk * slab), hi = min(p.m, lo + slab);
-
-        if (wk == 0) stamp(p, w, 2);
-        // apply: own slab
-        apply_load(q, ash, rb);
-        __syncthreads();
-        apply_rows(q, ash, w, r, rb, lo, hi, threadIdx.x, blockDim.x);
-        // the pivot rows' raw tails are final once every worker finished step
-        // w-1; the tables read them in place (their own swept tails go to ubuf)
-        if (w > 0 && !cta_wait(sy, &sy->t_count, nworkers * w, s_ok)) return;
+        const bool sweep = w + 1 < p.W;
+        const u32 tile0 = (w + 1) >> 3, tcap = cap_last_tile(w, p.W);
+        const u32 crow = pw_rows(nrows), nch = pw_chunks(nrows);
         for (u32 k = threadIdx.x; k < rb; k += blockDim.x) s_piv[k] = ldcg(p.perm + r + k);
         __syncthreads();
+        if (wk == 0) stamp(p, w, 2);
 
-        if (wk == 0) stamp(p, w, 3);
-        const u32 tile0 = (w + 1) >> 3;
-        if (w + 1 < p.W) {
-            // look-ahead tiles (those holding words w+1 and w+2): own slab,
-            // then release the panel CTA
-            const u32 tcap = (w + 2 < p.W) ? ((w + 2) >> 3) : tile0;
-            if (hi > lo) {
+        // Pre-work chunks of step w (apply + look-ahead tiles of crow rows),
+        // claimed from a per-step counter: the workers waiting for the last
+        // one of step w-1 do (nearly) all of it. Its tiles were finished by
+        // step w-1's look-ahead sweep, unless a new tile joins this step.
+        if (sweep && !early_cap(w, p.W) && w > 0 &&
+            !cta_wait(sy, &sy->t_count, nworkers * w, s_ok))
+            return;
+        u32 mine = 0;
+        bool loaded = false;
+        for (;;) {
+            if (threadIdx.x == 0) s_ok = atomicAdd(&p.ap_claim[w], 1u);
+            __syncthreads();
+            const u32 c = s_ok;
+            __syncthreads();
+            if (c >= nch) break;
+            if (!loaded) {  // pout is step w's while any chunk of it is open
+                apply_load(q, ash, rb);
+                __syncthreads();
+                loaded = true;
+            }
+            const u32 a0 = r + c * crow, a1 = min(p.m, a0 + crow);
+            apply_rows(q, ash, w, r, rb, a0, a1, threadIdx.x, blockDim.x);
+            if (sweep) {
                 for (u32 tt = tile0; tt <= tcap; ++tt) {
+                    __syncthreads();
                     if (rb > 0) {
-                        __syncthreads();
                         build_tables(q, smem, tt, w, rb, s_piv);
                         __syncthreads();
                     }
-                    trail_rows(q, smem, w, r, tt, lo - r, hi - lo, rb);
+                    trail_rows(q, smem, w, r, tt, a0 - r, a1 - a0, rb);
                 }
             }
-            cta_arrive(&sy->cap_count);
-            if (wk == 0) stamp(p, w, 4);
+            ++mine;
+        }
+        if (mine) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                red_release_add(&p.ap_done[w], mine);
+            }
+        }
+        // the rest: after step w-1 everywhere (the pivot rows' raw tails are
+        // final; tables read them in place, their swept tails go to ubuf) and
+        // all pre-work of step w (every row's info and compressed words)
+        if (threadIdx.x == 0)
+            s_ok = spin_geq2(&sy->t_count, nworkers * w, &p.ap_done[w], nch, &sy->error) ? 1u : 0u;
+        __syncthreads();
+        if (!s_ok) return;
+        if (wk == 0) stamp(p, w, 3);
+        if (sweep) {
             if (p.worker_ns && threadIdx.x == 0)
                 p.worker_ns[((size_t)w * nworkers + wk) * 2] = globaltimer();
-            // remaining tiles: linear share
             const u32 nt = (p.Wpad8 >> 3) - tcap - 1;
             const u64 total = (u64)nt * nrows;
             trail_share(q, smem, w, r, rb, tcap + 1, total * wk / nworkers,
                         total * (wk + 1) / nworkers, s_piv);
-        } else {
-            cta_arrive(&sy->cap_count);
         }
         if (p.worker_ns && threadIdx.x == 0) {
             p.worker_ns[((size_t)w * nworkers + wk) * 2 + 1] = globaltimer();
