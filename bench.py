@@ -71,8 +71,9 @@ def load_peaks():
 
 
 def load_traffic():
-    """DRAM bytes per trailing_update launch from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "trailing_traffic.json")
+    """DRAM bytes per algorithmic byte of the dominant kernel (the persistent
+    PLE kernel) from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "persistent_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -334,9 +335,11 @@ def gpu_arm(args, rank, world, local_rank):
         "peak_source": (f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                         else "fallback 6.65 TB/s"),
         "share_of_step": round(kern_ms / max(1e-9, dev_ms), 4),
+        # worker 0's device timestamps: rest sweep / panel CTA busy (overlapped
+        # with the sweep) / pre-work chunks (apply + look-ahead tiles) + step barrier
         "phases_ms_per_launch": {"trailing_sweep": round(trail_ms / max(1, launches), 3),
                                  "panel_factor_overlapped": round(panel_ms / max(1, launches), 3),
-                                 "apply_stage_barriers": round(apply_ms / max(1, launches), 3)},
+                                 "prework_and_step_barrier": round(apply_ms / max(1, launches), 3)},
         "trailing_sweep_GBps": round(per_launch_bytes / (trail_ms / max(1, launches) * 1e-3) / 1e9, 1)
         if trail_ms > 0 else None,
     }

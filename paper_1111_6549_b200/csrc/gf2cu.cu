@@ -270,6 +270,8 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         if (!ws.apctr) CU_TRY(cudaMalloc(&ws.apctr, 2 * (W + 1) * sizeof(u32)));
         p.ap_claim = ws.apctr;
         p.ap_done = ws.apctr + W + 1;
+        const char* dv = std::getenv("GF2CU_PW_DIV");
+        p.pw_div = dv ? (u32)std::max(64, std::atoi(dv)) : 8192u;
     }
 
     if (timing) {

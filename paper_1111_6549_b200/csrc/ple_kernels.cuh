@@ -94,6 +94,7 @@ struct Params {
     u32 ucap;
     u32* ap_claim;   // persistent driver: per step, pre-work chunks claimed / done
     u32* ap_done;
+    u32 pw_div;      // rows per 64 pre-work rows (chunk size tuning)
     // sharded driver only (null / 0 otherwise)
     u32* inv;        // global row -> position (kept in step with perm)
     u32* status;     // panel status words (see kPanelStatus*)
@@ -126,11 +127,11 @@ __device__ __forceinline__ bool early_cap(u32 w, u32 W) {
 // Persistent driver: rows per pre-work chunk (apply + look-ahead sweep) of a
 // step with `nrows` active rows, and the chunk count. Many small chunks when
 // few rows are left (latency), up to 1024 rows when many (fewer table builds).
-__device__ __forceinline__ u32 pw_rows(u32 nrows) {
-    return min(1024u, 64u * max(1u, (nrows + 64u * 128u - 1u) / (64u * 128u)));
+__device__ __forceinline__ u32 pw_rows(u32 nrows, u32 div) {
+    return min(1024u, 64u * max(1u, (nrows + div - 1u) / div));
 }
-__device__ __forceinline__ u32 pw_chunks(u32 nrows) {
-    const u32 c = pw_rows(nrows);
+__device__ __forceinline__ u32 pw_chunks(u32 nrows, u32 div) {
+    const u32 c = pw_rows(nrows, div);
     return (nrows + c - 1u) / c;
 }
 

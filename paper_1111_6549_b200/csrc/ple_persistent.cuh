@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         for (u32 w = 0; w < nsteps; ++w) {
             // step w-1's look-ahead capture = all of its pre-work chunks
             la.cap_ctr = p.ap_done + (w > 0 ? w - 1 : 0);
-            la.cap_target = w > 0 ? pw_chunks(p.m - prev_r) : 0u;
+            la.cap_target = w > 0 ? pw_chunks(p.m - prev_r, p.pw_div) : 0u;
             prev_r = la.r;
             stamp(p, w, 0);
             const u32 rb = panel_factor_body(p, w, psh, blockDim.x, &la);
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         const u32 nrows = p.m - r;
         const bool sweep = w + 1 < p.W;
         const u32 tile0 = (w + 1) >> 3, tcap = cap_last_tile(w, p.W);
-        const u32 crow = pw_rows(nrows), nch = pw_chunks(nrows);
+        const u32 crow = pw_rows(nrows, p.pw_div), nch = pw_chunks(nrows, p.pw_div);
         for (u32 k = threadIdx.x; k < rb; k += blockDim.x) s_piv[k] = ldcg(p.perm + r + k);
         __syncthreads();
         if (wk == 0) stamp(p, w, 2);
