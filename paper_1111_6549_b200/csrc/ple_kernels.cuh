@@ -203,20 +203,6 @@ __device__ __forceinline__ bool spin_geq2(const u32* a, u32 ta, const u32* b, u3
     }
 }
 
-// 32x32 bit transpose across a warp: on return lane l bit b = input lane b
-// bit l.
-__device__ __forceinline__ u32 transpose32(u32 x) {
-    const u32 lane = threadIdx.x & 31u;
-    const u32 hi[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int j = 16 >> k;
-        const u32 y = __shfl_xor_sync(0xffffffffu, x, j);
-        x = (lane & j) ? ((x & hi[k]) | ((y >> j) & ~hi[k])) : ((x & ~hi[k]) | ((y << j) & hi[k]));
-    }
-    return x;
-}
-
 // ---------------------------------------------------------------------------
 // layout conversion: row-major (stride Wp) <-> tile-major; untile also
 // gathers rows into position order through perm.
@@ -365,30 +351,6 @@ __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u3
         sh.o_phys = ldcg(p.perm + r + off);
     }
     named_bar(2, nthr);
-}
-
-// Transposed window state of warp 0: lane l owns panel columns l and l+32
-// (M[h], h = 0/1) and coefficient columns (pivot indices) l and l+32 (A[h]);
-// each is a 128-bit mask over the window rows (lo = rows 0..63, hi = 64..127).
-struct Col128 {
-    u64 lo, hi;
-};
-
-// Row swap t <-> p on one column mask, then the elimination XOR of the rows
-// R when the pivot row holds a 1 here (xor_if_set) or unconditionally (force).
-// Returns the pivot row's bit (bit t after the swap).
-__device__ __forceinline__ bool swap_elim(Col128& x, u64 tm, u64 pl, u64 ph, int t, u64 Rlo,
-                                          u64 Rhi, bool xor_if_set, bool force) {
-    const u64 bt = (x.lo >> t) & 1ull;
-    const u64 bp = ((x.lo & pl) | (x.hi & ph)) ? 1ull : 0ull;
-    const u64 dm = 0ull - (bt ^ bp);
-    x.lo ^= dm & (tm | pl);
-    x.hi ^= dm & ph;
-    const bool piv = bp != 0;
-    const u64 cm = 0ull - (u64)(force || (xor_if_set && piv));
-    x.lo ^= cm & Rlo;
-    x.hi ^= cm & Rhi;
-    return piv;
 }
 
 // The panel step w. Called by every thread of ONE CTA of `nthr` >= 256
