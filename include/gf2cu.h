@@ -236,6 +236,10 @@ gf2cu_status gf2cu_shard_finish(gf2cu_shard* s, size_t* swaps, size_t* q, size_t
 gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t stride, double density,
                                uint64_t seed);
 /* SURVEY.md 8(d) counter generator. */
+/* gf2::fill_random_rows (bit_matrix.hpp:489-520): exactly nnz ones per row,
+ * the reference's engine and draw order. GF2CU_EINVAL if nnz > n. */
+gf2cu_status gf2cu_fill_random_rows(uint64_t* words, size_t m, size_t n, size_t stride, size_t nnz,
+                                    uint64_t seed);
 gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, uint64_t seed);
 
 #ifdef __cplusplus

@@ -93,6 +93,10 @@ def ref():
         R.ref_rref_from_ple.restype = C.c_int
         R.ref_reconstructs.argtypes = [_u64p, _u64p, _sz, _sz, _sz, _sz, _szp, _szp, _szp, _sz]
         R.ref_reconstructs.restype = C.c_int
+        R.ref_save_matrix.argtypes = [_u64p, _sz, _sz, _sz, C.c_int, C.c_char_p, _sz]
+        R.ref_save_matrix.restype = C.c_longlong
+        R.ref_load_matrix.argtypes = [C.c_char_p, _sz, _u64p, _sz, _szp, _szp, C.c_char_p, _sz]
+        R.ref_load_matrix.restype = C.c_int
         R.ref_echelonize.argtypes = [_u64p, _sz, _sz, _sz, C.c_int, C.c_int]
         R.ref_echelonize.restype = C.c_longlong
         R.ref_trsm_upper_left_unit.argtypes = [_u64p, _sz, _sz, _u64p, _sz, _sz]
@@ -285,3 +289,26 @@ def ref_echelonize(a: np.ndarray, m: int, n: int, strategy: str = "ple_iterative
 def ref_trsm_upper_left_unit(u: np.ndarray, r: int, b: np.ndarray, n: int) -> None:
     if ref().ref_trsm_upper_left_unit(_u64(u), r, u.shape[1], _u64(b), n, b.shape[1]) != 0:
         raise RuntimeError("reference trsm_upper_left_unit threw")
+
+
+def ref_save_matrix(a: np.ndarray, m: int, n: int, ascii: bool = False) -> bytes:
+    """The reference's save_gf2b / save_ascii output bytes."""
+    cap = 64 + m * (n + 1) + 8 * a.size + 64
+    buf = C.create_string_buffer(cap)
+    got = ref().ref_save_matrix(_u64(a), m, n, a.shape[1] if a.ndim == 2 else 1, int(ascii), buf, cap)
+    if got < 0:
+        raise RuntimeError("reference save threw")
+    return buf.raw[:got]
+
+
+def ref_load_matrix(data: bytes):
+    """The reference's load_matrix: (m, n, words) or ('io_error', message)."""
+    cap = max(1, len(data) // 8 + 16)
+    words = np.zeros(cap, dtype=np.uint64)
+    m, n = C.c_size_t(), C.c_size_t()
+    err = C.create_string_buffer(256)
+    rc = ref().ref_load_matrix(data, len(data), _u64(words), cap, C.byref(m), C.byref(n), err, 256)
+    if rc != 0:
+        return ("io_error" if rc == 1 else "error", err.value.decode())
+    W = max(1, (n.value + 63) // 64)
+    return m.value, n.value, words[: m.value * W].reshape(m.value, W) if m.value else np.zeros((0, W), np.uint64)

@@ -12,6 +12,9 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include "gf2/io.hpp"
+#include <cstdio>
+#include <sstream>
 #include <exception>
 #include <vector>
 
@@ -198,6 +201,48 @@ int ref_trsm_upper_left_unit(const std::uint64_t* u, std::size_t r, std::size_t 
         return 0;
     } catch (const std::exception&) {
         return -1;
+    }
+}
+
+// gf2::save_gf2b / save_ascii (io.hpp:59-76) into a caller buffer: returns
+// the byte count (or -1 when it does not fit / the writer threw).
+long long ref_save_matrix(const std::uint64_t* words, std::size_t m, std::size_t n,
+                          std::size_t stride, int ascii, char* out, std::size_t cap) {
+    try {
+        gf2::BitMatrix a(m, n);
+        const std::size_t W = (n + 63) / 64;
+        for (std::size_t i = 0; i < m; ++i) std::memcpy(a.row_words(i), words + i * stride, W * 8);
+        std::ostringstream os;
+        if (ascii) gf2::save_ascii(os, a); else gf2::save_gf2b(os, a);
+        const std::string s = os.str();
+        if (s.size() > cap) return -1;
+        std::memcpy(out, s.data(), s.size());
+        return (long long)s.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// gf2::load_matrix (io.hpp:113-122) from a buffer. Returns 0 and the shape
+// (words copied when they fit in `cap` words at stride ceil(n/64)), 1 when
+// the loader threw io_error (its message copied to err).
+int ref_load_matrix(const char* buf, std::size_t len, std::uint64_t* words, std::size_t cap,
+                    std::size_t* m, std::size_t* n, char* err, std::size_t errcap) {
+    try {
+        std::istringstream is(std::string(buf, len));
+        gf2::BitMatrix a = gf2::load_matrix(is);
+        *m = a.nrows();
+        *n = a.ncols();
+        const std::size_t W = (a.ncols() + 63) / 64;
+        if (a.nrows() * W <= cap)
+            for (std::size_t i = 0; i < a.nrows(); ++i) std::memcpy(words + i * W, a.row_words(i), W * 8);
+        return 0;
+    } catch (const gf2::io_error& e) {
+        std::snprintf(err, errcap, "%s", e.what());
+        return 1;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errcap, "%s", e.what());
+        return 2;
     }
 }
 

@@ -26,6 +26,7 @@ from .ple import (  # noqa: F401
     extract_l,
     fill_ctr,
     fill_random,
+    fill_random_rows,
     host_checksum,
     rref_from_ple,
     trsm_upper_left_unit,
@@ -36,6 +37,6 @@ __all__ = [
     "BitMatrix", "ColSwap", "DeviceMatrix", "MatrixView", "PleConfig", "PleOutcome",
     "RowPermutation", "block_iterative_ple", "device_count", "fill_ctr", "fill_random",
     "host_checksum", "words_per_row", "build", "load", "echelonize", "extract_e", "extract_l",
-    "rref_from_ple", "trsm_upper_left_unit", "addmul", "mul", "mul_into", "recursive_ple",
+    "rref_from_ple", "trsm_upper_left_unit", "fill_random_rows", "addmul", "mul", "mul_into", "recursive_ple",
     "echelonize_strategy",
 ]

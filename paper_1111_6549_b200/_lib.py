@@ -128,6 +128,7 @@ SYMBOLS = {
     "gf2cu_shard_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),
     "gf2cu_fill_random": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_double, C.c_uint64]),
     "gf2cu_fill_ctr": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_uint64]),
+    "gf2cu_fill_random_rows": (C.c_int, [_u64p, _sz, _sz, _sz, _sz, C.c_uint64]),
 }
 
 _lib = None

@@ -1457,6 +1457,53 @@ gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t strid
     return GF2CU_OK;
 }
 
+gf2cu_status gf2cu_fill_random_rows(uint64_t* words, size_t m, size_t n, size_t stride, size_t nnz,
+                                    uint64_t seed) {
+    // gf2::fill_random_rows (bit_matrix.hpp:489-520): exactly nnz ones per
+    // row, same engine and draw order (partial Fisher-Yates when nnz > n/2,
+    // rejection sampling otherwise; bounded draws by masked rejection).
+    if (nnz > n) return fail(GF2CU_EINVAL, "nnz exceeds column count");
+    const size_t W = words_of(n);
+    if (m && W && !words) return fail(GF2CU_EINVAL, "null words");
+    if (stride < W) return fail(GF2CU_EINVAL, "stride smaller than the row");
+    std::mt19937_64 rng(seed);
+    auto bounded = [&](u64 lim) -> u64 {
+        if (lim == 1) return 0;
+        const int bits = 64 - __builtin_clzll(lim - 1);
+        const u64 mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+        u64 v;
+        do {
+            v = rng() & mask;
+        } while (v >= lim);
+        return v;
+    };
+    std::vector<u32> pool;
+    for (size_t i = 0; i < m; ++i) {
+        u64* row = reinterpret_cast<u64*>(words) + i * stride;
+        std::fill(row, row + W, 0ull);
+        if (nnz * 2 > n) {
+            pool.resize(n);
+            for (size_t j = 0; j < n; ++j) pool[j] = (u32)j;
+            for (size_t j = 0; j < nnz; ++j) {
+                const size_t pick = j + (size_t)bounded(n - j);
+                std::swap(pool[j], pool[pick]);
+                row[pool[j] >> 6] |= 1ull << (pool[j] & 63);
+            }
+        } else {
+            size_t placed = 0;
+            while (placed < nnz) {
+                const size_t q = (size_t)bounded(n);
+                const u64 bit = 1ull << (q & 63);
+                if (!(row[q >> 6] & bit)) {
+                    row[q >> 6] |= bit;
+                    ++placed;
+                }
+            }
+        }
+    }
+    return GF2CU_OK;
+}
+
 gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, uint64_t seed) {
     const size_t W = words_of(n);
     if (m && W && !words) return fail(GF2CU_EINVAL, "null words");

@@ -239,6 +239,13 @@ def fill_random(a: BitMatrix, density: float, seed: int) -> None:
                               a.stride(), float(density), int(seed) & (2**64 - 1)))
 
 
+def fill_random_rows(a: BitMatrix, nnz: int, seed: int) -> None:
+    """gf2::fill_random_rows (bit_matrix.hpp:489-520), host-side."""
+    L = _lib.load()
+    check(L.gf2cu_fill_random_rows(a.words.ctypes.data_as(C.POINTER(C.c_uint64)), a.nrows(),
+                                   a.ncols(), a.stride(), int(nnz), int(seed) & (2**64 - 1)))
+
+
 def fill_ctr(a: BitMatrix, seed: int) -> None:
     """The counter generator of SURVEY.md 8(d) (random access; the device
     generator DeviceMatrix.fill_ctr produces the same words)."""
