@@ -70,6 +70,20 @@ def run_ple(o) -> int:
     if o.inject_fault and work.nrows() and work.ncols():
         work.set(0, 0, not work.get(0, 0))
     if o.verify:
+        # the state invariants extract_e's closed form relies on (SURVEY.md
+        # 8(c)): pivots on the diagonal, rows >= rank zero from column rank on
+        r, n = out.rank, work.ncols()
+        if r:
+            idx = np.arange(r)
+            if not np.all((work.words[idx, idx >> 6] >> (idx & 63).astype(np.uint64)) & np.uint64(1)):
+                raise VerifyError("P*L*E does not reproduce the input")
+        if r < work.nrows() and r < n:
+            tail = work.words[r:].copy()
+            tail[:, : r >> 6] = 0
+            if r & 63:
+                tail[:, r >> 6] &= ~np.uint64((1 << (r & 63)) - 1)
+            if tail.any():
+                raise VerifyError("P*L*E does not reproduce the input")
         l, e = extract_l(work, out), extract_e(work, out)
         back = mul(l, e) if out.rank else BitMatrix(out.processed, work.ncols())
         out.p.apply_inverse(back.words)
