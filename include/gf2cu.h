@@ -62,6 +62,11 @@ typedef struct {
 #define GF2CU_FLAG_TIME_KERNELS 1u /* record CUDA events / device timestamps */
 #define GF2CU_FLAG_MULTI_KERNEL 2u /* one launch per phase instead of the
                                       persistent cooperative kernel          */
+#define GF2CU_FLAG_SINGLE_PANEL 4u /* force the persistent kernel with one
+                                      64-column panel per trailing sweep     */
+#define GF2CU_FLAG_SUPER_STEP 8u   /* force the super-step kernel: two panels
+                                      per sweep (default: chosen by size --
+                                      super-step from 2^24 matrix words)     */
 
 /* Mirrors gf2::ColSwap (ple.hpp:41-43). */
 typedef struct {
@@ -78,7 +83,8 @@ typedef struct {
     double alg_bytes;           /* sum over steps of 16*(m-r-rb)*(W-w-1)        */
     double h2d_bytes, d2h_bytes;/* host<->device bytes moved by gf2cu_ple       */
     double kernel_ms;           /* persistent kernel duration (CUDA events)     */
-    int driver;                 /* 1 = persistent cooperative, 0 = per phase    */
+    int driver;                 /* 2 = super-step (two panels per sweep),
+                                   1 = persistent single-panel, 0 = per phase   */
 } gf2cu_stats;
 
 /* Fills *cfg with the reference defaults (k=0, k_scale=0.75, table_count=4,

@@ -82,6 +82,8 @@ class gf2cu_stats(C.Structure):
 
 FLAG_TIME_KERNELS = 1
 FLAG_MULTI_KERNEL = 2
+FLAG_SINGLE_PANEL = 4
+FLAG_SUPER_STEP = 8
 
 # name -> (restype, argtypes): every symbol include/gf2cu.h declares.
 _sz, _szp = C.c_size_t, C.POINTER(C.c_size_t)

@@ -20,6 +20,7 @@
 #include "gf2cu.h"
 #include "ple_kernels.cuh"
 #include "ple_persistent.cuh"
+#include "ple_super.cuh"
 #include "ple_shard.cuh"
 #include "rref_kernels.cuh"
 #include "gemm_kernels.cuh"
@@ -72,6 +73,8 @@ struct Workspace {
     u64* ubuf = nullptr;         // persistent driver: swept pivot-row tails
     size_t ucap = 0;
     u32* apctr = nullptr;        // persistent driver: per-step pre-work chunk counters
+    gf2cu::PanelOut* pout_b = nullptr;  // super-step driver: panel b's outputs
+    gf2cu::SuperOut* sout = nullptr;
     std::vector<cudaEvent_t> ev;
 };
 
@@ -92,6 +95,8 @@ void free_ws(Workspace& w) {
     cudaFree(w.phase_ns);
     cudaFree(w.ubuf);
     cudaFree(w.apctr);
+    cudaFree(w.pout_b);
+    cudaFree(w.sout);
     if (w.host_r) cudaFreeHost(w.host_r);
     for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
     w = Workspace{};
@@ -183,7 +188,9 @@ gf2cu_status ensure_ws(gf2cu_matrix* a) {
     CU_TRY(cudaMalloc(&w.perm, std::max<size_t>(1, m) * sizeof(u32)));
     CU_TRY(cudaMalloc(&w.pb, std::max<size_t>(1, m) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.pb2, std::max<size_t>(1, m) * sizeof(u64)));
-    CU_TRY(cudaMalloc(&w.info, 2 * std::max<size_t>(1, m) * sizeof(ulonglong2)));
+    CU_TRY(cudaMalloc(&w.info, 4 * std::max<size_t>(1, m) * sizeof(ulonglong2)));
+    CU_TRY(cudaMalloc(&w.pout_b, sizeof(gf2cu::PanelOut)));
+    CU_TRY(cudaMalloc(&w.sout, sizeof(gf2cu::SuperOut)));
     CU_TRY(cudaMalloc(&w.sync, sizeof(gf2cu::SyncState)));
     CU_TRY(cudaMalloc(&w.phase_ns, (8 * (a->W + 1) + 8 + 2 * 64 * 5 + 3 * 160) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.stage, 64 * wpad8(a->W) * sizeof(u64)));
@@ -255,11 +262,21 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         CU_TRY(cudaFuncSetAttribute(gf2cu::ple_persistent_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     gf2cu::kTableBytes));
+        CU_TRY(cudaFuncSetAttribute(gf2cu::ple_super_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    gf2cu::kTableBytes));
         attr_set[a->device] = true;
     }
     const int sms = num_sms(a->device);
     const int apply_grid = sms * 4;
     const bool multi = cfg && (cfg->flags & GF2CU_FLAG_MULTI_KERNEL);
+    // Two panels per sweep halve the sweep's global traffic and the per-step
+    // synchronization, but the panel CTA's chain per super-step is longer:
+    // it pays from ~2^24 matrix words up (measured crossover near 32768^2).
+    const unsigned fl = cfg ? cfg->flags : 0u;
+    const bool super = !multi && !(fl & GF2CU_FLAG_SINGLE_PANEL) &&
+                       ((fl & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= 16777216.0);
+    const u32 Wpad4 = (u32)std::max<size_t>(4, (W + 3) / 4 * 4);
     if (!multi) {
         if (!ws.ubuf) {
             ws.ucap = std::max<size_t>(1, std::min(m, n));
@@ -284,8 +301,14 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
 
     *ws.host_r = 0;
-    gf2cu::tile_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, p.Wpad8);
-    gf2cu::ple_init_kernel<<<sms * 4, 256, 0, s>>>(p);
+    if (super) {
+        p.Wpad8 = Wpad4;  // the super-step driver's tile width is 32 bytes
+        gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4);
+        gf2cu::ple_init4_kernel<<<sms * 4, 256, 0, s>>>(p, a->data, (u32)a->Wp);
+    } else {
+        gf2cu::tile_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, p.Wpad8);
+        gf2cu::ple_init_kernel<<<sms * 4, 256, 0, s>>>(p);
+    }
     CU_TRY(cudaGetLastError());
 
     size_t steps = 0;
@@ -313,8 +336,15 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             CU_TRY(cudaMemsetAsync(wns, 0, wn_words * sizeof(u64), s));
         }
         p.worker_ns = wns;
-        CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_persistent_kernel, dim3(grid),
-                                           dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
+        if (super) {
+            u32 nss = (u32)((W + 1) / 2);
+            void* sargs[] = {&p, &ws.pout_b, &ws.sout, &nss};
+            CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_super_kernel, dim3(grid),
+                                               dim3(gf2cu::kTrailThreads), sargs, gf2cu::kTableBytes, s));
+        } else {
+            CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_persistent_kernel, dim3(grid),
+                                               dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
+        }
         if (E) cudaEventRecord(E[1], s);
         gf2cu::SyncState sy{};
         CU_TRY(cudaMemcpyAsync(&sy, ws.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
@@ -331,7 +361,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             }
         }
         if (sy.error) return fail(GF2CU_ECUDA, "persistent PLE kernel watchdog tripped");
-        steps = sy.panel_done;
+        steps = super ? std::min<size_t>(W, 2 * (size_t)sy.panel_done) : sy.panel_done;
         if (E) cudaEventElapsedTime(&kernel_ms, E[0], E[1]);
     } else {
         // ---- one launch per phase ----
@@ -377,8 +407,12 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
 
     // back to the row-major public layout, rows gathered into position order
-    gf2cu::untile_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
-                                                p.Wpad8, p.ubuf, p.ucap, ws.qcol, (u32)rk, (u32)W);
+    if (super)
+        gf2cu::untile4_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
+                                                     Wpad4, p.ubuf, p.ucap, ws.qcol, (u32)rk, (u32)W);
+    else
+        gf2cu::untile_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
+                                                    p.Wpad8, p.ubuf, p.ucap, ws.qcol, (u32)rk, (u32)W);
     CU_TRY(cudaGetLastError());
 
     std::vector<u32> sw(rk), qq(rk);
@@ -412,7 +446,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         stats->alg_bytes = bytes;
         stats->trailing_launches = launches;
         stats->kernel_ms = kernel_ms;
-        stats->driver = multi ? 0 : 1;
+        stats->driver = multi ? 0 : super ? 2 : 1;
         if (timing && !multi) {
             std::vector<u64> ph(8 * steps);
             CU_TRY(cudaMemcpy(ph.data(), ws.phase_ns, ph.size() * sizeof(u64), cudaMemcpyDeviceToHost));

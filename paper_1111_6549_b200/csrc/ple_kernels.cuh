@@ -290,6 +290,15 @@ struct PanelShared {
     u64 dacc[kWin];     // per window slot: d (its combination) and origin
     u32 dorg[kWin];
     int cap_ok;
+    // super-step driver
+    int super;          // 0, 1 (panel a) or 2 (panel b)
+    u64 wraw2[kWin];    // window rows' pre-super-step word w+1 (as loaded)
+    u64 ndacc[kWin];    // panel a: panel-a combination of each next-window slot
+    u64 oda[64];        // panel b: panel-a combination of pivots taken from outside
+    u64 o_da;
+    u64 Ea[64], Da[64]; // panel a's outputs, kept for panel b's miss scans
+    u32 qa[64];
+    u32 rba;
 };
 
 // Look-ahead mode of panel_factor_body (persistent driver): the step's r is
@@ -303,6 +312,10 @@ struct LookAhead {
     const u32* cap_ctr;
     u32 cap_target;
     u32* err;
+    // super-step driver (two 64-column panels per sweep): 1 = panel a, 2 = panel b
+    int super_mode = 0;
+    u64* piv2_out = nullptr;  // panel a: its pivot rows' pre-super-step word w+1
+    u64* C_out = nullptr;     // panel b: panel-a combination of each of its pivot rows
 };
 
 // All `nthr` threads: scan positions r + [nwin, nrem) reducing each raw panel
@@ -310,9 +323,21 @@ struct LookAhead {
 // >= j, offset), with the winner's reduced state in sh.o_*.
 __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem, int nthr) {
     const int t = sh.t, j = sh.j;
-    u64 best = ~0ull, b_red = 0, b_acc = 0;
+    const bool two = sh.super == 2;
+    u64 best = ~0ull, b_red = 0, b_acc = 0, b_da = 0;
     for (u32 off = nwin + threadIdx.x; off < nrem; off += nthr) {
-        u64 v = ldcg(p.pb + r + off), a = 0;
+        u64 v = ldcg(p.pb + r + off), a = 0, da = 0;
+        if (two) {
+            // panel b of a super-step: word w+1 after panel a, from the row's
+            // pre-super-step words (pb = word w, pb2 = word w+1)
+            for (u32 s = 0; s < sh.rba; ++s) {
+                const u64 msk = 0ull - ((v >> sh.qa[s]) & 1ull);
+                v ^= sh.Ea[s] & msk;
+                da ^= sh.Da[s] & msk;
+            }
+            v = ldcg(p.pb2 + r + off);
+            for (u32 s = 0; s < sh.rba; ++s) v ^= sh.piv2[s] & (0ull - ((da >> s) & 1ull));
+        }
         for (int s = 0; s < t; ++s) {
             const u64 msk = 0ull - ((v >> sh.q[s]) & 1ull);
             v ^= sh.E[s] & msk;
@@ -325,6 +350,7 @@ __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u3
                 best = key;
                 b_red = v;
                 b_acc = a;
+                b_da = da;
             }
         }
     }
@@ -348,7 +374,9 @@ __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u3
         sh.o_red = b_red;
         sh.o_acc = b_acc;
         sh.o_raw = ldcg(p.pb + r + off);
+        sh.o_raw2 = p.pb2 ? ldcg(p.pb2 + r + off) : 0ull;
         sh.o_phys = ldcg(p.perm + r + off);
+        sh.o_da = b_da;
     }
     named_bar(2, nthr);
 }
@@ -380,8 +408,14 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         }
         sh.t = 0;
         sh.cap_ok = la ? (la->cap_target == 0 ? 1 : 0) : 1;
+        sh.super = la ? la->super_mode : 0;
     }
     __syncthreads();
+    if (sh.super == 1 && !sh.cap_ok) {
+        // panel a reads its window from the previous super-step's capture
+        if (threadIdx.x == 0) sh.cap_ok = spin_geq(la->cap_ctr, la->cap_target, la->err) ? 1 : -1;
+        __syncthreads();
+    }
     const u32 r = sh.r;
     if (threadIdx.x == 0) {
         p.state->r = r;
@@ -419,8 +453,16 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         u64 red = 0ull, acc = 0ull;
         u32 org = me;  // window offset of the row this slot holds
         if (inwin) {
-            red = (la && la->have_window) ? sh.nraw[me] : ldcg(p.pb + r + me);
-            sh.wraw[me] = red;
+            if (sh.super) {
+                // keep the rows' pre-super-step words (pb, pb2): they follow
+                // the rows through the writeback for the workers' apply
+                sh.wraw[me] = ldcg(p.pb + r + me);
+                sh.wraw2[me] = ldcg(p.pb2 + r + me);
+                red = sh.super == 2 ? sh.nraw[me] : sh.wraw[me];
+            } else {
+                red = (la && la->have_window) ? sh.nraw[me] : ldcg(p.pb + r + me);
+                sh.wraw[me] = red;
+            }
             sh.wphys[me] = ldcg(p.perm + r + me);
         }
         named_bar(3, kWin);
@@ -499,7 +541,11 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 pacc = sh.o_acc;
                 porg = 0x80000000u | (u32)t;
                 if (me == (u32)t) {
-                    if (p.pb2 && w + 1 < p.W) {
+                    if (sh.super) {
+                        sh.opb2[t] = sh.o_raw2;
+                        p.pb2[r + P] = sh.wraw2[org];
+                        sh.oda[t] = sh.o_da;
+                    } else if (p.pb2 && w + 1 < p.W) {
                         // next-word capture follows the displaced window row
                         sh.opb2[t] = ldcg(p.pb2 + r + P);
                         p.pb2[r + P] = ldcg(p.pb2 + r + org);
@@ -547,8 +593,14 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             sh.t = aborted ? -1 : t;
         }
         named_bar(1, nthr);  // release the helpers
+        u64 rw2 = 0ull;
+        if (sh.super && inwin) {
+            const bool out = (org & 0x80000000u) != 0u;
+            rw2 = out ? sh.opb2[org & 63u] : sh.wraw2[org & 127u];
+        }
         if (inwin && !aborted) {
             p.pb[r + me] = rw;
+            if (sh.super) p.pb2[r + me] = rw2;
             p.perm[r + me] = ph;
             if (p.inv) p.inv[ph] = r + me;
         }
@@ -596,15 +648,38 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         }
     }
     __syncthreads();
-    if (la && w + 1 < p.W && r + t < p.m) {
-        // ---- next window: word w+1 after step w, for positions
-        //      [r + t, r + t + 128), from the pre-step capture pb2 ----
-        const u32 r1 = r + t;
-        const u32 nwin1 = min((u32)kWin, p.m - r1);
-        // pre-step word w+1 of each pivot row
+    if (sh.super == 2) {
+        // panel b: panel-a combination of each of its pivot rows
         for (u32 k = threadIdx.x; k < t; k += nthr) {
             const u32 o = sh.dorg[k];
-            sh.piv2[k] = (o & 0x80000000u) ? sh.opb2[o & 63u] : ldcg(p.pb2 + r + o);
+            la->C_out[k] = (o & 0x80000000u) ? sh.oda[o & 63u] : sh.ndacc[o & 127u];
+        }
+    }
+    if (sh.super == 1) {
+        // panel a: keep its outputs for panel b's miss scans
+        for (u32 k = threadIdx.x; k < t; k += nthr) {
+            sh.Ea[k] = sh.E[k];
+            sh.Da[k] = sh.D[k];
+            sh.qa[k] = sh.q[k];
+        }
+        if (threadIdx.x == 0) sh.rba = t;
+    }
+    if (la && sh.super != 2 && w + 1 < p.W && (r + t < p.m || sh.super == 1)) {
+        // ---- next window: word w+1 after step w, for positions
+        //      [r + t, r + t + 128), from the pre-step capture pb2 (the
+        //      super-step driver needs the pivot rows' word w+1 even when no
+        //      row is left for a next window) ----
+        const u32 r1 = r + t;
+        const u32 nwin1 = r1 < p.m ? min((u32)kWin, p.m - r1) : 0u;
+        // pre-step word w+1 of each pivot row
+        // (super-step driver: pb2 was permuted by the writeback; the window
+        // rows' pre-super-step words are in shared memory)
+        for (u32 k = threadIdx.x; k < t; k += nthr) {
+            const u32 o = sh.dorg[k];
+            sh.piv2[k] = (o & 0x80000000u) ? sh.opb2[o & 63u]
+                         : sh.super       ? sh.wraw2[o & 127u]
+                                          : ldcg(p.pb2 + r + o);
+            if (sh.super) la->piv2_out[k] = sh.piv2[k];
         }
         __syncthreads();
         for (u32 k = threadIdx.x; k < nwin1; k += nthr) {
@@ -612,7 +687,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             u64 d, pre;
             if (q - r < nwin) {
                 d = sh.dacc[q - r];
-                pre = ldcg(p.pb2 + r + sh.dorg[q - r]);
+                pre = sh.super ? sh.wraw2[sh.dorg[q - r] & 127u] : ldcg(p.pb2 + r + sh.dorg[q - r]);
             } else {
                 // a row entering the window: its combination for step w
                 u64 v = ldcg(p.pb + q);
@@ -631,6 +706,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 x ^= sh.piv2[s2] & (0ull - ((d >> s2) & 1ull));
             }
             sh.nraw[k] = x;
+            sh.ndacc[k] = d;
         }
         __syncthreads();
     }

@@ -1,0 +1,498 @@
+// ple_super.cuh -- super-step persistent driver: two 64-column panels per
+// trailing sweep (K = 128).
+//
+// The trailing sweep is bound by the L1 data pipe (8 table lookups of 64 B
+// per 64 B of row plus the global load and store). Fusing two panels into one
+// sweep keeps the lookups per panel but halves the global traffic and the
+// per-step synchronization. Because every row's update is a combination of
+// RAW pivot rows, two panels a, b fuse exactly:
+//
+//   new_tail = d~_a . R_a  ^  d_b . R_b,      d~_a = d_a ^ d_b . C
+//
+// R_a, R_b = the 64 + 64 pivot rows as they were before the super-step
+// (read in place; their own swept tails go to ubuf), d_a / d_b = the row's
+// combinations for panel a (from its word w) and panel b (from its word w+1
+// after panel a), C[t] = the panel-a combination of panel b's t-th pivot row.
+// 16 tables x 256 entries do not fit as 64-byte entries, so this driver uses
+// 32-byte tiles: word x of row i at ((x >> 2) * m + i) * 4 + (x & 3); a row's
+// 32-byte chunk is two lanes, a quarter-warp covers 4 rows which read 4
+// different tables placed in 4 different 32-byte bank quarters (conflict-free).
+//
+// Per super-step S (words w = 2S, w+1): the panel CTA factors panel a (window
+// from the previous super-step's capture of word w) and panel b (window =
+// word w+1 after panel a, computed by panel a's look-ahead); both writebacks
+// permute the rows' pre-super-step words (pb = word w, pb2 = word w+1). The
+// workers claim pre-work chunks (apply both panels, then sweep the chunk over
+// the look-ahead tile holding words w+2, w+3, capturing them into pb / pb2),
+// then sweep a linear share of the remaining tiles.
+#pragma once
+
+#include "ple_kernels.cuh"
+
+namespace gf2cu {
+
+__device__ __forceinline__ u64* tw4(u64* mat, u32 m, u32 row, u32 x) {
+    return mat + ((((size_t)(x >> 2) * m + row) << 2) + (x & 3u));
+}
+
+// row-major (stride Wp) -> 32-byte tiles (Wpad4 words per row)
+__global__ void tile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst, u32 m, u32 Wp,
+                             u32 Wpad4) {
+    const u32 per_row = Wpad4 >> 1;
+    const u64 total = (u64)m * per_row;
+    for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u32 row = (u32)(e / per_row), x = 2u * (u32)(e - (u64)row * per_row);
+        *reinterpret_cast<ulonglong2*>(tw4(dst, m, row, x)) =
+            *reinterpret_cast<const ulonglong2*>(src + (size_t)row * Wp + x);
+    }
+}
+
+// Back to row-major in position order; the pivot row at position i < rank of
+// super-step S = q_i / 128 takes its tiles from S's first swept tile
+// ((2S+2)/4) on from ubuf, when S swept.
+__global__ void untile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst,
+                               const u32* __restrict__ perm, u32 m, u32 Wp, u32 Wpad4,
+                               const u64* __restrict__ ubuf, u32 ucap, const u32* __restrict__ qcol,
+                               u32 rank, u32 W) {
+    const u32 per_row = Wpad4 >> 1;
+    const u64 total = (u64)m * per_row;
+    for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u32 row = (u32)(e / per_row), x = 2u * (u32)(e - (u64)row * per_row);
+        const u64* from = tw4(const_cast<u64*>(src), m, perm[row], x);
+        if (row < rank) {
+            const u32 w2 = 2u * (qcol[row] >> 7) + 2u;  // first word after the super-step
+            if (w2 < W && (x >> 2) >= (w2 >> 2)) from = tw4(const_cast<u64*>(ubuf), ucap, row, x);
+        }
+        *reinterpret_cast<ulonglong2*>(dst + (size_t)row * Wp + x) =
+            *reinterpret_cast<const ulonglong2*>(from);
+    }
+}
+
+// Initial state of the super-step driver: identity order, pb / pb2 = words
+// 0 / 1 of every row (read from the row-major input).
+__global__ void ple_init4_kernel(Params p, const u64* __restrict__ rowmajor, u32 Wp) {
+    const u32 stride = gridDim.x * blockDim.x;
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
+        p.perm[i] = i;
+        p.pb[i] = rowmajor[(size_t)i * Wp];
+        if (p.W > 1) p.pb2[i] = rowmajor[(size_t)i * Wp + 1];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.state->r = 0;
+        p.state->rb = 0;
+    }
+}
+
+// Panel-side outputs the workers need beyond the two PanelOuts.
+struct SuperOut {
+    u64 piv2[64];  // panel a's pivot rows: pre-super-step word w+1
+    u64 C[64];     // panel b's pivot rows: their panel-a combination
+};
+
+struct ApplyShared2 {
+    u64 Ea[64], Da[64], Eb[64], Db[64], piv2[64], C[64];
+    u32 qa[64], qb[64];
+};
+
+__device__ __forceinline__ void apply2_load(const Params& p, const PanelOut* pa, const PanelOut* pb,
+                                            const SuperOut* so, ApplyShared2& s, u32 rba, u32 rbb) {
+    for (u32 k = threadIdx.x; k < 64; k += blockDim.x) {
+        const bool va = k < rba, vb = k < rbb;
+        s.Ea[k] = va ? ldcg(&pa->E[k]) : 0ull;
+        s.Da[k] = va ? ldcg(&pa->D[k]) : 0ull;
+        s.qa[k] = va ? ldcg(&pa->qb[k]) : 0u;
+        s.piv2[k] = va ? ldcg(&so->piv2[k]) : 0ull;
+        s.Eb[k] = vb ? ldcg(&pb->E[k]) : 0ull;
+        s.Db[k] = vb ? ldcg(&pb->D[k]) : 0ull;
+        s.qb[k] = vb ? ldcg(&pb->qb[k]) : 0u;
+        s.C[k] = vb ? ldcg(&so->C[k]) : 0ull;
+    }
+}
+
+// Compressed write of one panel's multipliers c into columns [r0, r0 + rb)
+// (OR into the free zero bits of earlier words) and of the panel word wp
+// (overwritten: c's bits that land in it | the pivot row's E part).
+__device__ __forceinline__ void compress_write(u64* mat, u32 m, u32 ph, u32 r0, u32 wp, u64 c,
+                                               u64 epart) {
+    const u32 w0 = r0 >> 6, b0 = r0 & 63u;
+    const u64 clo = c << b0;
+    const u64 chi = b0 ? (c >> (64u - b0)) : 0ull;
+    if (w0 == wp) {
+        *tw4(mat, m, ph, wp) = clo | epart;
+    } else {
+        *tw4(mat, m, ph, w0) |= clo;
+        if (w0 + 1u == wp) {
+            *tw4(mat, m, ph, wp) = chi | epart;
+        } else {
+            if (chi) *tw4(mat, m, ph, w0 + 1u) |= chi;
+            *tw4(mat, m, ph, wp) = epart;
+        }
+    }
+}
+
+// Apply both panels of super-step (w, w+1) to the rows at positions
+// [lo, hi): multipliers, compressed words, and the sweep record
+// info[2 pos] = {d~_a, d_b}, info[2 pos + 1] = {physical row, 0}.
+__device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2& s, u32 w, u32 r,
+                                            u32 rba, u32 rbb, bool has_b, u32 lo, u32 hi, u32 tid,
+                                            u32 nthr) {
+    const u32 rb0 = r + rba;
+    for (u32 pos = lo + tid; pos < hi; pos += nthr) {
+        const u32 ph = ldcg(p.perm + pos);
+        u64 v = ldcg(p.pb + pos);
+        const u64 x1 = has_b ? ldcg(p.pb2 + pos) : 0ull;
+        // panel a (word w)
+        const u32 off = pos - r;
+        const u32 tla = off < rba ? off : rba;
+        u64 c = 0ull, da = 0ull, epa = 0ull;
+#pragma unroll 8
+        for (u32 k = 0; k < 64; ++k) {
+            if (k >= tla) break;
+            const u64 bit = (v >> s.qa[k]) & 1ull;
+            const u64 msk = 0ull - bit;
+            v ^= s.Ea[k] & msk;
+            da ^= s.Da[k] & msk;
+            c |= bit << k;
+        }
+        if (off < rba) {
+            c |= 1ull << off;
+            epa = v & ~low_mask64((int)s.qa[off] + 1);
+        }
+        compress_write(p.mat, p.m, ph, r, w, c, epa);
+        u64 db = 0ull, dta = da;
+        if (has_b) {
+            // word w+1 after panel a
+            u64 v1 = x1;
+#pragma unroll 8
+            for (u32 k = 0; k < 64; ++k) {
+                if (k >= rba) break;
+                v1 ^= s.piv2[k] & (0ull - ((da >> k) & 1ull));
+            }
+            if (pos < rb0) {
+                *tw4(p.mat, p.m, ph, w + 1u) = v1;  // a pivot row of panel a: its U word w+1
+            } else {
+                const u32 offb = pos - rb0;
+                const u32 tlb = offb < rbb ? offb : rbb;
+                u64 cb = 0ull, epb = 0ull;
+#pragma unroll 8
+                for (u32 k = 0; k < 64; ++k) {
+                    if (k >= tlb) break;
+                    const u64 bit = (v1 >> s.qb[k]) & 1ull;
+                    const u64 msk = 0ull - bit;
+                    v1 ^= s.Eb[k] & msk;
+                    db ^= s.Db[k] & msk;
+                    cb |= bit << k;
+                }
+                if (offb < rbb) {
+                    cb |= 1ull << offb;
+                    epb = v1 & ~low_mask64((int)s.qb[offb] + 1);
+                }
+                compress_write(p.mat, p.m, ph, rb0, w + 1u, cb, epb);
+#pragma unroll 8
+                for (u32 k = 0; k < 64; ++k) {
+                    if (k >= rbb) break;
+                    dta ^= s.C[k] & (0ull - ((db >> k) & 1ull));
+                }
+            }
+        }
+        p.info[2u * pos] = make_ulonglong2(dta, db);
+        p.info[2u * pos + 1u] = make_ulonglong2((u64)ph, 0ull);
+    }
+}
+
+// 16 tables x 256 entries x 32 B. Table t (t < 8: panel a, byte t of d~_a;
+// t >= 8: panel b, byte t-8 of d_b) lives in bank quarter t & 3:
+// entry e at ((t >> 2) * 256 + e) * 128 + (t & 3) * 32 + half * 16.
+__device__ __forceinline__ u32 tab16_off(u32 t, u32 e, u32 h) {
+    return (((t >> 2) * 256u + e) << 7) + ((t & 3u) << 5) + (h << 4);
+}
+
+// Gray walk (gray_code.hpp:105-112) of the 16 tables for one 32-byte tile
+// from the raw pivot rows of both panels (pa / pb = their physical rows;
+// words <= w+1 of the tile read as zero). Thread layout (512): h = tid & 1,
+// t & 3 = (tid >> 1) & 3, seg_lo = (tid >> 3) & 3, t >> 2 = (tid >> 5) & 3,
+// seg_hi = (tid >> 7) & 3; each thread walks 16 entries of one table half.
+__device__ __forceinline__ void build16(const Params& p, unsigned char* smem, u32 tile, u32 w,
+                                        const u32* pa, u32 rba, const u32* pb, u32 rbb) {
+    const u32 tid = threadIdx.x;
+    const u32 h = tid & 1u;
+    const u32 t = (((tid >> 5) & 3u) << 2) | ((tid >> 1) & 3u);
+    const u32 sg = (((tid >> 7) & 3u) << 2) | ((tid >> 3) & 3u);
+    const u32 x0 = tile * 4u;
+    const u32 zlim = w + 2u > x0 ? min(w + 2u - x0, 4u) : 0u;  // words <= w+1
+    const u32* src = t < 8u ? pa : pb;
+    const u32 nsrc = t < 8u ? rba : rbb;
+    const u32 base = 8u * (t & 7u);
+    ulonglong2 R[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        ulonglong2 v = make_ulonglong2(0ull, 0ull);
+        if (base + b < nsrc)
+            v = ldcg(reinterpret_cast<const ulonglong2*>(tw4(p.mat, p.m, src[base + b], x0) + 2u * h));
+        if (2u * h < zlim) v.x = 0ull;
+        if (2u * h + 1u < zlim) v.y = 0ull;
+        R[b] = v;
+    }
+    const u32 i0 = 16u * sg;
+    const u32 e0 = i0 ^ (i0 >> 1);
+    ulonglong2 acc = make_ulonglong2(0ull, 0ull);
+#pragma unroll
+    for (int b = 3; b < 8; ++b)
+        if ((e0 >> b) & 1u) xor2(acc, R[b]);
+    *reinterpret_cast<ulonglong2*>(smem + tab16_off(t, e0, h)) = acc;
+#pragma unroll
+    for (u32 k = 1; k < 16; ++k) {
+        const int b = (k & 1u) ? 0 : (k & 2u) ? 1 : (k & 4u) ? 2 : 3;  // ctz(k), folded
+        xor2(acc, R[b]);
+        const u32 i = i0 + k;
+        *reinterpret_cast<ulonglong2*>(smem + tab16_off(t, i ^ (i >> 1), h)) = acc;
+    }
+}
+
+constexpr u32 kRows16 = kTrailThreads / 2 * kUnroll;  // 1024 rows per iteration
+
+__device__ __forceinline__ void ld_info2(const ulonglong2* info, u32 pos, bool valid, ulonglong2& d,
+                                         u32& ph) {
+    if (valid) {
+        d = ldcg(info + 2u * pos);
+        ph = (u32)ldcg(info + 2u * pos + 1u).x;
+    } else {
+        d = make_ulonglong2(0ull, 0ull);
+        ph = 0u;
+    }
+}
+
+// Rows [row0, row0 + cnt) (offsets from r) of 32-byte tile `tile` with the 16
+// tables built. The tile holding words w+2, w+3 writes pb / pb2 (the next
+// super-step's panel words); rows with offset < npiv (both panels' pivot
+// rows) go to ubuf.
+__device__ __forceinline__ void trail16_rows(const Params& p, const unsigned char* smem, u32 w,
+                                             u32 r, u32 tile, u32 row0, u32 cnt, u32 npiv) {
+    const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const u32 rw = lane >> 1, h = lane & 1u, rq = rw & 3u;
+    const bool capture = (w + 2u < p.W) && ((w + 2u) >> 2) == tile;
+    const bool cap_lane = capture && (((w + 2u) & 3u) >> 1) == h;
+    const bool cap2 = cap_lane && (w + 3u < p.W);
+    const u32 lane_row = wid * 16u + rw;
+    u64* tbase = p.mat + (((size_t)tile * p.m) << 2) + 2u * h;
+    const u32 rend = row0 + cnt;
+    const u32 nit = (cnt + kRows16 - 1) / kRows16;
+    ulonglong2 dC[kUnroll], dN[kUnroll], valC[kUnroll];
+    u32 pC[kUnroll], pN[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+        const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 2);
+        ld_info2(p.info, r + ri, ri < rend, dC[k], pC[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+        const u32 ri = row0 + kRows16 + lane_row + (u32)k * (kTrailThreads / 2);
+        ld_info2(p.info, r + ri, ri < rend, dN[k], pN[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+        const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 2);
+        valC[k] = make_ulonglong2(0ull, 0ull);
+        if (ri < rend && ((dC[k].x | dC[k].y) != 0ull || capture || ri < npiv))
+            valC[k] = ldcg(reinterpret_cast<const ulonglong2*>(tbase + ((size_t)pC[k] << 2)));
+    }
+    for (u32 it = 0; it < nit; ++it) {
+        const u32 base = row0 + it * kRows16;
+        ulonglong2 valN[kUnroll], dNN[kUnroll];
+        u32 pNN[kUnroll];
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            const u32 ri = base + kRows16 + lane_row + (u32)k * (kTrailThreads / 2);
+            valN[k] = make_ulonglong2(0ull, 0ull);
+            if (ri < rend && ((dN[k].x | dN[k].y) != 0ull || capture || ri < npiv))
+                valN[k] = ldcg(reinterpret_cast<const ulonglong2*>(tbase + ((size_t)pN[k] << 2)));
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            const u32 ri = base + 2u * kRows16 + lane_row + (u32)k * (kTrailThreads / 2);
+            ld_info2(p.info, r + ri, ri < rend, dNN[k], pNN[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            const u32 ri = base + lane_row + (u32)k * (kTrailThreads / 2);
+            const ulonglong2 d = dC[k];
+            if ((d.x | d.y) != 0ull || (ri < npiv && ri < rend)) {
+#pragma unroll
+                for (u32 pp = 0; pp < 16; ++pp) {
+                    const u32 t = (pp + rq) & 15u;
+                    const u64 dw = t < 8u ? d.x : d.y;
+                    const u32 e = (u32)(dw >> (8u * (t & 7u))) & 0xffu;
+                    xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab16_off(t, e, h)));
+                }
+                if (ri < npiv)  // a pivot row of this super-step: its tail goes to ubuf
+                    *reinterpret_cast<ulonglong2*>(
+                        p.ubuf + ((((size_t)tile * p.ucap + r + ri) << 2) + 2u * h)) = valC[k];
+                else
+                    *reinterpret_cast<ulonglong2*>(tbase + ((size_t)pC[k] << 2)) = valC[k];
+            }
+            if (cap_lane && ri < rend) p.pb[r + ri] = valC[k].x;
+            if (cap2 && ri < rend) p.pb2[r + ri] = valC[k].y;
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+            dC[k] = dN[k];
+            pC[k] = pN[k];
+            dN[k] = dNN[k];
+            pN[k] = pNN[k];
+            valC[k] = valN[k];
+        }
+    }
+}
+
+__device__ __forceinline__ void stamp2(const Params& p, u32 w, u32 k) {
+    if (p.phase_ns && threadIdx.x == 0) p.phase_ns[(size_t)w * 8 + k] = globaltimer();
+}
+
+// One launch, grid = #SMs: CTA 0 runs the panels, CTAs 1.. the sweep. `nss` =
+// number of super-steps (ceil(W / 2)). panel_done counts published super-steps.
+__global__ void __launch_bounds__(kTrailThreads, 1)
+    ple_super_kernel(Params p, PanelOut* pout_b, SuperOut* so, u32 nss) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ PanelShared psh;
+    __shared__ ApplyShared2 ash;
+    __shared__ u32 s_ok;
+    __shared__ u32 s_pa[64], s_pb[64];
+    SyncState* sy = p.sync;
+    const u32 nworkers = gridDim.x - 1;
+
+    if (blockIdx.x == 0) {
+        // ------------------------------------------------------ panel CTA
+        LookAhead la{0u, false, p.ap_done, 0u, &sy->error};
+        la.piv2_out = so->piv2;
+        la.C_out = so->C;
+        Params pb_par = p;
+        pb_par.pout = pout_b;
+        u32 prev_r = 0u;
+        for (u32 S = 0; S < nss; ++S) {
+            const u32 w = 2u * S;
+            // nothing left: publish an empty super-step so the workers stop
+            const bool done0 = la.r >= p.m;
+            // panel a: its window and scans read the previous super-step's
+            // capture (all of its pre-work chunks)
+            la.cap_ctr = p.ap_done + (S > 0 ? S - 1 : 0);
+            la.cap_target = S > 0 ? pw_chunks(p.m - prev_r, p.pw_div) : 0u;
+            prev_r = la.r;
+            la.super_mode = 1;
+            la.have_window = false;
+            stamp2(p, w, 0);
+            const u32 rba = panel_factor_body(p, w, psh, blockDim.x, &la);
+            if (*(volatile u32*)&sy->error) return;
+            la.r += rba;
+            if (w + 1u < p.W) {
+                if (!done0 && la.r < p.m) {
+                    // panel b: window = word w+1 after panel a (panel a's
+                    // look-ahead); nothing to wait for
+                    la.super_mode = 2;
+                    la.have_window = true;
+                    la.cap_target = 0u;
+                    const u32 rbb = panel_factor_body(pb_par, w + 1u, psh, blockDim.x, &la);
+                    if (*(volatile u32*)&sy->error) return;
+                    la.r += rbb;
+                } else if (threadIdx.x == 0) {
+                    p.rhist[w + 1u] = la.r;
+                    p.rbhist[w + 1u] = 0u;
+                }
+            }
+            stamp2(p, w, 1);
+            cta_arrive(&sy->panel_done);
+            if (done0) return;
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- workers
+    const u32 wk = blockIdx.x - 1;
+    for (u32 S = 0; S < nss; ++S) {
+        if (!cta_wait(sy, &sy->panel_done, S + 1, s_ok)) return;
+        const u32 w = 2u * S;
+        const bool has_b = w + 1u < p.W;
+        const u32 r = *(volatile u32*)&p.rhist[w], rba = *(volatile u32*)&p.rbhist[w];
+        if (r >= p.m) return;
+        const u32 rbb = has_b ? *(volatile u32*)&p.rbhist[w + 1u] : 0u;
+        Params q = p;
+        q.info = p.info + (size_t)(S & 1u) * 2u * p.m;
+        const u32 nrows = p.m - r;
+        const bool sweep = w + 2u < p.W;
+        const u32 ct = (w + 2u) >> 2;  // look-ahead tile (words w+2, w+3)
+        const u32 crow = pw_rows(nrows, p.pw_div), nch = pw_chunks(nrows, p.pw_div);
+        for (u32 k = threadIdx.x; k < 64; k += blockDim.x) {
+            s_pa[k] = k < rba ? ldcg(p.perm + r + k) : 0u;
+            s_pb[k] = k < rbb ? ldcg(p.perm + r + rba + k) : 0u;
+        }
+        __syncthreads();
+        if (wk == 0) stamp2(p, w, 2);
+
+        // Pre-work chunks: the look-ahead tile was the previous super-step's
+        // (every row final there) unless the window just entered a new tile.
+        const bool early = S == 0 || ct == (w >> 2);
+        if (sweep && !early && !cta_wait(sy, &sy->t_count, nworkers * S, s_ok)) return;
+        u32 mine = 0;
+        bool loaded = false;
+        for (;;) {
+            if (threadIdx.x == 0) s_ok = atomicAdd(&p.ap_claim[S], 1u);
+            __syncthreads();
+            const u32 c = s_ok;
+            __syncthreads();
+            if (c >= nch) break;
+            if (!loaded) {  // the panel outputs stay S's while any chunk of S is open
+                apply2_load(p, p.pout, pout_b, so, ash, rba, rbb);
+                __syncthreads();
+                loaded = true;
+            }
+            const u32 a0 = r + c * crow, a1 = min(p.m, a0 + crow);
+            apply2_rows(q, ash, w, r, rba, rbb, has_b, a0, a1, threadIdx.x, blockDim.x);
+            if (sweep) {
+                __syncthreads();
+                if (rba + rbb > 0) {
+                    build16(q, smem, ct, w, s_pa, rba, s_pb, rbb);
+                    __syncthreads();
+                }
+                trail16_rows(q, smem, w, r, ct, a0 - r, a1 - a0, rba + rbb);
+            }
+            ++mine;
+        }
+        if (mine) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                red_release_add(&p.ap_done[S], mine);
+            }
+        }
+        // the rest: after super-step S-1 everywhere (pivot rows' raw tails)
+        // and all of S's pre-work (every row's info / compressed words)
+        if (threadIdx.x == 0)
+            s_ok = spin_geq2(&sy->t_count, nworkers * S, &p.ap_done[S], nch, &sy->error) ? 1u : 0u;
+        __syncthreads();
+        if (!s_ok) return;
+        if (wk == 0) stamp2(p, w, 3);
+        if (sweep) {
+            const u32 nt = (p.Wpad8 >> 2) - ct - 1;  // Wpad8 holds Wpad4 here
+            const u64 total = (u64)nt * nrows;
+            u64 u = total * wk / nworkers;
+            const u64 end = total * (wk + 1) / nworkers;
+            while (u < end) {
+                const u32 tile = ct + 1 + (u32)(u / nrows);
+                const u32 row0 = (u32)(u % nrows);
+                const u32 cnt = (u32)min((u64)(nrows - row0), end - u);
+                if (rba + rbb > 0) {
+                    __syncthreads();
+                    build16(q, smem, tile, w, s_pa, rba, s_pb, rbb);
+                    __syncthreads();
+                }
+                trail16_rows(q, smem, w, r, tile, row0, cnt, rba + rbb);
+                u += cnt;
+            }
+        }
+        cta_arrive(&sy->t_count);
+        if (wk == 0) stamp2(p, w, 5);
+    }
+}
+
+}  // namespace gf2cu

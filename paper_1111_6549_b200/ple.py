@@ -49,6 +49,8 @@ class PleConfig:
     stream: Optional[int] = None   # cudaStream_t as an int (e.g. torch stream.cuda_stream)
     time_kernels: bool = False
     multi_kernel: bool = False     # one launch per phase (cross-check driver)
+    single_panel: bool = False     # force the persistent driver with one panel per sweep
+    super_step: bool = False       # force the super-step driver (two panels per sweep)
 
     def to_c(self) -> gf2cu_cfg:
         c = gf2cu_cfg()
@@ -59,7 +61,9 @@ class PleConfig:
         c.device = int(self.device)
         c.stream = C.c_void_p(self.stream) if self.stream else None
         c.flags = (_lib.FLAG_TIME_KERNELS if self.time_kernels else 0) | \
-            (_lib.FLAG_MULTI_KERNEL if self.multi_kernel else 0)
+            (_lib.FLAG_MULTI_KERNEL if self.multi_kernel else 0) | \
+            (_lib.FLAG_SINGLE_PANEL if self.single_panel else 0) | \
+            (_lib.FLAG_SUPER_STEP if self.super_step else 0)
         return c
 
 

@@ -23,12 +23,14 @@ def load(name):
         return json.load(f)
 
 
-def test_suite_golden_gpu():
+@pytest.mark.parametrize("driver", ["single", "super"])
+def test_suite_golden_gpu(driver):
     bad = []
+    cfg = G.PleConfig(super_step=True) if driver == "super" else G.PleConfig(single_panel=True)
     for e in load("suite.json")["cases"]:
         m, n = e["m"], e["n"]
         a = G.BitMatrix(m, n, S.build(m, n, e["kind"], e["seed"]))
-        out = G.block_iterative_ple(a)
+        out = G.block_iterative_ple(a, cfg)
         h = S.outcome_hash(a.words, n, out.rank, out.p.swaps, out.q)
         if out.rank != e["rank"] or h != e["sha256"]:
             bad.append((m, n, e["kind"], e["seed"]))

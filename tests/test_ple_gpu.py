@@ -11,11 +11,11 @@ import paper_1111_6549_b200 as G
 pytestmark = pytest.mark.gpu
 
 
-def run_both(a_words, m, n):
+def run_both(a_words, m, n, cfg=None):
     ref = a_words.copy()
     want = O.ple(ref, m, n)
     bm = G.BitMatrix(m, n, a_words.copy())
-    got = G.block_iterative_ple(bm)
+    got = G.block_iterative_ple(bm, cfg)
     return ref, want, bm, got
 
 
@@ -30,11 +30,15 @@ def assert_same(ref, want, bm, got, what=""):
         raise AssertionError(f"{what}: {len(bad)} words differ, first at {bad[:5].tolist()}")
 
 
-@pytest.mark.parametrize("m,n", [(1, 1), (1, 64), (64, 1), (2, 3), (31, 33), (63, 64), (64, 64),
-                                 (65, 65), (127, 129), (128, 128), (129, 127), (150, 300),
-                                 (300, 150), (257, 193), (200, 1000), (1000, 200)])
+SMALL = [(1, 1), (1, 64), (64, 1), (2, 3), (31, 33), (63, 64), (64, 64), (65, 65), (127, 129),
+         (128, 128), (129, 127), (150, 300), (300, 150), (257, 193), (200, 1000), (1000, 200),
+         (130, 190), (190, 130), (70, 257)]
+
+
+@pytest.mark.parametrize("super_step", [False, True])
+@pytest.mark.parametrize("m,n", SMALL)
 @pytest.mark.parametrize("kind", ["dense", "thin", "ctr", "deficient"])
-def test_small_shapes(m, n, kind):
+def test_small_shapes(m, n, kind, super_step):
     seed = m * 1000 + n
     if kind == "dense":
         a = O.fill_random(m, n, 0.5, seed)
@@ -48,15 +52,18 @@ def test_small_shapes(m, n, kind):
         for _ in range(4):
             d, s = rng.integers(0, m, 2)
             a[d] = a[s]
-    assert_same(*run_both(a, m, n), what=f"{kind} {m}x{n}")
+    cfg = G.PleConfig(super_step=True) if super_step else None
+    assert_same(*run_both(a, m, n, cfg), what=f"{kind} {m}x{n} super={super_step}")
 
 
 @pytest.mark.parametrize("m,n,density", [(1024, 1024, 0.5), (2048, 2048, 0.5), (1500, 2500, 0.5),
                                          (2048, 2048, 1 / 64), (2048, 2048, 1 / 256),
                                          (4096, 4096, 0.5)])
-def test_medium(m, n, density):
+@pytest.mark.parametrize("super_step", [False, True])
+def test_medium(m, n, density, super_step):
     a = O.fill_random(m, n, density, 7)
-    assert_same(*run_both(a, m, n), what=f"{m}x{n} p={density}")
+    cfg = G.PleConfig(super_step=True) if super_step else G.PleConfig(single_panel=True)
+    assert_same(*run_both(a, m, n, cfg), what=f"{m}x{n} p={density} super={super_step}")
 
 
 def test_zero_and_identity():
@@ -100,11 +107,16 @@ def test_smoke_entry():
     __graft_entry__.smoke()
 
 
-@pytest.mark.parametrize("multi", [False, True])
+DRIVERS = {"super": (G.PleConfig(super_step=True), 2), "single": (G.PleConfig(single_panel=True), 1),
+           "multi": (G.PleConfig(multi_kernel=True), 0)}
+
+
+@pytest.mark.parametrize("driver", sorted(DRIVERS))
 @pytest.mark.parametrize("m,n,gen", [(3000, 3000, "dense"), (2048, 2048, "p256"), (1500, 4000, "ctr"),
                                      (4000, 1500, "ctr"), (2500, 2500, "dup")])
-def test_drivers_agree(m, n, gen, multi):
-    """Both drivers (persistent cooperative / one launch per phase) are bit-exact."""
+def test_drivers_agree(m, n, gen, driver):
+    """All drivers (super-step: two panels per sweep / persistent single-panel
+    / one launch per phase) are bit-exact."""
     if gen == "dense":
         a = O.fill_random(m, n, 0.5, 5)
     elif gen == "p256":
@@ -117,6 +129,7 @@ def test_drivers_agree(m, n, gen, multi):
     ref = a.copy()
     want = O.ple(ref, m, n)
     bm = G.BitMatrix(m, n, a.copy())
-    got = G.block_iterative_ple(bm, G.PleConfig(multi_kernel=multi))
-    assert got.stats["driver"] == (0 if multi else 1)
-    assert_same(ref, want, bm, got, what=f"{gen} {m}x{n} multi={multi}")
+    cfg, code = DRIVERS[driver]
+    got = G.block_iterative_ple(bm, cfg)
+    assert got.stats["driver"] == code
+    assert_same(ref, want, bm, got, what=f"{gen} {m}x{n} driver={driver}")
