@@ -70,10 +70,11 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic():
-    """DRAM bytes per algorithmic byte of the dominant kernel (the persistent
-    PLE kernel) from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "persistent_traffic.json")
+def load_traffic(driver: int = 2):
+    """DRAM bytes per algorithmic (sweep) byte of the dominant kernel from its
+    committed ncu --set full capture (super-step or single-panel driver)."""
+    name = "super_traffic.json" if driver == 2 else "persistent_traffic.json"
+    p = os.path.join(ROOT, "profiles", name)
     try:
         with open(p) as f:
             d = json.load(f)
@@ -256,6 +257,8 @@ def gpu_arm(args, rank, world, local_rank):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     tot_bytes = 0.0
+    sweep_bytes = 0.0   # bytes the trailing sweeps move (K = 128 for the super-step driver)
+    driver = 1
     trail_ms = 0.0      # device-timestamped trailing-update phases (inside the kernel)
     kern_ms = 0.0       # CUDA-event duration of the persistent PLE kernel
     launches = 0        # persistent-kernel launches (one per PLE)
@@ -266,6 +269,8 @@ def gpu_arm(args, rank, world, local_rank):
         out = G.block_iterative_ple(work, cfg_t)
         st = out.stats
         tot_bytes += st["alg_bytes"]
+        sweep_bytes += st["sweep_bytes"]
+        driver = int(st["driver"])
         trail_ms += st["trailing_ms"]
         kern_ms += st["kernel_ms"]
         panel_ms += st["panel_ms"]
@@ -322,16 +327,26 @@ def gpu_arm(args, rank, world, local_rank):
     value = sum_bytes / (max_ms * 1e-3) / 1e9
     e2e_value = e2e_sum_bytes / e2e_max_s / 1e9
     peak, peak_kind = load_peaks()
-    per_launch_bytes = tot_bytes / max(1, launches)
+    per_launch_k64 = tot_bytes / max(1, launches)
+    per_launch_bytes = sweep_bytes / max(1, launches)
     per_launch_ms = kern_ms / max(1, launches)
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else None
-    traffic_ratio = load_traffic()
+    traffic_ratio = load_traffic(driver)
+    super_step = driver == 2
     roofline = {
-        "kernel": "ple_persistent_kernel", "bound": "hbm",
+        "kernel": "ple_super_kernel" if super_step else "ple_persistent_kernel", "bound": "hbm",
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": (round(per_launch_bytes * traffic_ratio) if traffic_ratio else None),
-        "alg_bytes_per_launch": round(per_launch_bytes), "avg_launch_ms": round(per_launch_ms, 4),
+        # algorithmic bytes = one read + one write of every trailing tail word per
+        # sweep; a sweep covers 128 columns with the super-step
+        # driver, so its bytes are half the 64-column figure
+        "alg_bytes_per_launch": round(per_launch_bytes), "panel_columns_per_sweep": 128 if super_step else 64,
+        "alg_bytes_per_launch_k64": round(per_launch_k64),
+        "effective_k64_GBps": round(per_launch_k64 / (per_launch_ms * 1e-3) / 1e9, 1) if per_launch_ms else None,
+        "limiter": ("L1TEX data pipe: Gray-table lookups (16 B of shared memory per byte of row "
+                    "per panel) + the global load/store; see profiles/README.md"),
+        "avg_launch_ms": round(per_launch_ms, 4),
         "peak_source": (f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                         else "fallback 6.65 TB/s"),
         "share_of_step": round(kern_ms / max(1e-9, dev_ms), 4),
@@ -363,7 +378,8 @@ def gpu_arm(args, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"block_iterative_ple {m}x{n} (BASELINE config 5, 1 GPU)",
                    "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "rank": int(out.rank),
-                   "panel_bits": 64, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "panel_bits": 64, "panels_per_sweep": 2 if driver == 2 else 1,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "l2": "input 512 MiB > 126 MB L2; pristine copy restored each step (counted)",
                    "checksum": hex(checksum) if checksum is not None else None},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT,

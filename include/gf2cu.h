@@ -85,6 +85,10 @@ typedef struct {
     double kernel_ms;           /* persistent kernel duration (CUDA events)     */
     int driver;                 /* 2 = super-step (two panels per sweep),
                                    1 = persistent single-panel, 0 = per phase   */
+    double sweep_bytes;         /* bytes the trailing sweeps move: alg_bytes for
+                                   one panel per sweep; for the super-step driver
+                                   sum over super-steps of 16*(m-r-rba-rbb)*(W-w-2)
+                                   (one read + write per two panels)            */
 } gf2cu_stats;
 
 /* Fills *cfg with the reference defaults (k=0, k_scale=0.75, table_count=4,

@@ -444,6 +444,18 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             bytes += 16.0 * double(m - r0 - rb) * double(W - w - 1);
         }
         stats->alg_bytes = bytes;
+        double sweep = bytes;
+        if (super) {
+            sweep = 0.0;
+            for (size_t w = 0; w + 2 < W && w < steps; w += 2) {
+                const size_t r0 = rh[w];
+                const size_t rbb = (w + 1 < steps) ? rbh[w + 1] : 0;
+                if (r0 >= m) continue;
+                const size_t done = std::min(m, r0 + rbh[w] + rbb);
+                sweep += 16.0 * double(m - done) * double(W - w - 2);
+            }
+        }
+        stats->sweep_bytes = sweep;
         stats->trailing_launches = launches;
         stats->kernel_ms = kernel_ms;
         stats->driver = multi ? 0 : super ? 2 : 1;

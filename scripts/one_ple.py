@@ -7,4 +7,5 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 dm = G.DeviceMatrix(n, n)
 dm.fill_ctr(1)
 out = G.block_iterative_ple(dm)
-print("rank", out.rank)
+print("rank", out.rank, "driver", out.stats["driver"], "alg_bytes(k64)", out.stats["alg_bytes"],
+      "sweep_bytes", out.stats["sweep_bytes"])
