@@ -78,7 +78,7 @@ def load_traffic(driver: int = 2):
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_alg_byte")
+        return d.get("dram_bytes_per_k64_alg_byte", d.get("dram_bytes_per_alg_byte"))
     except Exception:
         return None
 
@@ -327,8 +327,12 @@ def gpu_arm(args, rank, world, local_rank):
     value = sum_bytes / (max_ms * 1e-3) / 1e9
     e2e_value = e2e_sum_bytes / e2e_max_s / 1e9
     peak, peak_kind = load_peaks()
-    per_launch_k64 = tot_bytes / max(1, launches)
-    per_launch_bytes = sweep_bytes / max(1, launches)
+    # algorithmic bytes = SURVEY.md 8(d)'s per-unit figure (one read + one write
+    # of every trailing tail word per 64-column panel step) x the steps of one
+    # launch. The super-step driver sweeps two panels per pass, so the bytes it
+    # actually moves (sweep_bytes, and the ncu DRAM traffic) are about half.
+    per_launch_bytes = tot_bytes / max(1, launches)
+    per_launch_sweep = sweep_bytes / max(1, launches)
     per_launch_ms = kern_ms / max(1, launches)
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else None
     traffic_ratio = load_traffic(driver)
@@ -338,12 +342,10 @@ def gpu_arm(args, rank, world, local_rank):
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": (round(per_launch_bytes * traffic_ratio) if traffic_ratio else None),
-        # algorithmic bytes = one read + one write of every trailing tail word per
-        # sweep; a sweep covers 128 columns with the super-step
-        # driver, so its bytes are half the 64-column figure
-        "alg_bytes_per_launch": round(per_launch_bytes), "panel_columns_per_sweep": 128 if super_step else 64,
-        "alg_bytes_per_launch_k64": round(per_launch_k64),
-        "effective_k64_GBps": round(per_launch_k64 / (per_launch_ms * 1e-3) / 1e9, 1) if per_launch_ms else None,
+        "alg_bytes_per_launch": round(per_launch_bytes),
+        "panel_columns_per_sweep": 128 if super_step else 64,
+        "sweep_bytes_per_launch": round(per_launch_sweep),
+        "sweep_GBps": round(per_launch_sweep / (per_launch_ms * 1e-3) / 1e9, 1) if per_launch_ms else None,
         "limiter": ("L1TEX data pipe: Gray-table lookups (16 B of shared memory per byte of row "
                     "per panel) + the global load/store; see profiles/README.md"),
         "avg_launch_ms": round(per_launch_ms, 4),
