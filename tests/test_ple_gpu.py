@@ -7,6 +7,7 @@ import pytest
 
 import oracle as O
 import paper_1111_6549_b200 as G
+import suite as S
 
 pytestmark = pytest.mark.gpu
 
@@ -133,3 +134,61 @@ def test_drivers_agree(m, n, gen, driver):
     got = G.block_iterative_ple(bm, cfg)
     assert got.stats["driver"] == code
     assert_same(ref, want, bm, got, what=f"{gen} {m}x{n} driver={driver}")
+
+
+def ctr_rows(rows, n, seed):
+    """Rows of the counter generator, random access."""
+    W = (n + 63) // 64
+    i = np.asarray(rows, dtype=np.uint64)[:, None]
+    x0 = np.arange(W, dtype=np.uint64)[None, :]
+    with np.errstate(over="ignore"):
+        x = (np.uint64(seed) << np.uint64(32)) + (i * np.uint64(W) + x0 + np.uint64(1)) * np.uint64(
+            0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    if n % 64:
+        x[:, -1] &= np.uint64((1 << (n % 64)) - 1)
+    return x
+
+
+@pytest.mark.slow
+def test_131072_reconstruction_sample():
+    """BASELINE config 5's large case (131072^2, 2 GiB) on one GPU: the
+    reference would take ~36 CPU-minutes, so the check is size-independent:
+    sampled rows of P * L * E (ple_reconstruct, ple.hpp:355-358, with E in
+    closed form) equal the input rows."""
+    n = 131072
+    dm = G.DeviceMatrix(n, n)
+    dm.fill_ctr(1)
+    out = G.block_iterative_ple(dm)
+    assert out.stats["driver"] == 2
+    r = out.rank
+    assert r > n - 64
+    words = dm.download()
+    W = words.shape[1]
+    q = np.asarray(out.q, dtype=np.int64)
+    # position i holds input row idx[i] (the swaps applied in order)
+    idx = np.arange(n)
+    for i, s in enumerate(np.asarray(out.p.swaps, dtype=np.int64)):
+        idx[i], idx[s] = idx[s], idx[i]
+    cols = np.arange(W)
+    for i in [0, 1, 63, 64, 12345, 65537, 131000, r - 1, min(r, n - 1), n - 1]:
+        lim = min(i, r)
+        lbits = S.unpack(words[i:i + 1], lim)[0] if lim else np.zeros(0, np.uint8)
+        sel = list(np.nonzero(lbits)[0])
+        if i < r:
+            sel.append(i)
+        sel = np.asarray(sel, dtype=np.int64)
+        if sel.size == 0:
+            prod = np.zeros(W, dtype=np.uint64)
+        else:
+            T = words[sel].copy()
+            qs = q[sel]
+            T[cols[None, :] < (qs >> 6)[:, None]] = 0
+            lo = (qs & 63) + 1
+            keep = np.where(lo >= 64, np.uint64(0), ~((np.uint64(1) << lo.astype(np.uint64)) - np.uint64(1)))
+            T[np.arange(sel.size), qs >> 6] &= keep
+            T[np.arange(sel.size), qs >> 6] |= np.uint64(1) << (qs & 63).astype(np.uint64)
+            prod = np.bitwise_xor.reduce(T, axis=0)
+        assert np.array_equal(prod, ctr_rows([idx[i]], n, 1)[0]), f"position {i}"
