@@ -229,6 +229,26 @@ gf2cu_status gf2cu_shard_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, in
 /* Apply step w to the local rows; packs this rank's pivot tails into pack. */
 gf2cu_status gf2cu_shard_apply(gf2cu_shard* s, size_t w, uint64_t* pack, void* stream);
 /* Stage owner rank's packed pivot tails (bitmask mask) for step w. */
+/* Asynchronous step protocol (no host decision per step; used by
+ * paper_1111_6549_b200/shard.py):
+ *   gather(0, m) into a zeroed buffer -> sum all-reduce -> panel(window_only
+ *   = 0, status_out = NULL: nothing is read back) -> pack_stage (this rank's
+ *   pivot tails straight into the stage layout, the rest zeroed) -> sum
+ *   all-reduce of the stage (disjoint contributions) -> apply(pack = NULL)
+ *   -> trailing.
+ * set_stage makes the library use the caller's stage buffer (64 rows x
+ * Wpad8 words, tile-major) so the collective can run on it in place; pivots
+ * returns the pivots found so far (synchronous, for a lagged stop check). */
+gf2cu_status gf2cu_shard_pack_stage(gf2cu_shard* s, size_t w, void* stream);
+/* The same protocol in three calls per step: step_gather (zero + gather the
+ * active column), step_panel (panel + pack_stage), step_update (apply +
+ * trailing); the caller all-reduces the column after step_gather and the
+ * stage after step_panel. */
+gf2cu_status gf2cu_shard_step_gather(gf2cu_shard* s, size_t w, uint64_t* pos_words, void* stream);
+gf2cu_status gf2cu_shard_step_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, void* stream);
+gf2cu_status gf2cu_shard_step_update(gf2cu_shard* s, size_t w, void* stream);
+gf2cu_status gf2cu_shard_set_stage(gf2cu_shard* s, uint64_t* stage);
+gf2cu_status gf2cu_shard_pivots(gf2cu_shard* s, size_t* pivots, void* stream);
 gf2cu_status gf2cu_shard_unpack(gf2cu_shard* s, size_t w, uint64_t mask, const uint64_t* pack,
                                 void* stream);
 /* Trailing update of step w on the local rows. */

@@ -125,6 +125,12 @@ SYMBOLS = {
     "gf2cu_shard_gather": (C.c_int, [_mp, _u64p, _sz, _sz, C.c_void_p]),
     "gf2cu_shard_panel": (C.c_int, [_mp, _sz, _u64p, C.c_int, C.POINTER(C.c_uint32), C.c_void_p]),
     "gf2cu_shard_apply": (C.c_int, [_mp, _sz, _u64p, C.c_void_p]),
+    "gf2cu_shard_pack_stage": (C.c_int, [_mp, _sz, C.c_void_p]),
+    "gf2cu_shard_step_gather": (C.c_int, [_mp, _sz, _u64p, C.c_void_p]),
+    "gf2cu_shard_step_panel": (C.c_int, [_mp, _sz, _u64p, C.c_void_p]),
+    "gf2cu_shard_step_update": (C.c_int, [_mp, _sz, C.c_void_p]),
+    "gf2cu_shard_set_stage": (C.c_int, [_mp, _u64p]),
+    "gf2cu_shard_pivots": (C.c_int, [_mp, _szp, C.c_void_p]),
     "gf2cu_shard_unpack": (C.c_int, [_mp, _sz, C.c_uint64, _u64p, C.c_void_p]),
     "gf2cu_shard_trailing": (C.c_int, [_mp, _sz, C.c_void_p]),
     "gf2cu_shard_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),

@@ -1159,6 +1159,7 @@ struct gf2cu_shard {
     unsigned char* retired = nullptr;
     gf2cu::StepState* lstate = nullptr;
     u64* stage = nullptr;
+    bool stage_owned = true;  // false once the caller supplied its own (set_stage)
     // replicated
     u32* perm = nullptr;
     u32* inv = nullptr;
@@ -1271,8 +1272,9 @@ gf2cu_status gf2cu_shard_create(size_t m, size_t n, int rank, int nranks, size_t
 gf2cu_status gf2cu_shard_destroy(gf2cu_shard* s) {
     if (!s) return GF2CU_OK;
     DeviceGuard g(s->device);
+    if (s->stage_owned) cudaFree(s->stage);
     for (void* p : {(void*)s->data, (void*)s->mat, (void*)s->pbl, (void*)s->info, (void*)s->retired,
-                    (void*)s->lstate, (void*)s->stage, (void*)s->perm, (void*)s->inv,
+                    (void*)s->lstate, (void*)s->perm, (void*)s->inv,
                     (void*)s->gstate, (void*)s->pout, (void*)s->swaps, (void*)s->qcol,
                     (void*)s->rhist, (void*)s->rbhist, (void*)s->status})
         cudaFree(p);
@@ -1355,7 +1357,7 @@ gf2cu_status gf2cu_shard_gather(gf2cu_shard* s, uint64_t* pos_words, size_t lo, 
 
 gf2cu_status gf2cu_shard_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, int window_only,
                                uint32_t* status_out, void* stream) {
-    if (!s || !pos_words || !status_out || w >= s->W) return fail(GF2CU_EINVAL, "bad panel call");
+    if (!s || !pos_words || w >= s->W) return fail(GF2CU_EINVAL, "bad panel call");
     DeviceGuard g(s->device);
     cudaStream_t st = shard_stream(s, stream);
     gf2cu::Params p{};
@@ -1378,25 +1380,82 @@ gf2cu_status gf2cu_shard_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, in
     p.Wpad8 = (u32)s->Wpad8;
     gf2cu::panel_factor_kernel<<<1, gf2cu::kPanelThreads, 0, st>>>(p, (u32)w);
     CU_TRY(cudaGetLastError());
-    CU_TRY(cudaMemcpyAsync(status_out, s->status, (8 + 2 * (size_t)s->nranks) * 4,
-                           cudaMemcpyDeviceToHost, st));
-    CU_TRY(cudaStreamSynchronize(st));
+    if (status_out) {  // (asynchronous when the caller does not read the status)
+        CU_TRY(cudaMemcpyAsync(status_out, s->status, (8 + 2 * (size_t)s->nranks) * 4,
+                               cudaMemcpyDeviceToHost, st));
+        CU_TRY(cudaStreamSynchronize(st));
+    }
     return GF2CU_OK;
 }
 
 gf2cu_status gf2cu_shard_apply(gf2cu_shard* s, size_t w, uint64_t* pack, void* stream) {
-    if (!s || !pack || w >= s->W) return fail(GF2CU_EINVAL, "bad apply call");
+    if (!s || w >= s->W) return fail(GF2CU_EINVAL, "bad apply call");
     DeviceGuard g(s->device);
     cudaStream_t st = shard_stream(s, stream);
     CU_TRY(cudaMemsetAsync(&s->lstate->r, 0xff, 4, st));
     if (s->m_loc) {
         gf2cu::ShardParams p = shard_params(s);
         p.pack = reinterpret_cast<u64*>(pack);
-        if (w + 1 < s->W)
+        if (pack && w + 1 < s->W)
             gf2cu::shard_pack_kernel<<<num_sms(s->device) * 4, 256, 0, st>>>(p, (u32)w);
         gf2cu::shard_apply_kernel<<<num_sms(s->device) * 4, gf2cu::kApplyThreads, 0, st>>>(p, (u32)w);
     }
     CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_pack_stage(gf2cu_shard* s, size_t w, void* stream) {
+    if (!s || w >= s->W) return fail(GF2CU_EINVAL, "bad pack_stage call");
+    if (w + 1 >= s->W) return GF2CU_OK;
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    const size_t x0 = (w + 1) & ~size_t(7);
+    const size_t lo = (x0 >> 3) * 64 * 8, hi = (s->Wpad8 >> 3) * 64 * 8;
+    CU_TRY(cudaMemsetAsync(s->stage + lo, 0, (hi - lo) * 8, st));
+    if (s->m_loc)
+        gf2cu::shard_pack_stage_kernel<<<num_sms(s->device) * 4, 256, 0, st>>>(shard_params(s), s->stage,
+                                                                             (u32)w);
+    CU_TRY(cudaGetLastError());
+    return GF2CU_OK;
+}
+
+// The asynchronous protocol's three calls per step (shard.py::_run_steps).
+gf2cu_status gf2cu_shard_step_gather(gf2cu_shard* s, size_t w, uint64_t* pos_words, void* stream) {
+    (void)w;
+    return gf2cu_shard_gather(s, pos_words, 0, s ? s->m : 0, stream);
+}
+
+gf2cu_status gf2cu_shard_step_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, void* stream) {
+    gf2cu_status st = gf2cu_shard_panel(s, w, pos_words, 0, nullptr, stream);
+    if (st == GF2CU_OK) st = gf2cu_shard_pack_stage(s, w, stream);
+    return st;
+}
+
+gf2cu_status gf2cu_shard_step_update(gf2cu_shard* s, size_t w, void* stream) {
+    gf2cu_status st = gf2cu_shard_apply(s, w, nullptr, stream);
+    if (st == GF2CU_OK) st = gf2cu_shard_trailing(s, w, stream);
+    return st;
+}
+
+gf2cu_status gf2cu_shard_set_stage(gf2cu_shard* s, uint64_t* stage) {
+    if (!s || !stage) return fail(GF2CU_EINVAL, "null stage");
+    DeviceGuard g(s->device);
+    if (s->stage_owned) {
+        cudaFree(s->stage);
+        s->stage_owned = false;
+    }
+    s->stage = reinterpret_cast<u64*>(stage);
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_shard_pivots(gf2cu_shard* s, size_t* pivots, void* stream) {
+    if (!s || !pivots) return fail(GF2CU_EINVAL, "null argument");
+    DeviceGuard g(s->device);
+    cudaStream_t st = shard_stream(s, stream);
+    gf2cu::StepState h{};
+    CU_TRY(cudaMemcpyAsync(&h, s->gstate, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    *pivots = (size_t)h.r + h.rb;
     return GF2CU_OK;
 }
 

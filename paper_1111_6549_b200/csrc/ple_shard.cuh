@@ -149,6 +149,26 @@ __global__ void shard_pack_kernel(ShardParams s, u32 w) {
     }
 }
 
+// This rank's pivot rows' raw tails (words [x0, Wpad8), x0 = (w+1) & ~7)
+// straight into the tile-major stage layout at their pivot slots t. The
+// caller zeroed that region; a sum all-reduce over the ranks' stages then
+// yields every pivot tail on every rank (the contributions are disjoint), so
+// no owner-dependent broadcast (and no host decision) is needed per step.
+__global__ void shard_pack_stage_kernel(ShardParams s, u64* stage, u32 w) {
+    const u32 r = s.gstate->r, rb = s.gstate->rb;
+    const u32 x0 = (w + 1) & ~7u;
+    const u32 tailw = s.Wpad8 > x0 ? s.Wpad8 - x0 : 0u;
+    const u64 total = (u64)rb * tailw;
+    for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u32 t = (u32)(e / tailw), x = x0 + (u32)(e - (u64)t * tailw);
+        const u32 g = s.perm[r + t];
+        if (shard_owner(g, s.nranks, s.block) != s.rank) continue;
+        stage[(((size_t)(x >> 3) * 64 + t) << 3) + (x & 7u)] =
+            *tword(s.mat, s.m_loc, shard_local(g, s.nranks, s.block), x);
+    }
+}
+
 // The ctr generator for this rank's rows (row-major local
 // buffer, stride Wp): the words of global row g, bit-identical to fill_ctr.
 __global__ void shard_fill_ctr_kernel(u64* data, u32 m_loc, u32 n, u32 Wp, u32 rank, u32 nranks,

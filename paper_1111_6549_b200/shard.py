@@ -7,14 +7,18 @@ positions (the reference's row order after its swaps) are a replicated
 permutation that every rank updates identically by running the same panel
 factorization. Per 64-column panel step w:
 
-1. all-reduce (sum) the panel words of the 128-row window (1 KiB);
-2. every rank factors the panel (window-only); on a window miss all ranks
-   all-reduce the whole active panel column and run the step again;
-3. every rank applies the step to its own rows (multipliers, compression,
-   the d combinations) and packs the raw tails of the pivot rows it owns;
-4. each owning rank broadcasts its packed pivot tails; every rank stages
-   them (the Gray-table sources);
-5. every rank runs the trailing update on its own rows (no communication).
+1. sum all-reduce of the active panel column (every rank contributes its
+   own rows' panel words at their positions, 8 bytes per row);
+2. every rank factors the panel from it (identical decisions everywhere);
+3. every rank packs the raw tails of the pivot rows it owns straight into
+   the tile-major stage (zeros elsewhere); sum all-reduce of the stage (the
+   contributions are disjoint) -> the Gray-table sources on every rank;
+4. every rank applies the step to its own rows (multipliers, compression,
+   the d combinations) and runs the trailing update on them.
+
+No step needs a host decision (no status read-back, no owner-dependent
+broadcasts), so the host enqueues the whole loop asynchronously; it only
+stops early from a lagged "all rows hold pivots" check.
 
 The collectives use torch.distributed (NCCL on CUDA tensors, gloo on CPU
 tensors), so the orchestration is also exercised by world_size-2/4 gloo tests
@@ -105,35 +109,34 @@ def run_sharded(engine, dist, group=None) -> ShardResult:
         return _run_steps(engine, dist, group)
 
 
-def _run_steps(engine, dist, group) -> ShardResult:
-    m, W, nranks = engine.m, engine.W, engine.nranks
+def _run_steps(engine, dist, group, check_every: int = 16) -> ShardResult:
+    """Per 64-column panel step, with no host decision inside the step (so
+    the whole loop is enqueued asynchronously on the device stream):
+
+    1. every rank writes its active rows' panel words at their positions into
+       a zeroed column; sum all-reduce -> the whole active column everywhere;
+    2. every rank factors the panel from it (full scans on window misses, so
+       the step never aborts; identical decisions on every rank);
+    3. every rank packs the raw tails of the pivot rows it owns straight into
+       the stage layout (zeros elsewhere); sum all-reduce -> all pivot tails
+       everywhere (the contributions are disjoint);
+    4. every rank applies the step to its rows and sweeps them.
+
+    The host only stops early (all rows hold pivots) from a lagged check
+    every `check_every` steps."""
+    m, W = engine.m, engine.W
+    solo = engine.nranks == 1  # the collectives are identities
     engine.begin()
-    r, rb = 0, 0
     for w in range(W):
-        r += rb
-        rb = 0
-        if r >= m:
+        if w and w % check_every == 0 and engine.pivots() >= m:
             break
-        hi = min(m, r + WINDOW)
-        dist.all_reduce(engine.gather(r, hi), group=group)
-        st = engine.panel(w, window_only=True)
-        if st.miss:
-            dist.all_reduce(engine.gather(r, m), group=group)
-            st = engine.panel(w, window_only=False)
-            assert not st.miss
-        assert st.r == r, (st.r, r)
-        rb = st.rb
-        engine.apply(w)
-        if w + 1 < W and rb > 0:
-            for o in range(nranks):
-                mask = int(st.owners[o])
-                if not mask:
-                    continue
-                cnt = bin(mask).count("1")
-                buf = engine.pack_view(w, cnt) if o == engine.rank else engine.recv_view(w, cnt)
-                dist.broadcast(buf, src=o, group=group)
-                engine.unpack(w, mask, buf)
-        engine.trailing(w)
+        col = engine.step_gather(w)
+        if not solo:
+            dist.all_reduce(col, group=group)
+        stage = engine.step_panel(w)
+        if stage is not None and not solo:
+            dist.all_reduce(stage, group=group)
+        engine.step_update(w)
     return engine.finish()
 
 
@@ -176,6 +179,9 @@ class GpuShardEngine:
         self.pack = torch.zeros(pw.value, dtype=torch.int64, device=dev)
         self.recv = torch.zeros(pw.value, dtype=torch.int64, device=dev)
         self.status = np.zeros(8 + 2 * nranks, dtype=np.uint32)
+        # the stage lives in a torch tensor so the collective runs on it in place
+        self.stage = torch.zeros(64 * self.Wpad8, dtype=torch.int64, device=dev)
+        check(L.gf2cu_shard_set_stage(h, self._p(self.stage)))
         # One explicit stream for the library calls AND the torch copies /
         # collectives around them (run_sharded enters stream_ctx()); the legacy
         # default stream (handle 0) would leave them unordered.
@@ -230,6 +236,41 @@ class GpuShardEngine:
 
     def apply(self, w: int):
         check(self.L.gf2cu_shard_apply(self.h, w, self._p(self.pack), self._s()))
+
+    # --- asynchronous protocol (_run_steps) -----------------------------
+    def step_gather(self, w: int):
+        check(self.L.gf2cu_shard_step_gather(self.h, w, self._p(self.pos_words), self._s()))
+        return self.pos_words
+
+    def step_panel(self, w: int):
+        check(self.L.gf2cu_shard_step_panel(self.h, w, self._p(self.pos_words), self._s()))
+        if w + 1 >= self.W:
+            return None
+        x0 = (w + 1) & ~7
+        return self.stage[(x0 >> 3) * 64 * 8:]
+
+    def step_update(self, w: int):
+        check(self.L.gf2cu_shard_step_update(self.h, w, self._s()))
+
+    def gather_full(self, w: int):
+        check(self.L.gf2cu_shard_gather(self.h, self._p(self.pos_words), 0, self.m, self._s()))
+        return self.pos_words
+
+    def panel_full(self, w: int):
+        check(self.L.gf2cu_shard_panel(self.h, w, self._p(self.pos_words), 0, None, self._s()))
+
+    def pack_stage(self, w: int):
+        check(self.L.gf2cu_shard_pack_stage(self.h, w, self._s()))
+        x0 = (w + 1) & ~7
+        return self.stage[(x0 >> 3) * 64 * 8:]
+
+    def apply_staged(self, w: int):
+        check(self.L.gf2cu_shard_apply(self.h, w, None, self._s()))
+
+    def pivots(self) -> int:
+        v = C.c_size_t()
+        check(self.L.gf2cu_shard_pivots(self.h, C.byref(v), self._s()))
+        return int(v.value)
 
     def _tailw(self, w):
         x0 = (w + 1) & ~7

@@ -29,6 +29,9 @@ class NumpyShardEngine:
         self.pack = np.zeros(64 * self.Wpad8, dtype=U64)
         self.recv = np.zeros(64 * self.Wpad8, dtype=U64)
         self.stage = np.zeros((64, self.Wpad8), dtype=U64)
+        # tile-major stage of the asynchronous protocol (the device layout):
+        # word x of pivot slot t at ((x >> 3) * 64 + t) * 8 + (x & 7)
+        self.stage_flat = np.zeros(64 * self.Wpad8, dtype=U64)
 
     # --- protocol -------------------------------------------------------
     def stream_ctx(self):
@@ -142,6 +145,55 @@ class NumpyShardEngine:
                 else:
                     row[w0 + 1] |= hi_
                     row[w] = epart
+
+    # --- asynchronous protocol (shard.py::_run_steps) --------------------
+    def gather_full(self, w):
+        return self.gather(0, self.m)
+
+    def panel_full(self, w):
+        self.panel(w, window_only=False)
+
+    def pack_stage(self, w):
+        x0 = (w + 1) & ~7
+        lo = (x0 >> 3) * 64 * 8
+        self.stage_flat[lo:] = 0
+        r, rb = self.r, self.rb
+        for t in range(rb):
+            g = int(self.perm[r + t])
+            if owner_of(g, self.nranks, self.block) != self.rank:
+                continue
+            l = int(np.nonzero(self.g_of == g)[0][0])
+            for x in range(x0, self.Wpad8):
+                self.stage_flat[((x >> 3) * 64 + t) * 8 + (x & 7)] = self.mat[l, x]
+        return torch.from_numpy(self.stage_flat[lo:].view(np.int64))
+
+    def apply_staged(self, w):
+        """apply without the owner-ordered packing; the stage comes from the
+        all-reduced stage_flat."""
+        save = self.pack
+        self.pack = np.zeros(64 * self.Wpad8, dtype=U64)
+        try:
+            self.apply(w)
+        finally:
+            self.pack = save
+        x0 = (w + 1) & ~7
+        for t in range(64):
+            for x in range(x0, self.Wpad8):
+                self.stage[t, x] = self.stage_flat[((x >> 3) * 64 + t) * 8 + (x & 7)]
+
+    def pivots(self):
+        return self.r + self.rb
+
+    def step_gather(self, w):
+        return self.gather_full(w)
+
+    def step_panel(self, w):
+        self.panel_full(w)
+        return self.pack_stage(w) if w + 1 < self.W else None
+
+    def step_update(self, w):
+        self.apply_staged(w)
+        self.trailing(w)
 
     def _tailw(self, w):
         return self.Wpad8 - ((w + 1) & ~7)

@@ -1,8 +1,10 @@
 """CPU, world_size 2 and 4 over gloo: the multi-rank orchestration of the
 row-sharded PLE (paper_1111_6549_b200/shard.py::run_sharded) with the numpy
 test engine, assembled and compared bit-exactly with the oracle. Covers the
-window all-reduce, the window-miss full-gather re-run, per-owner pivot-tail
-broadcasts (small blocks -> many owners per step) and the final assembly."""
+asynchronous step protocol (sum all-reduce of the active panel column, full
+scans on window misses, pivot tails packed into the stage by their owners and
+summed -- small blocks give many owners per step), the lagged stop check and
+the final assembly."""
 import os
 import socket
 
