@@ -425,6 +425,10 @@ def gpu_sharded_arm(args, rank, world, local_rank):
     from paper_1111_6549_b200 import shard as S
 
     torch.cuda.set_device(local_rank)
+    if "RANK" not in os.environ:  # --sharded at N=1 without torchrun
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        os.environ["RANK"], os.environ["WORLD_SIZE"] = "0", "1"
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     n = args.n if args.n != N_DEFAULT else weak_n(world)
     m = n
