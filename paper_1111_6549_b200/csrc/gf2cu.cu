@@ -547,18 +547,20 @@ gf2cu_status solve_upper(gf2cu_matrix* a, const gf2cu::RrefParams& p, cudaStream
     if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
         CU_TRY(cudaFuncSetAttribute(gf2cu::rref_update_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, gf2cu::kTableBytes));
+        CU_TRY(cudaFuncSetAttribute(gf2cu::rref_step_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, gf2cu::kTableBytes));
         attr_set[a->device] = true;
     }
     const int sms = num_sms(a->device);
     const u32 nblk = p.R / 64;
-    const u32 solve_grid = (p.Wn + 7) / 8;
-    for (u32 J = nblk; J-- > 0;) {
-        gf2cu::rref_block_solve_kernel<<<solve_grid, 256, 0, s>>>(p, J);
-        if (J > 0) {
-            const u64 units = (u64)(p.WnPad8 / 8) * 64u * J;
-            const int grid = (int)std::min<u64>((u64)sms, std::max<u64>(1, units / 256));
-            gf2cu::rref_update_kernel<<<grid, gf2cu::kTrailThreads, gf2cu::kTableBytes, s>>>(p, J);
-        }
+    const u32 ntiles = p.WnPad8 / 8;
+    // the top block needs no update; then one launch per block J: X_J to the
+    // rows above, block J-1 finished in the same launch
+    gf2cu::rref_block_solve_kernel<<<(p.Wn + 7) / 8, 256, 0, s>>>(p, nblk - 1);
+    for (u32 J = nblk - 1; J >= 1; --J) {
+        const u64 units = (u64)ntiles * 64u * (J - 1u);
+        const int upd = units ? (int)std::min<u64>((u64)sms, std::max<u64>(1, units / 256)) : 0;
+        gf2cu::rref_step_kernel<<<ntiles + upd, gf2cu::kTrailThreads, gf2cu::kTableBytes, s>>>(p, J);
     }
     CU_TRY(cudaGetLastError());
     return GF2CU_OK;

@@ -184,6 +184,101 @@ __global__ void __launch_bounds__(kTrailThreads, 1) rref_update_kernel(RrefParam
     }
 }
 
+// One launch per 64-row block: rref_step_kernel(J) applies X_J to the rows
+// above block J and, in the same launch, finishes block J-1 -- CTAs
+// [0, ntiles) update block J-1's rows of one N tile each (X_J rows staged in
+// shared memory, one thread per row and word) and solve it in place (one warp
+// per word, 64 shuffle steps); the other CTAs update rows [0, 64(J-1)) with
+// the Gray tables. The next launch reads X_{J-1} in stream order.
+__global__ void __launch_bounds__(kTrailThreads, 1) rref_step_kernel(RrefParams p, u32 J) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const u32 ntiles = p.WnPad8 >> 3;
+    const u64* ucol = p.U + (size_t)J * p.R;
+    if (blockIdx.x < ntiles) {
+        // ---- block J-1 of tile blockIdx.x: update, then solve ----
+        u64 (*xs)[8] = reinterpret_cast<u64 (*)[8]>(smem);
+        const u32 tile = blockIdx.x;
+        for (u32 k = threadIdx.x; k < 512u; k += blockDim.x)
+            xs[k >> 3][k & 7u] = ldcg(nword(p.N, p.R, 64u * J + (k >> 3), tile * 8u + (k & 7u)));
+        __syncthreads();
+        for (u32 k = threadIdx.x; k < 512u; k += blockDim.x) {
+            const u32 row = 64u * (J - 1u) + (k >> 3), x = k & 7u;
+            if (tile * 8u + x >= p.Wn) continue;
+            u64 d = ldcg(ucol + row);
+            u64 acc = 0ull;
+            while (d) {
+                const int j = __ffsll((long long)d) - 1;
+                d &= d - 1ull;
+                acc ^= xs[j][x];
+            }
+            *nword(p.N, p.R, row, tile * 8u + x) ^= acc;
+        }
+        __syncthreads();
+        const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+        const u32 x = tile * 8u + wid;
+        if (wid < 8u && x < p.Wn) {
+            const u32 Jb = J - 1u;
+            const u32 i0 = 64u * Jb + lane, i1 = i0 + 32u;
+            const u64 u0 = p.U[(size_t)Jb * p.R + i0] & ~low_mask64((int)lane + 1);
+            const u64 u1 = p.U[(size_t)Jb * p.R + i1] & ~low_mask64((int)lane + 33);
+            u64* n0 = nword(p.N, p.R, i0, x);
+            u64* n1 = nword(p.N, p.R, i1, x);
+            u64 v0 = *n0, v1 = *n1;
+#pragma unroll 8
+            for (int j = 63; j >= 0; --j) {
+                const u64 xj = shfl64(j >= 32 ? v1 : v0, j & 31);
+                if ((u0 >> j) & 1ull) v0 ^= xj;
+                if ((u1 >> j) & 1ull) v1 ^= xj;
+            }
+            *n0 = v0;
+            *n1 = v1;
+        }
+        return;
+    }
+    // ---- rows [0, 64(J-1)) of every tile: Gray-table update ----
+    const u32 nrows = 64u * (J - 1u);
+    if (nrows == 0u) return;
+    const u32 nb = gridDim.x - ntiles, bi = blockIdx.x - ntiles;
+    const u64 total = (u64)ntiles * nrows;
+    const u64 beg = total * bi / nb, end = total * (bi + 1) / nb;
+    const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
+    u64 u = beg;
+    while (u < end) {
+        const u32 tile = (u32)(u / nrows);
+        const u32 row0 = (u32)(u % nrows);
+        const u32 cnt = (u32)min((u64)(nrows - row0), end - u);
+        __syncthreads();
+        gray_tables(smem, p.N + (((size_t)tile * p.R + 64u * J) << 3), 64u, 0u);
+        __syncthreads();
+        u64* tbase = p.N + (((size_t)tile * p.R) << 3) + 2u * ch;
+        for (u32 b = row0 + wid * 8u + rg; b < row0 + cnt; b += 4u * (kTrailThreads / 4)) {
+            u64 d[kUnroll];
+            ulonglong2 v[kUnroll];
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k) {
+                const u32 i = b + (u32)k * (kTrailThreads / 4);
+                d[k] = i < row0 + cnt ? ldcg(ucol + i) : 0ull;
+                v[k] = d[k] ? ldcg(reinterpret_cast<const ulonglong2*>(tbase + ((size_t)i << 3)))
+                            : make_ulonglong2(0ull, 0ull);
+            }
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k) {
+                if (!d[k]) continue;
+#pragma unroll
+                for (u32 gi = 0; gi < kTables; ++gi) {
+                    const u32 g = gi ^ par;
+                    const u32 e = (u32)(d[k] >> (8u * g)) & 0xffu;
+                    xor2(v[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
+                }
+                const u32 i = b + (u32)k * (kTrailThreads / 4);
+                *reinterpret_cast<ulonglong2*>(tbase + ((size_t)i << 3)) = v[k];
+            }
+        }
+        u += cnt;
+    }
+}
+
 // Reduced rows back in the original column order: R_i = bit q_i + X_i on the
 // non-pivot columns for i < r, zero rows below (row-major, words < W).
 __global__ void rref_scatter_kernel(RrefParams p) {
