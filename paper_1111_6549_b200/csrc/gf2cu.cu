@@ -125,6 +125,21 @@ int num_sms(int dev) {
     return g_num_sms[dev];
 }
 
+// GF2CU_WATCHDOG_S=<seconds> raises the spin watchdog of the persistent
+// kernels (runs under compute-sanitizer are 10-100x slower); once per device.
+void apply_watchdog_env(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    done[dev] = true;
+    if (const char* e = std::getenv("GF2CU_WATCHDOG_S")) {
+        const double sec = std::atof(e);
+        if (sec > 0) {
+            const unsigned long long ns = (unsigned long long)(sec * 1e9);
+            cudaMemcpyToSymbol(gf2cu::g_watchdog_ns, &ns, sizeof(ns));
+        }
+    }
+}
+
 }  // namespace
 
 namespace {
@@ -887,6 +902,7 @@ gf2cu_status gf2cu_matrix_create(size_t m, size_t n, int device, gf2cu_matrix** 
     cudaError_t e = cudaMalloc(&a->data, bytes);
     if (e == cudaSuccess) e = cudaMemset(a->data, 0, bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) apply_watchdog_env(device);
     if (e != cudaSuccess) {
         cudaFree(a->data);
         delete a;
@@ -1263,6 +1279,7 @@ gf2cu_status gf2cu_shard_create(size_t m, size_t n, int rank, int nranks, size_t
     if (e == cudaSuccess) e = cudaMemset(s->data, 0, ml * s->Wp * 8);
     if (e == cudaSuccess) e = cudaMemset(s->stage, 0, 64 * s->Wpad8 * 8);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) apply_watchdog_env(s->device);
     if (e != cudaSuccess) {
         gf2cu_shard_destroy(s);
         return cuda_fail(e, "gf2cu_shard_create");

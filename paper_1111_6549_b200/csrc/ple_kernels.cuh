@@ -169,15 +169,19 @@ __device__ __forceinline__ void red_release_add(u32* a, u32 v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
-// Spin (one thread) until *a >= target. Watchdog: after ~4 s sets sync->error
-// and returns false instead of hanging the GPU.
+// Watchdog budget of one spin (ns): 4 s unless the host raised it
+// (GF2CU_WATCHDOG_S, e.g. for runs under compute-sanitizer).
+__device__ unsigned long long g_watchdog_ns = 4000000000ull;
+
+// Spin (one thread) until *a >= target. Watchdog: after g_watchdog_ns sets
+// sync->error and returns false instead of hanging the GPU.
 __device__ __forceinline__ bool spin_geq(const u32* a, u32 target, u32* err) {
     if (ld_acquire(a) >= target) return true;
     const u64 t0 = globaltimer();
     for (;;) {
         if (ld_acquire(a) >= target) return true;
         if (*(volatile u32*)err) return false;
-        if (globaltimer() - t0 > 4000000000ull) {
+        if (globaltimer() - t0 > g_watchdog_ns) {
             atomicExch(err, 1u);
             return false;
         }
@@ -195,7 +199,7 @@ __device__ __forceinline__ bool spin_geq2(const u32* a, u32 ta, const u32* b, u3
         vb = ld_acquire(b);
         if (va >= ta && vb >= tb) return true;
         if (*(volatile u32*)err) return false;
-        if (globaltimer() - t0 > 4000000000ull) {
+        if (globaltimer() - t0 > g_watchdog_ns) {
             atomicExch(err, 1u);
             return false;
         }
