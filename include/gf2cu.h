@@ -68,6 +68,13 @@ typedef struct {
                                       per sweep (default: chosen by size --
                                       super-step from 2^24 matrix words)     */
 
+/* The device-driven row-sharded driver (ple_peer.cuh)
+ * with g = 1..8 ranks emulated on the one device: one cooperative launch,
+ * sms/g CTAs per rank, the ranks exchanging panel words and pivot tails
+ * through each other's buffers exactly as they do over NVLink peer memory
+ * when each rank owns a GPU. Same outputs as every other driver. */
+#define GF2CU_FLAG_PEER_RANKS(g) ((((unsigned)(g)) & 15u) << 16)
+
 /* Mirrors gf2::ColSwap (ple.hpp:41-43). */
 typedef struct {
     size_t a, b, from_row;
@@ -83,8 +90,9 @@ typedef struct {
     double alg_bytes;           /* sum over steps of 16*(m-r-rb)*(W-w-1)        */
     double h2d_bytes, d2h_bytes;/* host<->device bytes moved by gf2cu_ple       */
     double kernel_ms;           /* persistent kernel duration (CUDA events)     */
-    int driver;                 /* 2 = super-step (two panels per sweep),
-                                   1 = persistent single-panel, 0 = per phase   */
+    int driver;                 /* 3 = row-sharded (peer memory), 2 = super-step
+                                   (two panels per sweep), 1 = persistent
+                                   single-panel, 0 = per phase                  */
     double sweep_bytes;         /* bytes the trailing sweeps move: alg_bytes for
                                    one panel per sweep; for the super-step driver
                                    sum over super-steps of 16*(m-r-rba-rbb)*(W-w-2)

@@ -22,6 +22,7 @@
 #include "ple_persistent.cuh"
 #include "ple_super.cuh"
 #include "ple_shard.cuh"
+#include "ple_peer.cuh"
 #include "rref_kernels.cuh"
 #include "gemm_kernels.cuh"
 
@@ -177,6 +178,25 @@ cudaError_t grow(T** ptr, size_t* have, size_t need) {
 
 }  // namespace
 
+namespace {
+
+// Buffers of the device-driven row-sharded driver (ple_peer.cuh) when all G
+// ranks run in one cooperative launch on this matrix's device.
+struct PeerWs {
+    unsigned G = 0, block = 0;
+    std::vector<gf2cu::PeerParams> hp;  // host copies of the ranks' parameters
+    gf2cu::PeerParams* dp = nullptr;    // device copy (the kernel argument)
+    std::vector<void*> allocs;
+};
+
+void free_peer(PeerWs& w) {
+    for (void* x : w.allocs) cudaFree(x);
+    cudaFree(w.dp);
+    w = PeerWs{};
+}
+
+}  // namespace
+
 struct gf2cu_matrix {
     size_t m = 0, n = 0, W = 0, Wp = 0;
     int device = 0;
@@ -184,6 +204,7 @@ struct gf2cu_matrix {
     u64* alt = nullptr;  // tile-major working copy used by the factorization
     Workspace ws;
     RrefWs rw;
+    PeerWs pw;
     cudaStream_t own = nullptr;
 };
 
@@ -227,10 +248,184 @@ gf2cu_status check_cfg(const gf2cu_cfg* cfg) {
     return GF2CU_OK;
 }
 
+size_t shard_rows(size_t m, size_t rank, size_t G, size_t block) {
+    const size_t cyc = block * G, full = m / cyc, rem = m % cyc;
+    const size_t lo = rank * block;
+    return full * block + (rem > lo ? std::min(block, rem - lo) : 0);
+}
+
+// The row-sharded driver (ple_peer.cuh) with G ranks emulated on this
+// matrix's device: one cooperative launch, sms/G CTAs per rank, every rank's
+// buffers in this device's memory (the peers' stores are ordinary stores).
+// Same outputs as run_ple.
+gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, size_t* swaps,
+                          size_t* q, size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+                          gf2cu_stats* stats) {
+    const size_t m = a->m, n = a->n, W = a->W, Wp8 = wpad8(W);
+    const size_t mn = std::max<size_t>(1, std::min(m, n));
+    const unsigned block = 256;
+    cudaStream_t s = pick_stream(a, cfg ? cfg->stream : nullptr);
+    const bool timing = cfg && (cfg->flags & GF2CU_FLAG_TIME_KERNELS);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (m == 0 || n == 0) {
+        *rank = 0;
+        if (n_col_swaps) *n_col_swaps = 0;
+        return GF2CU_OK;
+    }
+    const int sms = num_sms(a->device);
+    if (G < 1 || G > (unsigned)gf2cu::kMaxRanks || (unsigned)sms / G < 2)
+        return fail(GF2CU_EINVAL, "peer driver: 1..8 ranks, at least 2 CTAs each");
+    PeerWs& pw = a->pw;
+    if (pw.G != G || pw.block != block) {
+        free_peer(pw);
+        pw.G = G;
+        pw.block = block;
+        pw.hp.assign(G, gf2cu::PeerParams{});
+        auto alloc = [&](void** ptr, size_t bytes) -> cudaError_t {
+            cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+            if (e == cudaSuccess) pw.allocs.push_back(*ptr);
+            return e;
+        };
+#define PA(ptr, bytes) CU_TRY(alloc(reinterpret_cast<void**>(&(ptr)), (bytes)))
+        for (unsigned k = 0; k < G; ++k) {
+            gf2cu::PeerParams& h = pw.hp[k];
+            gf2cu::Params& p = h.p;
+            h.m_loc = (u32)shard_rows(m, k, G, block);
+            h.rank = k;
+            h.nranks = G;
+            h.block = block;
+            PA(h.mat, (size_t)h.m_loc * Wp8 * 8);
+            PA(h.info[0], (size_t)h.m_loc * 16);
+            PA(h.info[1], (size_t)h.m_loc * 16);
+            PA(h.lo, (W + 1) * 4);
+            PA(p.perm, m * 4);
+            PA(p.inv, m * 4);
+            PA(p.state, sizeof(gf2cu::StepState));
+            PA(p.pout, sizeof(gf2cu::PanelOut));
+            PA(p.swaps, mn * 4);
+            PA(p.qcol, mn * 4);
+            PA(p.rhist, (W + 1) * 4);
+            PA(p.rbhist, (W + 1) * 4);
+            PA(p.sync, sizeof(gf2cu::SyncState));
+            PA(p.ap_claim, 2 * (W + 1) * 4);
+            p.ap_done = p.ap_claim + W + 1;
+            gf2cu::PeerBufs& b = h.peer[k];
+            for (int x = 0; x < 2; ++x) {
+                PA(b.pb[x], m * 8);
+                PA(b.pb2[x], m * 8);
+                PA(b.stage[x], 64 * Wp8 * 8);
+            }
+            PA(b.ctr, gf2cu::kCtrWords * 4);
+            const char* dv = std::getenv("GF2CU_PW_DIV");
+            p.pw_div = dv ? (u32)std::max(64, std::atoi(dv)) : 8192u;
+            p.m = (u32)m;
+            p.n = (u32)n;
+            p.W = (u32)W;
+            p.Wpad8 = (u32)Wp8;
+        }
+#undef PA
+        for (unsigned k = 0; k < G; ++k)
+            for (unsigned j = 0; j < G; ++j) pw.hp[k].peer[j] = pw.hp[j].peer[j];
+        CU_TRY(cudaMalloc(&pw.dp, G * sizeof(gf2cu::PeerParams)));
+        CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
+        static bool attr_set[64] = {false};
+        if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
+            CU_TRY(cudaFuncSetAttribute(gf2cu::ple_peer_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, gf2cu::kTableBytes));
+            attr_set[a->device] = true;
+        }
+    }
+    for (unsigned k = 0; k < G; ++k) {
+        const gf2cu::PeerParams& h = pw.hp[k];
+        CU_TRY(cudaMemsetAsync(h.p.sync, 0, sizeof(gf2cu::SyncState), s));
+        CU_TRY(cudaMemsetAsync(h.p.ap_claim, 0, 2 * (W + 1) * 4, s));
+        CU_TRY(cudaMemsetAsync(h.lo, 0xff, (W + 1) * 4, s));
+        CU_TRY(cudaMemsetAsync(h.peer[k].ctr, 0, gf2cu::kCtrWords * 4, s));
+    }
+    gf2cu::peer_tile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
+    CU_TRY(cudaGetLastError());
+    const u32 cpr = (u32)sms / G;
+    u32 nsteps = (u32)W;
+    void* args[] = {&pw.dp, (void*)&cpr, &nsteps};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (timing) {
+        CU_TRY(cudaEventCreate(&ev[0]));
+        CU_TRY(cudaEventCreate(&ev[1]));
+        CU_TRY(cudaEventRecord(ev[0], s));
+    }
+    CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_peer_kernel, dim3(cpr * G),
+                                       dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
+    if (timing) CU_TRY(cudaEventRecord(ev[1], s));
+    gf2cu::peer_untile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
+    CU_TRY(cudaGetLastError());
+
+    const gf2cu::PeerParams& h0 = pw.hp[0];
+    u32 err = 0;
+    for (unsigned k = 0; k < G; ++k) {
+        u32 c[gf2cu::kCtrWords];
+        CU_TRY(cudaMemcpyAsync(c, pw.hp[k].peer[k].ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaStreamSynchronize(s));
+        err |= c[gf2cu::kCtrErr];
+    }
+    if (err) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
+    gf2cu::SyncState sy{};
+    gf2cu::StepState fin{};
+    CU_TRY(cudaMemcpyAsync(&sy, h0.p.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaMemcpyAsync(&fin, h0.p.state, sizeof(fin), cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    const size_t steps = std::min<size_t>(W, sy.panel_done);
+    const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
+    std::vector<u32> sw(rk), qq(rk), rh(steps), rbh(steps);
+    if (rk) {
+        CU_TRY(cudaMemcpyAsync(sw.data(), h0.p.swaps, rk * 4, cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaMemcpyAsync(qq.data(), h0.p.qcol, rk * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (steps) {
+        CU_TRY(cudaMemcpyAsync(rh.data(), h0.p.rhist, steps * 4, cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaMemcpyAsync(rbh.data(), h0.p.rbhist, steps * 4, cudaMemcpyDeviceToHost, s));
+    }
+    CU_TRY(cudaStreamSynchronize(s));
+    *rank = rk;
+    size_t ncs = 0;
+    for (size_t i = 0; i < rk; ++i) {
+        swaps[i] = sw[i];
+        q[i] = qq[i];
+        if (qq[i] != i) {
+            if (col_swaps) col_swaps[ncs] = gf2cu_colswap{i, (size_t)qq[i], i};
+            ++ncs;
+        }
+    }
+    if (n_col_swaps) *n_col_swaps = ncs;
+    if (stats) {
+        stats->steps = steps;
+        double bytes = 0.0;
+        for (size_t w = 0; w < steps; ++w) {
+            if (rh[w] >= m || w + 1 >= W) continue;
+            ++stats->trailing_launches;
+            bytes += 16.0 * double(m - rh[w] - rbh[w]) * double(W - w - 1);
+        }
+        stats->alg_bytes = bytes;
+        stats->sweep_bytes = bytes;
+        stats->driver = 3;
+        if (timing) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[0], ev[1]);
+            stats->kernel_ms = ms;
+        }
+    }
+    if (timing) {
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+    }
+    return GF2CU_OK;
+}
+
 // Launches the whole decomposition on `s`; outputs are copied to the host.
 gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
                      size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
                      gf2cu_stats* stats) {
+    if (const unsigned pr = cfg ? (cfg->flags >> 16) & 15u : 0u)
+        return run_ple_peer(a, cfg, pr, swaps, q, rank, col_swaps, n_col_swaps, stats);
     gf2cu_status st = ensure_ws(a);
     if (st != GF2CU_OK) return st;
     Workspace& ws = a->ws;
@@ -919,6 +1114,7 @@ gf2cu_status gf2cu_matrix_destroy(gf2cu_matrix* a) {
     cudaFree(a->alt);
     free_ws(a->ws);
     free_rref(a->rw);
+    free_peer(a->pw);
     if (a->own) cudaStreamDestroy(a->own);
     delete a;
     return GF2CU_OK;

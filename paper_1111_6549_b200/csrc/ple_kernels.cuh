@@ -189,6 +189,32 @@ __device__ __forceinline__ bool spin_geq(const u32* a, u32 target, u32* err) {
     }
 }
 
+// System scope (the row-sharded driver: counters that other GPUs signal
+// through NVLink peer memory).
+__device__ __forceinline__ u32 ld_acquire_sys(const u32* a) {
+    u32 v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_release_add_sys(u32* a, u32 v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ bool spin_geq_sys(const u32* a, u32 target, u32* err) {
+    if (ld_acquire_sys(a) >= target) return true;
+    const u64 t0 = globaltimer();
+    for (;;) {
+        if (ld_acquire_sys(a) >= target) return true;
+        if (*(volatile u32*)err) return false;
+        if (globaltimer() - t0 > g_watchdog_ns) {
+            atomicExch(err, 1u);
+            return false;
+        }
+        __nanosleep(64);
+    }
+}
+
 // Both counters at once (their loads in flight together).
 __device__ __forceinline__ bool spin_geq2(const u32* a, u32 ta, const u32* b, u32 tb, u32* err) {
     u32 va = ld_acquire(a), vb = ld_acquire(b);
@@ -320,6 +346,7 @@ struct LookAhead {
     int super_mode = 0;
     u64* piv2_out = nullptr;  // panel a: its pivot rows' pre-super-step word w+1
     u64* C_out = nullptr;     // panel b: panel-a combination of each of its pivot rows
+    bool sys = false;         // cap_ctr is signalled by other GPUs (system-scope acquire)
 };
 
 // All `nthr` threads: scan positions r + [nwin, nrem) reducing each raw panel
@@ -397,7 +424,8 @@ __device__ __forceinline__ void la_wait_cap(const LookAhead* la, PanelShared& sh
                                             int bar_cnt) {
     if (!la || sh.cap_ok) return;
     if (threadIdx.x == 0)
-        sh.cap_ok = spin_geq(la->cap_ctr, la->cap_target, la->err) ? 1 : -1;
+        sh.cap_ok = (la->sys ? spin_geq_sys(la->cap_ctr, la->cap_target, la->err)
+                             : spin_geq(la->cap_ctr, la->cap_target, la->err)) ? 1 : -1;
     named_bar(bar_id, bar_cnt);
 }
 

@@ -51,6 +51,8 @@ class PleConfig:
     multi_kernel: bool = False     # one launch per phase (cross-check driver)
     single_panel: bool = False     # force the persistent driver with one panel per sweep
     super_step: bool = False       # force the super-step driver (two panels per sweep)
+    peer_ranks: int = 0            # >0: the row-sharded peer-memory driver with this many
+                                   # ranks emulated on the one device (ple_peer.cuh)
 
     def to_c(self) -> gf2cu_cfg:
         c = gf2cu_cfg()
@@ -63,7 +65,8 @@ class PleConfig:
         c.flags = (_lib.FLAG_TIME_KERNELS if self.time_kernels else 0) | \
             (_lib.FLAG_MULTI_KERNEL if self.multi_kernel else 0) | \
             (_lib.FLAG_SINGLE_PANEL if self.single_panel else 0) | \
-            (_lib.FLAG_SUPER_STEP if self.super_step else 0)
+            (_lib.FLAG_SUPER_STEP if self.super_step else 0) | \
+            ((int(self.peer_ranks) & 15) << 16)
         return c
 
 
