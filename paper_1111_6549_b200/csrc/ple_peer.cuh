@@ -162,6 +162,39 @@ __device__ __forceinline__ void peer_ship(const PeerParams& s, const u32* piv, u
     }
 }
 
+// The part of step w's remaining-tile shipment that this worker's own step
+// w-1 sweep share finalized: the share is units [beg, end) of (tile, local
+// row) pairs over tiles from tlo and rows [lo, lo + nrows), tile-major, so
+// for one pivot row the tiles inside it are a contiguous range. Tiles below
+// t_first (step w's look-ahead tiles, shipped separately) are skipped.
+__device__ __forceinline__ void peer_ship_share(const PeerParams& s, const u32* piv, u32 rb, u32 w,
+                                                u32 t_first, u32 ntiles, u32 tlo, u32 lo,
+                                                u32 nrows, u64 beg, u64 end) {
+    if (nrows == 0 || beg >= end) return;
+    // the share runs from (tile bt, row br) to (tile et, row er), inclusive
+    const u32 bt = (u32)(beg / nrows), br = (u32)(beg - (u64)bt * nrows);
+    const u32 et = (u32)((end - 1) / nrows), er = (u32)(end - 1 - (u64)et * nrows);
+    // all (pivot, tile, 16-byte chunk) units at once, so the loads overlap
+    const u32 span = (et - bt + 1u) * 4u;
+    for (u32 e = threadIdx.x; e < rb * span; e += blockDim.x) {
+        const u32 k = e / span, rem = e - k * span;
+        const u32 g = piv[k];
+        if (shard_owner(g, s.nranks, s.block) != s.rank) continue;
+        const u32 l = shard_local(g, s.nranks, s.block);
+        if (l < lo || l >= lo + nrows) continue;
+        const u32 off = l - lo;
+        const u32 t = bt + (rem >> 2), q = rem & 3u;  // share-relative tile
+        if ((t == bt && off < br) || (t == et && off > er)) continue;
+        const u32 tt = tlo + t;
+        if (tt < t_first || tt >= ntiles) continue;
+        const ulonglong2 v = ldcg(reinterpret_cast<const ulonglong2*>(
+            s.mat + (((size_t)tt * s.m_loc + l) << 3) + 2u * q));
+        const size_t o = (((size_t)tt * 64u + k) << 3) + 2u * q;
+        for (u32 j2 = 0; j2 < s.nranks; ++j2)
+            *reinterpret_cast<ulonglong2*>(s.peer[j2].stage[w & 1u] + o) = v;
+    }
+}
+
 // Local rows [row0, row0 + cnt) of tile `tile` (trail_rows with rows indexed
 // locally): tail ^= sum_g T_g[byte_g(d)]; the tile holding word w+1 (w+2)
 // stores each active row's new word into every rank's pb (pb2) at the row's
@@ -348,6 +381,11 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             if (atomicAdd(&sy->cap_count, 1u) == nworkers - 1u) peer_signal(s, kCtrCap);
         }
     }
+    // this worker's sweep share of the previous step (tile-major units
+    // [pbeg, pend) over tiles from ptlo and local rows [plo, plo + pnrows))
+    u32 ptlo = 0, plo = 0, pnrows = 0;
+    u64 pbeg = 0, pend = 0;
+    const u32 ntiles = p.Wpad8 >> 3;
     for (u32 w = 0; w < nsteps; ++w) {
         if (!peer_wait(s, &sy->panel_done, w + 1u, false, s_ok)) return;
         const u32 r = *(volatile u32*)&p.rhist[w], rb = *(volatile u32*)&p.rbhist[w];
@@ -365,6 +403,22 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         for (u32 k = threadIdx.x; k < rb; k += blockDim.x) s_piv[k] = ldcg(p.perm + r + k);
         __syncthreads();
 
+        // close step w-1: stage on every rank the tiles of step w's pivot
+        // rows that this worker's step w-1 share finished, then arrive; the
+        // last arrival of the rank tells every rank (kCtrSt). One barrier per
+        // step, as in the single-GPU driver.
+        if (sweep && rb > 0 && tcap + 1u < ntiles) {
+            if (w == 0)
+                peer_ship(s, s_piv, rb, w, tcap + 1u, ntiles - 1u, wk, nworkers);
+            else
+                peer_ship_share(s, s_piv, rb, w, tcap + 1u, ntiles, ptlo, plo, pnrows, pbeg, pend);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&sy->t_count, 1u) == nworkers * (w + 1u) - 1u) peer_signal(s, kCtrSt);
+        }
+
         // pre-work: job 0 stages this rank's pivots' look-ahead tiles on
         // every rank; jobs 1.. apply a chunk of local rows and sweep them
         // over the look-ahead tiles (capturing words w+1, w+2 everywhere)
@@ -378,7 +432,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             if (job == 0) {
                 if (sweep) {
                     if (!early_cap(w, p.W) && w > 0 &&
-                        !peer_wait(s, &sy->t_count, nworkers * w, false, s_ok))
+                        !peer_wait(s, &sy->t_count, nworkers * (w + 1u), false, s_ok))
                         return;
                     peer_ship(s, s_piv, rb, w, tile0, tcap, 0, 1);
                 }
@@ -417,6 +471,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             // the chunk that completes the step's pre-work tells every rank
             // that this rank's captures landed
             if (mine) {
+                // (gpu scope suffices here: the signalling thread's system-
+                // scope fence and release are cumulative over what it saw)
                 __threadfence();
                 if (atomicAdd(&p.ap_done[w], mine) + mine == nch) peer_signal(s, kCtrCap);
             } else if (nch == 0 && wk == 0) {
@@ -424,28 +480,31 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             }
         }
 
-        // rest: after this rank's step w-1 (its pivot rows' tails are final)
-        // and all of this step's pre-work (every row's info)
+        // rest: after every local worker closed step w-1 (t_count) and all of
+        // this step's pre-work (every row's info); then, for the sweep, after
+        // every rank staged its pivots' remaining tiles (kCtrSt)
         if (threadIdx.x == 0) {
-            s_ok = spin_geq2(&sy->t_count, nworkers * w, &p.ap_done[w], nch, err) ? 1u : 0u;
+            s_ok = spin_geq2(&sy->t_count, nworkers * (w + 1u), &p.ap_done[w], nch, err) ? 1u : 0u;
             if (!s_ok) peer_fail(s);
         }
         __syncthreads();
         if (!s_ok) return;
-        const u32 ntiles = p.Wpad8 >> 3;
-        if (sweep) peer_ship(s, s_piv, rb, w, tcap + 1u, ntiles - 1u, wk, nworkers);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence_system();
-            if (atomicAdd(&sy->st_count, 1u) == nworkers * (w + 1u) - 1u) peer_signal(s, kCtrSt);
-        }
+        ptlo = tcap + 1u;
+        plo = lo;
+        pnrows = nrows;
+        pbeg = pend = 0;
         if (sweep && tcap + 1u < ntiles && nrows > 0) {
-            if (!peer_wait(s, ctr + kCtrSt, G * (w + 1u), true, s_ok)) return;
             const u64 total = (u64)(ntiles - tcap - 1u) * nrows;
-            peer_trail_share(s, q, smem, w, r, rb, lo, tcap + 1u, total * wk / nworkers,
-                             total * (wk + 1u) / nworkers, info);
+            pbeg = total * wk / nworkers;
+            pend = total * (wk + 1u) / nworkers;
         }
-        cta_arrive(&sy->t_count);
+        if (sweep && tcap + 1u < ntiles) {
+            // (waited even without work: a rank's step w+2 stores into
+            // stage[w & 1] must follow every rank's step w reads of it)
+            if (!peer_wait(s, ctr + kCtrSt, G * (w + 1u), true, s_ok)) return;
+            if (rb > 0 && pend > pbeg)
+                peer_trail_share(s, q, smem, w, r, rb, lo, tcap + 1u, pbeg, pend, info);
+        }
     }
 }
 
