@@ -263,7 +263,10 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
                           gf2cu_stats* stats) {
     const size_t m = a->m, n = a->n, W = a->W, Wp8 = wpad8(W);
     const size_t mn = std::max<size_t>(1, std::min(m, n));
-    const unsigned block = 256;
+    // 256-row blocks; small matrices get smaller ones so that every rank
+    // owns rows (the result does not depend on the distribution)
+    unsigned block = (unsigned)std::max<size_t>(1, std::min<size_t>(256, m / (2 * (size_t)std::max(1u, G))));
+    if (const char* e = std::getenv("GF2CU_PEER_BLOCK")) block = (unsigned)std::max(1, std::atoi(e));
     cudaStream_t s = pick_stream(a, cfg ? cfg->stream : nullptr);
     const bool timing = cfg && (cfg->flags & GF2CU_FLAG_TIME_KERNELS);
     if (stats) std::memset(stats, 0, sizeof(*stats));

@@ -23,10 +23,14 @@ def load(name):
         return json.load(f)
 
 
-@pytest.mark.parametrize("driver", ["single", "super"])
+SUITE_CFGS = {"single": G.PleConfig(single_panel=True), "super": G.PleConfig(super_step=True),
+              "peer2": G.PleConfig(peer_ranks=2), "peer5": G.PleConfig(peer_ranks=5)}
+
+
+@pytest.mark.parametrize("driver", sorted(SUITE_CFGS))
 def test_suite_golden_gpu(driver):
     bad = []
-    cfg = G.PleConfig(super_step=True) if driver == "super" else G.PleConfig(single_panel=True)
+    cfg = SUITE_CFGS[driver]
     for e in load("suite.json")["cases"]:
         m, n = e["m"], e["n"]
         a = G.BitMatrix(m, n, S.build(m, n, e["kind"], e["seed"]))
@@ -79,6 +83,27 @@ def test_full_config_bit_exact(name):
     d = G.DeviceMatrix(m, n)
     d.upload(a.words)
     out = G.block_iterative_ple(d)
+    d.download(a.words)
+    assert out.rank == cfg["rank"]
+    assert S.outcome_hash(a.words, n, out.rank, out.p.swaps, out.q) == cfg["sha256"]
+
+
+@pytest.mark.parametrize("name,ranks", [("c2_16384x65536_dense", 4), ("c3_32768_p256", 4),
+                                        ("c4_32768_xy", 3), ("c5_65536_ctr", 8)])
+def test_full_config_peer_ranks(name, ranks):
+    """The row-sharded peer-memory driver (ple_peer.cuh) with `ranks` ranks
+    emulated on the one GPU, bit-exact on full-size BASELINE configs: sparse
+    (window misses), rank-deficient, wide, and config 5 over 8 ranks."""
+    cfgs = {c["name"]: c for c in load("full_configs.json")["configs"]}
+    if name not in cfgs:
+        pytest.skip(f"{name} not in full_configs.json yet")
+    cfg = cfgs[name]
+    m, n = cfg["m"], cfg["n"]
+    a = full_input(cfg)
+    d = G.DeviceMatrix(m, n)
+    d.upload(a.words)
+    out = G.block_iterative_ple(d, G.PleConfig(peer_ranks=ranks))
+    assert out.stats["driver"] == 3
     d.download(a.words)
     assert out.rank == cfg["rank"]
     assert S.outcome_hash(a.words, n, out.rank, out.p.swaps, out.q) == cfg["sha256"]

@@ -57,6 +57,22 @@ def test_small_shapes(m, n, kind, super_step):
     assert_same(*run_both(a, m, n, cfg), what=f"{kind} {m}x{n} super={super_step}")
 
 
+@pytest.mark.parametrize("ranks", [1, 2, 5, 8])
+@pytest.mark.parametrize("m,n", SMALL)
+@pytest.mark.parametrize("kind", ["dense", "deficient"])
+def test_small_shapes_peer_ranks(m, n, kind, ranks):
+    """The row-sharded peer-memory driver with 1-8 emulated ranks; many
+    ranks own no rows at these sizes (block-cyclic 256-row blocks)."""
+    seed = m * 1000 + n
+    a = O.fill_random(m, n, 0.5, seed)
+    if kind == "deficient":
+        rng = np.random.default_rng(seed)
+        for _ in range(4):
+            d, s = rng.integers(0, m, 2)
+            a[d] = a[s]
+    assert_same(*run_both(a, m, n, G.PleConfig(peer_ranks=ranks)), what=f"{kind} {m}x{n} ranks={ranks}")
+
+
 @pytest.mark.parametrize("m,n,density", [(1024, 1024, 0.5), (2048, 2048, 0.5), (1500, 2500, 0.5),
                                          (2048, 2048, 1 / 64), (2048, 2048, 1 / 256),
                                          (4096, 4096, 0.5)])
@@ -109,7 +125,8 @@ def test_smoke_entry():
 
 
 DRIVERS = {"super": (G.PleConfig(super_step=True), 2), "single": (G.PleConfig(single_panel=True), 1),
-           "multi": (G.PleConfig(multi_kernel=True), 0)}
+           "multi": (G.PleConfig(multi_kernel=True), 0), "peer1": (G.PleConfig(peer_ranks=1), 3),
+           "peer3": (G.PleConfig(peer_ranks=3), 3), "peer8": (G.PleConfig(peer_ranks=8), 3)}
 
 
 @pytest.mark.parametrize("driver", sorted(DRIVERS))
