@@ -268,6 +268,48 @@ gf2cu_status gf2cu_shard_finish(gf2cu_shard* s, size_t* swaps, size_t* q, size_t
                                 uint32_t* perm, void* stream);
 
 /* ------------------------------------------------------------------ */
+/* Row-sharded multi-GPU PLE driven on the device (one process per GPU) */
+/* ------------------------------------------------------------------ */
+/* The same block-cyclic row distribution as gf2cu_shard_*, but the whole
+ * factorization is ONE persistent kernel per rank (ple_peer.cuh): the ranks
+ * exchange panel words and pivot-row tails by storing into each other's
+ * exchange buffers over NVLink (CUDA IPC mappings) and signalling
+ * system-scope counters; no host call or collective per step. Sequence per
+ * rank (paper_1111_6549_b200/peer.py):
+ *   create -> export (IPC handle of this rank's exchange buffers) -> the
+ *   caller all-gathers the handles -> connect(all handles, rank order) ->
+ *   upload / fill_ctr -> [reset -> barrier across ranks -> run -> finish ->
+ *   download]*.
+ * run blocks until this rank's kernel is done; all ranks must run
+ * concurrently (one process per GPU). A rank stuck waiting on another trips
+ * the kernel watchdog (GF2CU_ECUDA) instead of hanging. With nranks = 1,
+ * connect may be skipped. */
+typedef struct gf2cu_peer gf2cu_peer;
+
+#define GF2CU_PEER_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
+
+gf2cu_status gf2cu_peer_create(size_t m, size_t n, int rank, int nranks, size_t block, int device,
+                               gf2cu_peer** out);
+gf2cu_status gf2cu_peer_destroy(gf2cu_peer* p);
+gf2cu_status gf2cu_peer_info(const gf2cu_peer* p, size_t* m_local);
+gf2cu_status gf2cu_peer_export(const gf2cu_peer* p, void* handle);
+/* handles: nranks x GF2CU_PEER_HANDLE_BYTES in rank order (own entry ignored). */
+gf2cu_status gf2cu_peer_connect(gf2cu_peer* p, const void* handles);
+/* Local rows in local order, host_stride words apart. */
+gf2cu_status gf2cu_peer_upload(gf2cu_peer* p, const uint64_t* host, size_t host_stride, void* stream);
+gf2cu_status gf2cu_peer_download(const gf2cu_peer* p, uint64_t* host, size_t host_stride,
+                                 void* stream);
+gf2cu_status gf2cu_peer_fill_ctr(gf2cu_peer* p, uint64_t seed, void* stream);
+/* Zero this rank's counters; every rank must reset before any rank runs. */
+gf2cu_status gf2cu_peer_reset(gf2cu_peer* p, void* stream);
+/* The factorization of this rank's rows (stats: steps, alg_bytes of the whole
+ * matrix, kernel_ms of this rank's launch). */
+gf2cu_status gf2cu_peer_run(gf2cu_peer* p, void* stream, gf2cu_stats* stats);
+/* Replicated outcome (as gf2cu_shard_finish); local rows then download. */
+gf2cu_status gf2cu_peer_finish(gf2cu_peer* p, size_t* swaps, size_t* q, size_t* rank,
+                               uint32_t* perm, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* Host-side input generators (bench/test inputs; not the hot path)     */
 /* ------------------------------------------------------------------ */
 /* gf2::fill_random (bit_matrix.hpp:459-486), mt19937_64-driven. */

@@ -84,6 +84,11 @@ FLAG_TIME_KERNELS = 1
 FLAG_MULTI_KERNEL = 2
 FLAG_SINGLE_PANEL = 4
 FLAG_SUPER_STEP = 8
+PEER_HANDLE_BYTES = 64  # GF2CU_PEER_HANDLE_BYTES
+
+
+def FLAG_PEER_RANKS(g: int) -> int:
+    return (int(g) & 15) << 16
 
 # name -> (restype, argtypes): every symbol include/gf2cu.h declares.
 _sz, _szp = C.c_size_t, C.POINTER(C.c_size_t)
@@ -134,6 +139,17 @@ SYMBOLS = {
     "gf2cu_shard_unpack": (C.c_int, [_mp, _sz, C.c_uint64, _u64p, C.c_void_p]),
     "gf2cu_shard_trailing": (C.c_int, [_mp, _sz, C.c_void_p]),
     "gf2cu_shard_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),
+    "gf2cu_peer_create": (C.c_int, [_sz, _sz, C.c_int, C.c_int, _sz, C.c_int, C.POINTER(_mp)]),
+    "gf2cu_peer_destroy": (C.c_int, [_mp]),
+    "gf2cu_peer_info": (C.c_int, [_mp, _szp]),
+    "gf2cu_peer_export": (C.c_int, [_mp, C.c_void_p]),
+    "gf2cu_peer_connect": (C.c_int, [_mp, C.c_void_p]),
+    "gf2cu_peer_upload": (C.c_int, [_mp, _u64p, _sz, C.c_void_p]),
+    "gf2cu_peer_download": (C.c_int, [_mp, _u64p, _sz, C.c_void_p]),
+    "gf2cu_peer_fill_ctr": (C.c_int, [_mp, C.c_uint64, C.c_void_p]),
+    "gf2cu_peer_reset": (C.c_int, [_mp, C.c_void_p]),
+    "gf2cu_peer_run": (C.c_int, [_mp, C.c_void_p, C.POINTER(gf2cu_stats)]),
+    "gf2cu_peer_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),
     "gf2cu_fill_random": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_double, C.c_uint64]),
     "gf2cu_fill_ctr": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_uint64]),
     "gf2cu_fill_random_rows": (C.c_int, [_u64p, _sz, _sz, _sz, _sz, C.c_uint64]),

@@ -254,6 +254,147 @@ size_t shard_rows(size_t m, size_t rank, size_t G, size_t block) {
     return full * block + (rem > lo ? std::min(block, rem - lo) : 0);
 }
 
+// One rank's exchange buffers (ple_peer.cuh PeerBufs) live in ONE allocation
+// so a single IPC handle maps them: pb[2], pb2[2], stage[2], counters.
+size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+size_t peer_xbytes(size_t m, size_t Wp8) {
+    return 4 * al256(std::max<size_t>(1, m) * 8) + 2 * al256(64 * Wp8 * 8) + al256(gf2cu::kCtrWords * 4);
+}
+gf2cu::PeerBufs peer_bufs_at(void* base, size_t m, size_t Wp8) {
+    char* c = static_cast<char*>(base);
+    const size_t a = al256(std::max<size_t>(1, m) * 8), st = al256(64 * Wp8 * 8);
+    gf2cu::PeerBufs b{};
+    b.pb[0] = reinterpret_cast<u64*>(c);
+    b.pb[1] = reinterpret_cast<u64*>(c + a);
+    b.pb2[0] = reinterpret_cast<u64*>(c + 2 * a);
+    b.pb2[1] = reinterpret_cast<u64*>(c + 3 * a);
+    b.stage[0] = reinterpret_cast<u64*>(c + 4 * a);
+    b.stage[1] = reinterpret_cast<u64*>(c + 4 * a + st);
+    b.ctr = reinterpret_cast<u32*>(c + 4 * a + 2 * st);
+    return b;
+}
+
+// Allocates rank k's local rows and replicated state (h.p) and its exchange
+// buffers (*xbuf, h.peer[k]); every allocation is appended to `allocs`.
+gf2cu_status peer_alloc_rank(gf2cu::PeerParams& h, std::vector<void*>& allocs, size_t m, size_t n,
+                             unsigned k, unsigned G, unsigned block, void** xbuf) {
+    const size_t W = words_of(n), Wp8 = wpad8(W), mn = std::max<size_t>(1, std::min(m, n));
+    auto alloc = [&](void** ptr, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+        if (e == cudaSuccess) allocs.push_back(*ptr);
+        return e;
+    };
+#define PA(ptr, bytes) CU_TRY(alloc(reinterpret_cast<void**>(&(ptr)), (bytes)))
+    h = gf2cu::PeerParams{};
+    gf2cu::Params& p = h.p;
+    h.m_loc = (u32)shard_rows(m, k, G, block);
+    h.rank = k;
+    h.nranks = G;
+    h.block = block;
+    PA(h.mat, (size_t)h.m_loc * Wp8 * 8);
+    PA(h.info[0], (size_t)h.m_loc * 16);
+    PA(h.info[1], (size_t)h.m_loc * 16);
+    PA(h.lo, (W + 1) * 4);
+    PA(p.perm, m * 4);
+    PA(p.inv, m * 4);
+    PA(p.state, sizeof(gf2cu::StepState));
+    PA(p.pout, sizeof(gf2cu::PanelOut));
+    PA(p.swaps, mn * 4);
+    PA(p.qcol, mn * 4);
+    PA(p.rhist, (W + 1) * 4);
+    PA(p.rbhist, (W + 1) * 4);
+    PA(p.sync, sizeof(gf2cu::SyncState));
+    PA(p.ap_claim, 2 * (W + 1) * 4);
+    p.ap_done = p.ap_claim + W + 1;
+    PA(*xbuf, peer_xbytes(m, Wp8));
+#undef PA
+    h.peer[k] = peer_bufs_at(*xbuf, m, Wp8);
+    const char* dv = std::getenv("GF2CU_PW_DIV");
+    p.pw_div = dv ? (u32)std::max(64, std::atoi(dv)) : 8192u;
+    p.m = (u32)m;
+    p.n = (u32)n;
+    p.W = (u32)W;
+    p.Wpad8 = (u32)Wp8;
+    return GF2CU_OK;
+}
+
+gf2cu_status peer_reset_rank(const gf2cu::PeerParams& h, cudaStream_t s) {
+    const size_t W = h.p.W;
+    CU_TRY(cudaMemsetAsync(h.p.sync, 0, sizeof(gf2cu::SyncState), s));
+    CU_TRY(cudaMemsetAsync(h.p.ap_claim, 0, 2 * (W + 1) * 4, s));
+    CU_TRY(cudaMemsetAsync(h.lo, 0xff, (W + 1) * 4, s));
+    CU_TRY(cudaMemsetAsync(h.peer[h.rank].ctr, 0, gf2cu::kCtrWords * 4, s));
+    return GF2CU_OK;
+}
+
+gf2cu_status peer_launch(const gf2cu::PeerParams* dp, unsigned ranks_here, unsigned cpr, size_t W,
+                         int device, cudaStream_t s) {
+    static bool attr_set[64] = {false};
+    if (device >= 0 && device < 64 && !attr_set[device]) {
+        CU_TRY(cudaFuncSetAttribute(gf2cu::ple_peer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    gf2cu::kTableBytes));
+        attr_set[device] = true;
+    }
+    u32 c = cpr, nsteps = (u32)W;
+    void* args[] = {(void*)&dp, &c, &nsteps};
+    CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_peer_kernel, dim3(cpr * ranks_here),
+                                       dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
+    return GF2CU_OK;
+}
+
+// The replicated outcome from one rank's state (after its kernel finished):
+// rank, swaps, q, canonical col_swaps, optional perm and stats.
+gf2cu_status peer_outputs(const gf2cu::PeerParams& h, cudaStream_t s, size_t* swaps, size_t* q,
+                          size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+                          uint32_t* perm, gf2cu_stats* stats) {
+    const size_t m = h.p.m, n = h.p.n, W = h.p.W;
+    u32 c[gf2cu::kCtrWords];
+    gf2cu::SyncState sy{};
+    gf2cu::StepState fin{};
+    CU_TRY(cudaMemcpyAsync(c, h.peer[h.rank].ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaMemcpyAsync(&sy, h.p.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaMemcpyAsync(&fin, h.p.state, sizeof(fin), cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    if (c[gf2cu::kCtrErr]) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
+    const size_t steps = std::min<size_t>(W, sy.panel_done);
+    const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
+    std::vector<u32> sw(rk), qq(rk), rh(steps), rbh(steps);
+    if (rk) {
+        CU_TRY(cudaMemcpyAsync(sw.data(), h.p.swaps, rk * 4, cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaMemcpyAsync(qq.data(), h.p.qcol, rk * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (steps) {
+        CU_TRY(cudaMemcpyAsync(rh.data(), h.p.rhist, steps * 4, cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaMemcpyAsync(rbh.data(), h.p.rbhist, steps * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (perm) CU_TRY(cudaMemcpyAsync(perm, h.p.perm, m * 4, cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    if (rank) *rank = rk;
+    size_t ncs = 0;
+    for (size_t i = 0; i < rk; ++i) {
+        if (swaps) swaps[i] = sw[i];
+        if (q) q[i] = qq[i];
+        if (qq[i] != i) {
+            if (col_swaps) col_swaps[ncs] = gf2cu_colswap{i, (size_t)qq[i], i};
+            ++ncs;
+        }
+    }
+    if (n_col_swaps) *n_col_swaps = ncs;
+    if (stats) {
+        stats->steps = steps;
+        double bytes = 0.0;
+        for (size_t w = 0; w < steps; ++w) {
+            if (rh[w] >= m || w + 1 >= W) continue;
+            ++stats->trailing_launches;
+            bytes += 16.0 * double(m - rh[w] - rbh[w]) * double(W - w - 1);
+        }
+        stats->alg_bytes = bytes;
+        stats->sweep_bytes = bytes;
+        stats->driver = 3;
+    }
+    return GF2CU_OK;
+}
+
 // The row-sharded driver (ple_peer.cuh) with G ranks emulated on this
 // matrix's device: one cooperative launch, sms/G CTAs per rank, every rank's
 // buffers in this device's memory (the peers' stores are ordinary stores).
@@ -261,8 +402,7 @@ size_t shard_rows(size_t m, size_t rank, size_t G, size_t block) {
 gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, size_t* swaps,
                           size_t* q, size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
                           gf2cu_stats* stats) {
-    const size_t m = a->m, n = a->n, W = a->W, Wp8 = wpad8(W);
-    const size_t mn = std::max<size_t>(1, std::min(m, n));
+    const size_t m = a->m, n = a->n, W = a->W;
     // 256-row blocks; small matrices get smaller ones so that every rank
     // owns rows (the result does not depend on the distribution)
     unsigned block = (unsigned)std::max<size_t>(1, std::min<size_t>(256, m / (2 * (size_t)std::max(1u, G))));
@@ -284,143 +424,50 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
         pw.G = G;
         pw.block = block;
         pw.hp.assign(G, gf2cu::PeerParams{});
-        auto alloc = [&](void** ptr, size_t bytes) -> cudaError_t {
-            cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
-            if (e == cudaSuccess) pw.allocs.push_back(*ptr);
-            return e;
-        };
-#define PA(ptr, bytes) CU_TRY(alloc(reinterpret_cast<void**>(&(ptr)), (bytes)))
         for (unsigned k = 0; k < G; ++k) {
-            gf2cu::PeerParams& h = pw.hp[k];
-            gf2cu::Params& p = h.p;
-            h.m_loc = (u32)shard_rows(m, k, G, block);
-            h.rank = k;
-            h.nranks = G;
-            h.block = block;
-            PA(h.mat, (size_t)h.m_loc * Wp8 * 8);
-            PA(h.info[0], (size_t)h.m_loc * 16);
-            PA(h.info[1], (size_t)h.m_loc * 16);
-            PA(h.lo, (W + 1) * 4);
-            PA(p.perm, m * 4);
-            PA(p.inv, m * 4);
-            PA(p.state, sizeof(gf2cu::StepState));
-            PA(p.pout, sizeof(gf2cu::PanelOut));
-            PA(p.swaps, mn * 4);
-            PA(p.qcol, mn * 4);
-            PA(p.rhist, (W + 1) * 4);
-            PA(p.rbhist, (W + 1) * 4);
-            PA(p.sync, sizeof(gf2cu::SyncState));
-            PA(p.ap_claim, 2 * (W + 1) * 4);
-            p.ap_done = p.ap_claim + W + 1;
-            gf2cu::PeerBufs& b = h.peer[k];
-            for (int x = 0; x < 2; ++x) {
-                PA(b.pb[x], m * 8);
-                PA(b.pb2[x], m * 8);
-                PA(b.stage[x], 64 * Wp8 * 8);
-            }
-            PA(b.ctr, gf2cu::kCtrWords * 4);
-            const char* dv = std::getenv("GF2CU_PW_DIV");
-            p.pw_div = dv ? (u32)std::max(64, std::atoi(dv)) : 8192u;
-            p.m = (u32)m;
-            p.n = (u32)n;
-            p.W = (u32)W;
-            p.Wpad8 = (u32)Wp8;
+            void* xbuf = nullptr;
+            gf2cu_status st = peer_alloc_rank(pw.hp[k], pw.allocs, m, n, k, G, block, &xbuf);
+            if (st != GF2CU_OK) return st;
         }
-#undef PA
         for (unsigned k = 0; k < G; ++k)
             for (unsigned j = 0; j < G; ++j) pw.hp[k].peer[j] = pw.hp[j].peer[j];
         CU_TRY(cudaMalloc(&pw.dp, G * sizeof(gf2cu::PeerParams)));
         CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
-        static bool attr_set[64] = {false};
-        if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
-            CU_TRY(cudaFuncSetAttribute(gf2cu::ple_peer_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, gf2cu::kTableBytes));
-            attr_set[a->device] = true;
-        }
     }
     for (unsigned k = 0; k < G; ++k) {
-        const gf2cu::PeerParams& h = pw.hp[k];
-        CU_TRY(cudaMemsetAsync(h.p.sync, 0, sizeof(gf2cu::SyncState), s));
-        CU_TRY(cudaMemsetAsync(h.p.ap_claim, 0, 2 * (W + 1) * 4, s));
-        CU_TRY(cudaMemsetAsync(h.lo, 0xff, (W + 1) * 4, s));
-        CU_TRY(cudaMemsetAsync(h.peer[k].ctr, 0, gf2cu::kCtrWords * 4, s));
+        gf2cu_status st = peer_reset_rank(pw.hp[k], s);
+        if (st != GF2CU_OK) return st;
     }
     gf2cu::peer_tile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
     CU_TRY(cudaGetLastError());
-    const u32 cpr = (u32)sms / G;
-    u32 nsteps = (u32)W;
-    void* args[] = {&pw.dp, (void*)&cpr, &nsteps};
     cudaEvent_t ev[2] = {nullptr, nullptr};
     if (timing) {
         CU_TRY(cudaEventCreate(&ev[0]));
         CU_TRY(cudaEventCreate(&ev[1]));
         CU_TRY(cudaEventRecord(ev[0], s));
     }
-    CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_peer_kernel, dim3(cpr * G),
-                                       dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
+    gf2cu_status st = peer_launch(pw.dp, G, (unsigned)sms / G, W, a->device, s);
+    if (st != GF2CU_OK) return st;
     if (timing) CU_TRY(cudaEventRecord(ev[1], s));
     gf2cu::peer_untile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
     CU_TRY(cudaGetLastError());
-
-    const gf2cu::PeerParams& h0 = pw.hp[0];
-    u32 err = 0;
-    for (unsigned k = 0; k < G; ++k) {
+    CU_TRY(cudaStreamSynchronize(s));
+    for (unsigned k = 1; k < G; ++k) {  // any rank's watchdog
         u32 c[gf2cu::kCtrWords];
-        CU_TRY(cudaMemcpyAsync(c, pw.hp[k].peer[k].ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
-        CU_TRY(cudaStreamSynchronize(s));
-        err |= c[gf2cu::kCtrErr];
+        CU_TRY(cudaMemcpy(c, pw.hp[k].peer[k].ctr, sizeof(c), cudaMemcpyDeviceToHost));
+        if (c[gf2cu::kCtrErr]) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
     }
-    if (err) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
-    gf2cu::SyncState sy{};
-    gf2cu::StepState fin{};
-    CU_TRY(cudaMemcpyAsync(&sy, h0.p.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
-    CU_TRY(cudaMemcpyAsync(&fin, h0.p.state, sizeof(fin), cudaMemcpyDeviceToHost, s));
-    CU_TRY(cudaStreamSynchronize(s));
-    const size_t steps = std::min<size_t>(W, sy.panel_done);
-    const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
-    std::vector<u32> sw(rk), qq(rk), rh(steps), rbh(steps);
-    if (rk) {
-        CU_TRY(cudaMemcpyAsync(sw.data(), h0.p.swaps, rk * 4, cudaMemcpyDeviceToHost, s));
-        CU_TRY(cudaMemcpyAsync(qq.data(), h0.p.qcol, rk * 4, cudaMemcpyDeviceToHost, s));
-    }
-    if (steps) {
-        CU_TRY(cudaMemcpyAsync(rh.data(), h0.p.rhist, steps * 4, cudaMemcpyDeviceToHost, s));
-        CU_TRY(cudaMemcpyAsync(rbh.data(), h0.p.rbhist, steps * 4, cudaMemcpyDeviceToHost, s));
-    }
-    CU_TRY(cudaStreamSynchronize(s));
-    *rank = rk;
-    size_t ncs = 0;
-    for (size_t i = 0; i < rk; ++i) {
-        swaps[i] = sw[i];
-        q[i] = qq[i];
-        if (qq[i] != i) {
-            if (col_swaps) col_swaps[ncs] = gf2cu_colswap{i, (size_t)qq[i], i};
-            ++ncs;
-        }
-    }
-    if (n_col_swaps) *n_col_swaps = ncs;
-    if (stats) {
-        stats->steps = steps;
-        double bytes = 0.0;
-        for (size_t w = 0; w < steps; ++w) {
-            if (rh[w] >= m || w + 1 >= W) continue;
-            ++stats->trailing_launches;
-            bytes += 16.0 * double(m - rh[w] - rbh[w]) * double(W - w - 1);
-        }
-        stats->alg_bytes = bytes;
-        stats->sweep_bytes = bytes;
-        stats->driver = 3;
-        if (timing) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev[0], ev[1]);
-            stats->kernel_ms = ms;
-        }
+    st = peer_outputs(pw.hp[0], s, swaps, q, rank, col_swaps, n_col_swaps, nullptr, stats);
+    if (st == GF2CU_OK && stats && timing) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[0], ev[1]);
+        stats->kernel_ms = ms;
     }
     if (timing) {
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
     }
-    return GF2CU_OK;
+    return st;
 }
 
 // Launches the whole decomposition on `s`; outputs are copied to the host.
@@ -1745,6 +1792,219 @@ gf2cu_status gf2cu_shard_finish(gf2cu_shard* s, size_t* swaps, size_t* q, size_t
     }
     *rank = rk;
     return GF2CU_OK;
+}
+
+// ------------------------------------------------------ row-sharded, peer
+}  // extern "C"
+
+struct gf2cu_peer {
+    size_t m = 0, n = 0, W = 0, Wp = 0, Wp8 = 0;
+    int device = 0;
+    u64* data = nullptr;  // local rows, row-major (stride Wp)
+    void* xbuf = nullptr; // this rank's exchange buffers (IPC-exported)
+    std::vector<void*> allocs;
+    std::vector<void*> opened;  // peers' exchange buffers mapped here
+    gf2cu::PeerParams hp{};
+    gf2cu::PeerParams* dp = nullptr;
+    bool connected = false;
+    cudaStream_t own = nullptr;
+};
+
+namespace {
+cudaStream_t peer_stream(gf2cu_peer* p, void* st) {
+    return st ? reinterpret_cast<cudaStream_t>(st) : p->own;
+}
+}  // namespace
+
+extern "C" {
+
+gf2cu_status gf2cu_peer_create(size_t m, size_t n, int rank, int nranks, size_t block, int device,
+                               gf2cu_peer** out) {
+    if (!out) return fail(GF2CU_EINVAL, "out is null");
+    *out = nullptr;
+    if (nranks < 1 || nranks > gf2cu::kMaxRanks || rank < 0 || rank >= nranks || block == 0)
+        return fail(GF2CU_EINVAL, "bad rank / nranks (1..8) / block");
+    if (m >= (1ull << 31) || n >= (1ull << 31)) return fail(GF2CU_EINVAL, "dimensions exceed 2^31");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(GF2CU_ENODEVICE, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(GF2CU_EINVAL, "bad device ordinal");
+    cudaDeviceProp pr;
+    CU_TRY(cudaGetDeviceProperties(&pr, device));
+    if (pr.major != 10) return fail(GF2CU_ENODEVICE, "device is not sm_100 (built for sm_100a only)");
+    DeviceGuard g(device);
+    apply_watchdog_env(device);
+    auto* p = new (std::nothrow) gf2cu_peer;
+    if (!p) return fail(GF2CU_ENOMEM, "host allocation failed");
+    p->m = m;
+    p->n = n;
+    p->W = words_of(n);
+    p->Wp = padded_stride(n);
+    p->Wp8 = wpad8(p->W);
+    p->device = device;
+    gf2cu_status st = peer_alloc_rank(p->hp, p->allocs, m, n, (unsigned)rank, (unsigned)nranks,
+                                      (unsigned)block, &p->xbuf);
+    cudaError_t e = cudaSuccess;
+    if (st == GF2CU_OK) {
+        const size_t bytes = std::max<size_t>(1, p->hp.m_loc) * p->Wp * 8;
+        e = cudaMalloc(&p->data, bytes);
+        if (e == cudaSuccess) e = cudaMemset(p->data, 0, bytes);
+        if (e == cudaSuccess) e = cudaMemset(p->xbuf, 0, peer_xbytes(m, p->Wp8));
+        if (e == cudaSuccess) e = cudaMalloc(&p->dp, sizeof(gf2cu::PeerParams));
+        if (e == cudaSuccess) e = cudaMemcpy(p->dp, &p->hp, sizeof(p->hp), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking);
+    }
+    if (st != GF2CU_OK || e != cudaSuccess) {
+        gf2cu_peer_destroy(p);
+        return st != GF2CU_OK ? st : cuda_fail(e, "gf2cu_peer_create");
+    }
+    p->connected = nranks == 1;
+    *out = p;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_destroy(gf2cu_peer* p) {
+    if (!p) return GF2CU_OK;
+    DeviceGuard g(p->device);
+    cudaDeviceSynchronize();
+    for (void* x : p->opened) cudaIpcCloseMemHandle(x);
+    for (void* x : p->allocs) cudaFree(x);
+    cudaFree(p->data);
+    cudaFree(p->dp);
+    if (p->own) cudaStreamDestroy(p->own);
+    delete p;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_info(const gf2cu_peer* p, size_t* m_local) {
+    if (!p) return fail(GF2CU_EINVAL, "null peer");
+    if (m_local) *m_local = p->hp.m_loc;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_export(const gf2cu_peer* p, void* handle) {
+    if (!p || !handle) return fail(GF2CU_EINVAL, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == GF2CU_PEER_HANDLE_BYTES, "IPC handle size");
+    DeviceGuard g(p->device);
+    cudaIpcMemHandle_t h;
+    CU_TRY(cudaIpcGetMemHandle(&h, p->xbuf));
+    std::memcpy(handle, &h, sizeof(h));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_connect(gf2cu_peer* p, const void* handles) {
+    if (!p || (!handles && p->hp.nranks > 1)) return fail(GF2CU_EINVAL, "null argument");
+    DeviceGuard g(p->device);
+    for (void* x : p->opened) cudaIpcCloseMemHandle(x);
+    p->opened.clear();
+    const unsigned G = p->hp.nranks, me = p->hp.rank;
+    for (unsigned j = 0; j < G; ++j) {
+        if (j == me) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char*>(handles) + (size_t)j * GF2CU_PEER_HANDLE_BYTES, sizeof(h));
+        void* ptr = nullptr;
+        CU_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        p->opened.push_back(ptr);
+        p->hp.peer[j] = peer_bufs_at(ptr, p->m, p->Wp8);
+    }
+    CU_TRY(cudaMemcpy(p->dp, &p->hp, sizeof(p->hp), cudaMemcpyHostToDevice));
+    p->connected = true;
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_upload(gf2cu_peer* p, const uint64_t* host, size_t host_stride, void* stream) {
+    if (!p || (!host && p->hp.m_loc)) return fail(GF2CU_EINVAL, "null argument");
+    if (host_stride < p->W) return fail(GF2CU_EINVAL, "host stride smaller than the row");
+    if (!p->hp.m_loc || !p->W) return GF2CU_OK;
+    DeviceGuard g(p->device);
+    cudaStream_t st = peer_stream(p, stream);
+    CU_TRY(cudaMemcpy2DAsync(p->data, p->Wp * 8, host, host_stride * 8, p->W * 8, p->hp.m_loc,
+                             cudaMemcpyHostToDevice, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_download(const gf2cu_peer* p, uint64_t* host, size_t host_stride, void* stream) {
+    if (!p || (!host && p->hp.m_loc)) return fail(GF2CU_EINVAL, "null argument");
+    if (host_stride < p->W) return fail(GF2CU_EINVAL, "host stride smaller than the row");
+    if (!p->hp.m_loc || !p->W) return GF2CU_OK;
+    DeviceGuard g(p->device);
+    cudaStream_t st = peer_stream(const_cast<gf2cu_peer*>(p), stream);
+    CU_TRY(cudaMemcpy2DAsync(host, host_stride * 8, p->data, p->Wp * 8, p->W * 8, p->hp.m_loc,
+                             cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_fill_ctr(gf2cu_peer* p, uint64_t seed, void* stream) {
+    if (!p) return fail(GF2CU_EINVAL, "null peer");
+    if (!p->hp.m_loc) return GF2CU_OK;
+    DeviceGuard g(p->device);
+    cudaStream_t st = peer_stream(p, stream);
+    gf2cu::shard_fill_ctr_kernel<<<num_sms(p->device) * 8, 256, 0, st>>>(
+        p->data, p->hp.m_loc, (u32)p->n, (u32)p->Wp, p->hp.rank, p->hp.nranks, p->hp.block, seed);
+    CU_TRY(cudaGetLastError());
+    CU_TRY(cudaStreamSynchronize(st));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_reset(gf2cu_peer* p, void* stream) {
+    if (!p) return fail(GF2CU_EINVAL, "null peer");
+    DeviceGuard g(p->device);
+    cudaStream_t st = peer_stream(p, stream);
+    gf2cu_status s2 = peer_reset_rank(p->hp, st);
+    if (s2 != GF2CU_OK) return s2;
+    CU_TRY(cudaStreamSynchronize(st));
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_peer_run(gf2cu_peer* p, void* stream, gf2cu_stats* stats) {
+    if (!p) return fail(GF2CU_EINVAL, "null peer");
+    if (!p->connected) return fail(GF2CU_EINVAL, "gf2cu_peer_connect has not been called");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (p->m == 0 || p->n == 0) return GF2CU_OK;
+    DeviceGuard g(p->device);
+    cudaStream_t st = peer_stream(p, stream);
+    const int sms = num_sms(p->device);
+    if (p->hp.m_loc)
+        gf2cu::tile_kernel<<<sms * 8, 256, 0, st>>>(p->data, p->hp.mat, p->hp.m_loc, (u32)p->Wp,
+                                                   (u32)p->Wp8);
+    CU_TRY(cudaGetLastError());
+    cudaEvent_t ev[2];
+    CU_TRY(cudaEventCreate(&ev[0]));
+    CU_TRY(cudaEventCreate(&ev[1]));
+    CU_TRY(cudaEventRecord(ev[0], st));
+    gf2cu_status s2 = peer_launch(p->dp, 1, (unsigned)sms, p->W, p->device, st);
+    if (s2 == GF2CU_OK) {
+        CU_TRY(cudaEventRecord(ev[1], st));
+        if (p->hp.m_loc)
+            gf2cu::untile_kernel<<<sms * 8, 256, 0, st>>>(p->hp.mat, p->data, nullptr, p->hp.m_loc,
+                                                         (u32)p->Wp, (u32)p->Wp8);
+        CU_TRY(cudaGetLastError());
+        CU_TRY(cudaStreamSynchronize(st));
+        s2 = peer_outputs(p->hp, st, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, stats);
+        if (s2 == GF2CU_OK && stats) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[0], ev[1]);
+            stats->kernel_ms = ms;
+        }
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    return s2;
+}
+
+gf2cu_status gf2cu_peer_finish(gf2cu_peer* p, size_t* swaps, size_t* q, size_t* rank, uint32_t* perm,
+                               void* stream) {
+    if (!p || !rank || !perm || ((!swaps || !q) && std::min(p->m, p->n) > 0))
+        return fail(GF2CU_EINVAL, "null argument");
+    *rank = 0;
+    if (p->m == 0 || p->n == 0) {
+        for (size_t i = 0; i < p->m; ++i) perm[i] = (uint32_t)i;
+        return GF2CU_OK;
+    }
+    DeviceGuard g(p->device);
+    return peer_outputs(p->hp, peer_stream(p, stream), swaps, q, rank, nullptr, nullptr, perm, nullptr);
 }
 
 gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t stride, double density,

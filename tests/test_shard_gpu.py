@@ -88,3 +88,50 @@ def test_sharded_device_engine(world, backend, case, block):
         assert np.array_equal(swaps, want.swaps.astype(np.uint64))
         assert np.array_equal(qq, want.q.astype(np.uint64))
         assert np.array_equal(full, ref), f"rank {rk}"
+
+
+def _peer_worker(port, case, block, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1111_6549_b200.peer import peer_block_iterative_ple
+        a, m, n = _make(case)
+        res, full = peer_block_iterative_ple(a, m, n, block=block)
+        q.put((0, res.rank, res.swaps, res.q, full))
+    except Exception:
+        import traceback
+        q.put((0, "error", traceback.format_exc(), None, None))
+        os._exit(1)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,block", [("dense", 256), ("sparse", 64), ("deficient", 32), ("big", 256)])
+def test_peer_multiprocess_api_world1(case, block):
+    """The multi-process device-driven path (gf2cu_peer_*: create, handle
+    exchange, reset, barrier, persistent kernel, finish, assembly) at
+    world_size 1 over NCCL -- one GPU is all a test may use; more ranks run
+    in the one-GPU emulation (peer_ranks tests)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_peer_worker, args=(_free_port(), case, block, q))
+    p.start()
+    try:
+        o = q.get(timeout=240)
+        assert o[1] != "error", o[2]
+    finally:
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
+    assert p.exitcode == 0
+    a, m, n = _make(case)
+    ref = a.copy()
+    want = O.ple(ref, m, n)
+    _, rank, swaps, qq, full = o
+    assert rank == want.rank
+    assert np.array_equal(swaps, want.swaps.astype(np.uint64))
+    assert np.array_equal(qq, want.q.astype(np.uint64))
+    assert np.array_equal(full, ref)
