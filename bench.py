@@ -23,9 +23,11 @@ cpu_baseline = the reference itself (oracle/_ref/libgf2ref.so, compiled from
              same matrix), rank 0 at N=1 only.
 
 --impl reference runs that reference arm alone (rank 0; other ranks exit 0).
-Multi-GPU (torchrun, N>1): weak-scaling replicas -- each rank factors its own
-65536^2 instance (the sharded 131072^2 path is not benchmarked
-here); value is the total over ranks / max-over-ranks time.
+Multi-GPU (torchrun, N>1): the device-driven row-sharded PLE (peer.py,
+csrc/ple_peer.cuh) on the weak-scaling size n = 65536 * N^(1/3) (N = 8 is
+BASELINE config 5's 131072^2); value = the matrix's algorithmic bytes / the
+max-over-ranks device time. --host-sharded: the NCCL host-orchestrated path;
+--replicas: independent single-GPU instances.
 """
 from __future__ import annotations
 
@@ -506,6 +508,115 @@ def gpu_sharded_arm(args, rank, world, local_rank):
     dist.destroy_process_group()
 
 
+def gpu_peer_arm(args, rank, world, local_rank):
+    """N > 1 (default): the device-driven row-sharded PLE (peer.py, kernel
+    csrc/ple_peer.cuh): one process and ONE persistent kernel per GPU for the
+    whole factorization, the ranks exchanging the panel column and pivot-row
+    tails through NVLink peer memory (CUDA IPC) with device-side counters --
+    no host call or collective per step. Weak scaling: n = 65536 * N^(1/3)
+    (N = 8 is BASELINE config 5's 131072^2)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1111_6549_b200.peer import PeerEngine, exchange_handles
+
+    torch.cuda.set_device(local_rank)
+    if "RANK" not in os.environ:  # --sharded at N=1 without torchrun
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29563")
+        os.environ["RANK"], os.environ["WORLD_SIZE"] = "0", "1"
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    n = args.n if args.n != N_DEFAULT else weak_n(world)
+    m = n
+    stream = torch.cuda.current_stream()
+    eng = PeerEngine(m, n, rank, world, block=256, device=local_rank, stream=stream.cuda_stream)
+    exchange_handles(eng, dist)
+    kernel_ms = []
+
+    def one():
+        eng.fill_ctr(SEED)  # the input, regenerated on the device (counted)
+        eng.reset()
+        dist.barrier()
+        st = eng.run()
+        kernel_ms.append(st["kernel_ms"])
+        return st
+
+    st = None
+    for _ in range(args.warmup):
+        st = one()
+    kernel_ms.clear()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        st = one()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    res = eng.finish()
+    bytes_per_step = float(st["alg_bytes"])
+    # e2e: each rank's rows in from pinned host memory, its L\E rows back out
+    Wd = (n + 63) // 64
+    host_in = torch.empty((max(1, eng.m_local), Wd), dtype=torch.int64, pin_memory=True)
+    eng.fill_ctr(SEED)
+    host_in_np = host_in.numpy().view(np.uint64)
+    eng.download(host_in_np)
+    t_e2e = 0.0
+    e2e_steps = max(1, min(args.steps, 2))
+    for _ in range(e2e_steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.upload(host_in_np[: eng.m_local])
+        eng.reset()
+        dist.barrier()
+        eng.run()
+        out2 = eng.finish()  # replicated outcome + this rank's rows to the host
+        torch.cuda.synchronize()
+        t_e2e += time.perf_counter() - t0
+        assert out2.rank == res.rank
+    vals = torch.tensor([dev_ms, t_e2e, max(kernel_ms)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    max_ms, e2e_max_s, kmax = float(vals[0]), float(vals[1]), float(vals[2])
+    if rank == 0:
+        value = bytes_per_step * args.steps / (max_ms * 1e-3) / 1e9
+        peak, peak_kind = load_peaks()
+        per_gpu_kernel = bytes_per_step / world / (kmax * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"block_iterative_ple {m}x{n} row-sharded over {world} GPUs "
+                                   f"(weak scaling: n = 65536*N^(1/3); N=8 is BASELINE config 5's 131072^2)",
+                       "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "rank": int(res.rank),
+                       "panel_bits": 64,
+                       "parallelism": f"row-sharded x{world} (block-cyclic 256-row blocks), one persistent "
+                                      "kernel per GPU, NVLink peer-memory exchange (ple_peer.cuh)",
+                       "l2": "per-GPU shard > 126 MB L2; input regenerated on the device each step (counted)"},
+            "e2e": {"value": round(bytes_per_step * e2e_steps / e2e_max_s / 1e9, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": int(m * Wd * 8), "d2h_bytes_per_step": int(m * Wd * 8),
+                    "steps": e2e_steps},
+            "roofline": {"kernel": "ple_peer_kernel", "bound": "hbm",
+                         "achieved": round(per_gpu_kernel, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(per_gpu_kernel / peak, 4), "traffic": None,
+                         "avg_launch_ms": round(kmax, 3),
+                         "note": "per GPU: the matrix's algorithmic bytes / N over the slowest rank's kernel",
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+            "cpu_baseline": None,
+            "clocks": clk,
+            "gpu_launches": 4 * args.steps,
+        }))
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -518,6 +629,9 @@ def main():
                     help="use the row-sharded PLE even at N=1 (testing)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent single-GPU replicas instead of the row-sharded PLE")
+    ap.add_argument("--host-sharded", action="store_true",
+                    help="the host-orchestrated row-sharded path (shard.py, NCCL collectives per "
+                         "step) instead of the device-driven one (peer.py)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -526,7 +640,10 @@ def main():
         reference_arm(args, rank)
         return
     if (world > 1 and not args.replicas) or args.sharded:
-        gpu_sharded_arm(args, rank, world, local_rank)
+        if args.host_sharded:
+            gpu_sharded_arm(args, rank, world, local_rank)
+        else:
+            gpu_peer_arm(args, rank, world, local_rank)
         return
     gpu_arm(args, rank, world, local_rank)
 

@@ -33,8 +33,10 @@ from .shard import ShardResult, assemble, local_rows
 class PeerEngine:
     """One rank's rows and exchange buffers (C ABI gf2cu_peer_*)."""
 
-    def __init__(self, m: int, n: int, rank: int, nranks: int, block: int = 256, device: int = 0):
+    def __init__(self, m: int, n: int, rank: int, nranks: int, block: int = 256, device: int = 0,
+                 stream: Optional[int] = None):
         L = _lib.load()
+        self.stream = stream  # cudaStream_t as an int (None: the library's own stream)
         self.L = L
         self.m, self.n, self.rank, self.nranks, self.block = m, n, rank, nranks, block
         self.W = (n + 63) // 64
@@ -46,6 +48,9 @@ class PeerEngine:
         check(L.gf2cu_peer_info(h, C.byref(ml)))
         self.m_local = ml.value
         self.last_stats = {}
+
+    def _s(self):
+        return C.c_void_p(self.stream) if self.stream else None
 
     def close(self):
         if getattr(self, "h", None):
@@ -73,19 +78,24 @@ class PeerEngine:
     def upload(self, words: np.ndarray) -> None:
         words = np.ascontiguousarray(words, dtype=np.uint64)
         check(self.L.gf2cu_peer_upload(self.h, words.ctypes.data_as(C.POINTER(C.c_uint64)),
-                                       words.shape[1] if words.ndim == 2 else 1, None))
+                                       words.shape[1] if words.ndim == 2 else 1, self._s()))
 
     def fill_ctr(self, seed: int) -> None:
-        check(self.L.gf2cu_peer_fill_ctr(self.h, C.c_uint64(seed), None))
+        check(self.L.gf2cu_peer_fill_ctr(self.h, C.c_uint64(seed), self._s()))
 
     def reset(self) -> None:
-        check(self.L.gf2cu_peer_reset(self.h, None))
+        check(self.L.gf2cu_peer_reset(self.h, self._s()))
 
     def run(self) -> dict:
         st = gf2cu_stats()
-        check(self.L.gf2cu_peer_run(self.h, None, C.byref(st)))
+        check(self.L.gf2cu_peer_run(self.h, self._s(), C.byref(st)))
         self.last_stats = {f: getattr(st, f) for f, _ in gf2cu_stats._fields_}
         return self.last_stats
+
+    def download(self, out: np.ndarray) -> None:
+        """This rank's rows (local order) into `out` (m_local x >= W words)."""
+        check(self.L.gf2cu_peer_download(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), out.shape[1],
+                                         self._s()))
 
     def finish(self) -> ShardResult:
         cap = max(1, min(self.m, self.n))
@@ -95,10 +105,10 @@ class PeerEngine:
         rank = C.c_size_t()
         szp = C.POINTER(C.c_size_t)
         check(self.L.gf2cu_peer_finish(self.h, swaps.ctypes.data_as(szp), q.ctypes.data_as(szp),
-                                       C.byref(rank), perm.ctypes.data_as(C.POINTER(C.c_uint32)), None))
+                                       C.byref(rank), perm.ctypes.data_as(C.POINTER(C.c_uint32)), self._s()))
         Wd = max(1, self.W)
         loc = np.zeros((max(1, self.m_local), Wd), dtype=np.uint64)
-        check(self.L.gf2cu_peer_download(self.h, loc.ctypes.data_as(C.POINTER(C.c_uint64)), Wd, None))
+        check(self.L.gf2cu_peer_download(self.h, loc.ctypes.data_as(C.POINTER(C.c_uint64)), Wd, self._s()))
         r = int(rank.value)
         return ShardResult(r, swaps[:r].astype(np.uint64), q[:r].astype(np.uint64),
                            perm[: self.m].astype(np.int64), loc[: self.m_local])
