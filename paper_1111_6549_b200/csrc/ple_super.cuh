@@ -35,6 +35,14 @@ __device__ __forceinline__ u64* tw4(u64* mat, u32 m, u32 row, u32 x) {
     return mat + ((((size_t)(x >> 2) * m + row) << 2) + (x & 3u));
 }
 
+// The physical-row array that follows the m sweep records {d~_a, d_b}.
+__device__ __forceinline__ u32* info_phys(ulonglong2* info, u32 m) {
+    return reinterpret_cast<u32*>(info + m);
+}
+__device__ __forceinline__ const u32* info_phys(const ulonglong2* info, u32 m) {
+    return reinterpret_cast<const u32*>(info + m);
+}
+
 // row-major (stride Wp) -> 32-byte tiles (Wpad4 words per row)
 __global__ void tile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst, u32 m, u32 Wp,
                              u32 Wpad4) {
@@ -134,7 +142,9 @@ __device__ __forceinline__ void compress_write(u64* mat, u32 m, u32 ph, u32 r0, 
 
 // Apply both panels of super-step (w, w+1) to the rows at positions
 // [lo, hi): multipliers, compressed words, and the sweep record
-// info[2 pos] = {d~_a, d_b}, info[2 pos + 1] = {physical row, 0}.
+// info[pos] = {d~_a, d_b}, and the physical row in the u32 array that
+// follows the m records (info_phys): dense records keep the sweep's loads of
+// them at 2 + 1 L1 wavefronts per warp (the sweep is L1-bound).
 __device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2& s, u32 w, u32 r,
                                             u32 rba, u32 rbb, bool has_b, u32 lo, u32 hi, u32 tid,
                                             u32 nthr) {
@@ -197,8 +207,8 @@ __device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2&
                 }
             }
         }
-        p.info[2u * pos] = make_ulonglong2(dta, db);
-        p.info[2u * pos + 1u] = make_ulonglong2((u64)ph, 0ull);
+        p.info[pos] = make_ulonglong2(dta, db);
+        info_phys(p.info, p.m)[pos] = ph;
     }
 }
 
@@ -253,11 +263,11 @@ __device__ __forceinline__ void build16(const Params& p, unsigned char* smem, u3
 
 constexpr u32 kRows16 = kTrailThreads / 2 * kUnroll;  // 1024 rows per iteration
 
-__device__ __forceinline__ void ld_info2(const ulonglong2* info, u32 pos, bool valid, ulonglong2& d,
-                                         u32& ph) {
+__device__ __forceinline__ void ld_info2(const ulonglong2* info, u32 m, u32 pos, bool valid,
+                                         ulonglong2& d, u32& ph) {
     if (valid) {
-        d = ldcg(info + 2u * pos);
-        ph = (u32)ldcg(info + 2u * pos + 1u).x;
+        d = ldcg(info + pos);
+        ph = ldcg(info_phys(info, m) + pos);
     } else {
         d = make_ulonglong2(0ull, 0ull);
         ph = 0u;
@@ -284,12 +294,12 @@ __device__ __forceinline__ void trail16_rows(const Params& p, const unsigned cha
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
         const u32 ri = row0 + lane_row + (u32)k * (kTrailThreads / 2);
-        ld_info2(p.info, r + ri, ri < rend, dC[k], pC[k]);
+        ld_info2(p.info, p.m, r + ri, ri < rend, dC[k], pC[k]);
     }
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
         const u32 ri = row0 + kRows16 + lane_row + (u32)k * (kTrailThreads / 2);
-        ld_info2(p.info, r + ri, ri < rend, dN[k], pN[k]);
+        ld_info2(p.info, p.m, r + ri, ri < rend, dN[k], pN[k]);
     }
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
@@ -312,7 +322,7 @@ __device__ __forceinline__ void trail16_rows(const Params& p, const unsigned cha
 #pragma unroll
         for (int k = 0; k < kUnroll; ++k) {
             const u32 ri = base + 2u * kRows16 + lane_row + (u32)k * (kTrailThreads / 2);
-            ld_info2(p.info, r + ri, ri < rend, dNN[k], pNN[k]);
+            ld_info2(p.info, p.m, r + ri, ri < rend, dNN[k], pNN[k]);
         }
 #pragma unroll
         for (int k = 0; k < kUnroll; ++k) {
