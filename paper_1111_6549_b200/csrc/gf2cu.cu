@@ -23,6 +23,7 @@
 #include "ple_super.cuh"
 #include "ple_shard.cuh"
 #include "ple_peer.cuh"
+#include "ple_peer_super.cuh"
 #include "rref_kernels.cuh"
 #include "gemm_kernels.cuh"
 
@@ -257,12 +258,13 @@ size_t shard_rows(size_t m, size_t rank, size_t G, size_t block) {
 // One rank's exchange buffers (ple_peer.cuh PeerBufs) live in ONE allocation
 // so a single IPC handle maps them: pb[2], pb2[2], stage[2], counters.
 size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+// (the stage holds 128 pivot rows: the super-step form's two panels)
 size_t peer_xbytes(size_t m, size_t Wp8) {
-    return 4 * al256(std::max<size_t>(1, m) * 8) + 2 * al256(64 * Wp8 * 8) + al256(gf2cu::kCtrWords * 4);
+    return 4 * al256(std::max<size_t>(1, m) * 8) + 2 * al256(128 * Wp8 * 8) + al256(gf2cu::kCtrWords * 4);
 }
 gf2cu::PeerBufs peer_bufs_at(void* base, size_t m, size_t Wp8) {
     char* c = static_cast<char*>(base);
-    const size_t a = al256(std::max<size_t>(1, m) * 8), st = al256(64 * Wp8 * 8);
+    const size_t a = al256(std::max<size_t>(1, m) * 8), st = al256(128 * Wp8 * 8);
     gf2cu::PeerBufs b{};
     b.pb[0] = reinterpret_cast<u64*>(c);
     b.pb[1] = reinterpret_cast<u64*>(c + a);
@@ -294,6 +296,10 @@ gf2cu_status peer_alloc_rank(gf2cu::PeerParams& h, std::vector<void*>& allocs, s
     PA(h.mat, (size_t)h.m_loc * Wp8 * 8);
     PA(h.info[0], (size_t)h.m_loc * 16);
     PA(h.info[1], (size_t)h.m_loc * 16);
+    PA(h.ipos[0], (size_t)h.m_loc * 4);
+    PA(h.ipos[1], (size_t)h.m_loc * 4);
+    PA(h.pout_b, sizeof(gf2cu::PanelOut));
+    PA(h.so, sizeof(gf2cu::SuperOut));
     PA(h.lo, (W + 1) * 4);
     PA(p.perm, m * 4);
     PA(p.inv, m * 4);
@@ -327,25 +333,36 @@ gf2cu_status peer_reset_rank(const gf2cu::PeerParams& h, cudaStream_t s) {
     return GF2CU_OK;
 }
 
+// Two panels per sweep (ple_peer_super.cuh) on the same size rule as the
+// single-GPU drivers (run_ple), unless forced by flags or GF2CU_PEER_SUPER.
+bool peer_super(size_t m, size_t W, unsigned flags) {
+    if (const char* e = std::getenv("GF2CU_PEER_SUPER")) return std::atoi(e) != 0;
+    if (flags & GF2CU_FLAG_SINGLE_PANEL) return false;
+    return (flags & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= 16777216.0;
+}
+
 gf2cu_status peer_launch(const gf2cu::PeerParams* dp, unsigned ranks_here, unsigned cpr, size_t W,
-                         int device, cudaStream_t s) {
+                         bool super, int device, cudaStream_t s) {
     static bool attr_set[64] = {false};
     if (device >= 0 && device < 64 && !attr_set[device]) {
         CU_TRY(cudaFuncSetAttribute(gf2cu::ple_peer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     gf2cu::kTableBytes));
+        CU_TRY(cudaFuncSetAttribute(gf2cu::ple_peer_super_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, gf2cu::kTableBytes));
         attr_set[device] = true;
     }
-    u32 c = cpr, nsteps = (u32)W;
+    u32 c = cpr, nsteps = super ? (u32)((W + 1) / 2) : (u32)W;
     void* args[] = {(void*)&dp, &c, &nsteps};
-    CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_peer_kernel, dim3(cpr * ranks_here),
-                                       dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
+    void* fn = super ? (void*)gf2cu::ple_peer_super_kernel : (void*)gf2cu::ple_peer_kernel;
+    CU_TRY(cudaLaunchCooperativeKernel(fn, dim3(cpr * ranks_here), dim3(gf2cu::kTrailThreads), args,
+                                       gf2cu::kTableBytes, s));
     return GF2CU_OK;
 }
 
 // The replicated outcome from one rank's state (after its kernel finished):
 // rank, swaps, q, canonical col_swaps, optional perm and stats.
-gf2cu_status peer_outputs(const gf2cu::PeerParams& h, cudaStream_t s, size_t* swaps, size_t* q,
-                          size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
+gf2cu_status peer_outputs(const gf2cu::PeerParams& h, bool super, cudaStream_t s, size_t* swaps,
+                          size_t* q, size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
                           uint32_t* perm, gf2cu_stats* stats) {
     const size_t m = h.p.m, n = h.p.n, W = h.p.W;
     u32 c[gf2cu::kCtrWords];
@@ -356,7 +373,7 @@ gf2cu_status peer_outputs(const gf2cu::PeerParams& h, cudaStream_t s, size_t* sw
     CU_TRY(cudaMemcpyAsync(&fin, h.p.state, sizeof(fin), cudaMemcpyDeviceToHost, s));
     CU_TRY(cudaStreamSynchronize(s));
     if (c[gf2cu::kCtrErr]) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
-    const size_t steps = std::min<size_t>(W, sy.panel_done);
+    const size_t steps = std::min<size_t>(W, super ? 2 * (size_t)sy.panel_done : (size_t)sy.panel_done);
     const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
     std::vector<u32> sw(rk), qq(rk), rh(steps), rbh(steps);
     if (rk) {
@@ -389,8 +406,18 @@ gf2cu_status peer_outputs(const gf2cu::PeerParams& h, cudaStream_t s, size_t* sw
             bytes += 16.0 * double(m - rh[w] - rbh[w]) * double(W - w - 1);
         }
         stats->alg_bytes = bytes;
-        stats->sweep_bytes = bytes;
-        stats->driver = 3;
+        double sweep = bytes;
+        if (super) {  // one read + write per two panels (as run_ple)
+            sweep = 0.0;
+            for (size_t w = 0; w + 2 < W && w < steps; w += 2) {
+                if (rh[w] >= m) continue;
+                const size_t rbb = (w + 1 < steps) ? rbh[w + 1] : 0;
+                const size_t done = std::min(m, (size_t)rh[w] + rbh[w] + rbb);
+                sweep += 16.0 * double(m - done) * double(W - w - 2);
+            }
+        }
+        stats->sweep_bytes = sweep;
+        stats->driver = super ? 4 : 3;
     }
     return GF2CU_OK;
 }
@@ -434,11 +461,20 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
         CU_TRY(cudaMalloc(&pw.dp, G * sizeof(gf2cu::PeerParams)));
         CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
     }
+    const bool super = peer_super(m, W, cfg ? cfg->flags : 0u);
+    const u32 wpad = super ? (u32)std::max<size_t>(4, (W + 3) / 4 * 4) : (u32)wpad8(W);
+    if (pw.hp[0].p.Wpad8 != wpad) {
+        for (unsigned k = 0; k < G; ++k) pw.hp[k].p.Wpad8 = wpad;
+        CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
+    }
     for (unsigned k = 0; k < G; ++k) {
         gf2cu_status st = peer_reset_rank(pw.hp[k], s);
         if (st != GF2CU_OK) return st;
     }
-    gf2cu::peer_tile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
+    if (super)
+        gf2cu::peer_tile4_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
+    else
+        gf2cu::peer_tile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
     CU_TRY(cudaGetLastError());
     cudaEvent_t ev[2] = {nullptr, nullptr};
     if (timing) {
@@ -446,10 +482,13 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
         CU_TRY(cudaEventCreate(&ev[1]));
         CU_TRY(cudaEventRecord(ev[0], s));
     }
-    gf2cu_status st = peer_launch(pw.dp, G, (unsigned)sms / G, W, a->device, s);
+    gf2cu_status st = peer_launch(pw.dp, G, (unsigned)sms / G, W, super, a->device, s);
     if (st != GF2CU_OK) return st;
     if (timing) CU_TRY(cudaEventRecord(ev[1], s));
-    gf2cu::peer_untile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
+    if (super)
+        gf2cu::peer_untile4_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
+    else
+        gf2cu::peer_untile_kernel<<<dim3(sms * 4, G), 256, 0, s>>>(pw.dp, a->data, (u32)a->Wp);
     CU_TRY(cudaGetLastError());
     CU_TRY(cudaStreamSynchronize(s));
     for (unsigned k = 1; k < G; ++k) {  // any rank's watchdog
@@ -457,7 +496,7 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
         CU_TRY(cudaMemcpy(c, pw.hp[k].peer[k].ctr, sizeof(c), cudaMemcpyDeviceToHost));
         if (c[gf2cu::kCtrErr]) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
     }
-    st = peer_outputs(pw.hp[0], s, swaps, q, rank, col_swaps, n_col_swaps, nullptr, stats);
+    st = peer_outputs(pw.hp[0], super, s, swaps, q, rank, col_swaps, n_col_swaps, nullptr, stats);
     if (st == GF2CU_OK && stats && timing) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[0], ev[1]);
@@ -1807,6 +1846,7 @@ struct gf2cu_peer {
     gf2cu::PeerParams hp{};
     gf2cu::PeerParams* dp = nullptr;
     bool connected = false;
+    bool super = false;  // the last run used two panels per sweep
     cudaStream_t own = nullptr;
 };
 
@@ -1966,23 +2006,37 @@ gf2cu_status gf2cu_peer_run(gf2cu_peer* p, void* stream, gf2cu_stats* stats) {
     DeviceGuard g(p->device);
     cudaStream_t st = peer_stream(p, stream);
     const int sms = num_sms(p->device);
-    if (p->hp.m_loc)
-        gf2cu::tile_kernel<<<sms * 8, 256, 0, st>>>(p->data, p->hp.mat, p->hp.m_loc, (u32)p->Wp,
-                                                   (u32)p->Wp8);
+    p->super = peer_super(p->m, p->W, 0u);
+    const u32 wpad = p->super ? (u32)std::max<size_t>(4, (p->W + 3) / 4 * 4) : (u32)p->Wp8;
+    if (p->hp.p.Wpad8 != wpad) {
+        p->hp.p.Wpad8 = wpad;
+        CU_TRY(cudaMemcpy(p->dp, &p->hp, sizeof(p->hp), cudaMemcpyHostToDevice));
+    }
+    if (p->hp.m_loc) {
+        if (p->super)
+            gf2cu::tile4_kernel<<<sms * 8, 256, 0, st>>>(p->data, p->hp.mat, p->hp.m_loc, (u32)p->Wp, wpad);
+        else
+            gf2cu::tile_kernel<<<sms * 8, 256, 0, st>>>(p->data, p->hp.mat, p->hp.m_loc, (u32)p->Wp, wpad);
+    }
     CU_TRY(cudaGetLastError());
     cudaEvent_t ev[2];
     CU_TRY(cudaEventCreate(&ev[0]));
     CU_TRY(cudaEventCreate(&ev[1]));
     CU_TRY(cudaEventRecord(ev[0], st));
-    gf2cu_status s2 = peer_launch(p->dp, 1, (unsigned)sms, p->W, p->device, st);
+    gf2cu_status s2 = peer_launch(p->dp, 1, (unsigned)sms, p->W, p->super, p->device, st);
     if (s2 == GF2CU_OK) {
         CU_TRY(cudaEventRecord(ev[1], st));
-        if (p->hp.m_loc)
-            gf2cu::untile_kernel<<<sms * 8, 256, 0, st>>>(p->hp.mat, p->data, nullptr, p->hp.m_loc,
-                                                         (u32)p->Wp, (u32)p->Wp8);
+        if (p->hp.m_loc) {
+            if (p->super)
+                gf2cu::untile4_local_kernel<<<sms * 8, 256, 0, st>>>(p->hp.mat, p->data, p->hp.m_loc,
+                                                                    (u32)p->Wp, wpad);
+            else
+                gf2cu::untile_kernel<<<sms * 8, 256, 0, st>>>(p->hp.mat, p->data, nullptr, p->hp.m_loc,
+                                                             (u32)p->Wp, wpad);
+        }
         CU_TRY(cudaGetLastError());
         CU_TRY(cudaStreamSynchronize(st));
-        s2 = peer_outputs(p->hp, st, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, stats);
+        s2 = peer_outputs(p->hp, p->super, st, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, stats);
         if (s2 == GF2CU_OK && stats) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, ev[0], ev[1]);
@@ -2004,7 +2058,8 @@ gf2cu_status gf2cu_peer_finish(gf2cu_peer* p, size_t* swaps, size_t* q, size_t* 
         return GF2CU_OK;
     }
     DeviceGuard g(p->device);
-    return peer_outputs(p->hp, peer_stream(p, stream), swaps, q, rank, nullptr, nullptr, perm, nullptr);
+    return peer_outputs(p->hp, p->super, peer_stream(p, stream), swaps, q, rank, nullptr, nullptr, perm,
+                        nullptr);
 }
 
 gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t stride, double density,

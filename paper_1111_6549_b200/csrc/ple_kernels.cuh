@@ -445,7 +445,9 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
     __syncthreads();
     if (sh.super == 1 && !sh.cap_ok) {
         // panel a reads its window from the previous super-step's capture
-        if (threadIdx.x == 0) sh.cap_ok = spin_geq(la->cap_ctr, la->cap_target, la->err) ? 1 : -1;
+        if (threadIdx.x == 0)
+            sh.cap_ok = (la->sys ? spin_geq_sys(la->cap_ctr, la->cap_target, la->err)
+                                 : spin_geq(la->cap_ctr, la->cap_target, la->err)) ? 1 : -1;
         __syncthreads();
     }
     const u32 r = sh.r;

@@ -51,10 +51,16 @@ constexpr int kCtrSt = 2;   // +1 per rank per step: its pivots' remaining tiles
 constexpr int kCtrErr = 3;  // watchdog tripped somewhere (set on every rank)
 constexpr int kCtrWords = 8;
 
+struct SuperOut;
+
 struct PeerParams {
     Params p;             // this rank's replicated state (p.m = global rows); p.sync, p.ap_* local
     u64* mat;             // this rank's rows, tile-major (m_loc rows per tile)
     ulonglong2* info[2];  // per local row {d, (position << 32) | local row}, by step parity
+                          // (super-step form: {d~_a, d_b}, positions in ipos)
+    u32* ipos[2];         // super-step form: position of each local row, by parity
+    PanelOut* pout_b;     // super-step form: panel b's outputs and the panel-side extras
+    SuperOut* so;
     u32* lo;              // [W+1]: first local row still active at step w (lo[0] unused)
     u32 m_loc, rank, nranks, block;
     PeerBufs peer[kMaxRanks];  // every rank's buffers, this rank's included

@@ -14,8 +14,8 @@ import paper_1111_6549_b200 as G  # noqa: E402
 
 bad = 0
 t0 = time.time()
-for Gr in (1, 2, 3, 4, 8):
-    cfg = G.PleConfig(peer_ranks=Gr)
+for Gr, sup in ((1, False), (2, False), (3, False), (8, False), (1, True), (2, True), (3, True), (8, True)):
+    cfg = G.PleConfig(peer_ranks=Gr, super_step=sup)
     for sp in S.suite_specs(120)[::3] + [(700, 900, 2, 5), (600, 600, 3, 6), (1000, 200, 5, 7),
                                           (200, 1000, 6, 8)]:
         m, n, kind, seed = sp
@@ -36,21 +36,22 @@ for Gr in (1, 2, 3, 4, 8):
               and np.array_equal(got.p.swaps, want.swaps.astype(np.uint64)))
         if not ok:
             bad += 1
-            print("MISMATCH", Gr, sp, got.rank, want.rank, flush=True)
-    print(f"G={Gr}: small suite done, {bad} bad so far ({time.time() - t0:.1f} s)", flush=True)
+            print("MISMATCH", Gr, sup, sp, got.rank, want.rank, flush=True)
+    print(f"G={Gr} super={sup}: small suite done, {bad} bad so far ({time.time() - t0:.1f} s)", flush=True)
 
 for n in (4096, 16384):
     base = G.DeviceMatrix(n, n)
     base.fill_ctr(1)
     ref = G.block_iterative_ple(base)
     want = base.checksum()
-    for Gr in (1, 2, 4, 8):
+    for Gr, sup in ((1, False), (2, False), (8, False), (1, True), (2, True), (8, True)):
         dm = G.DeviceMatrix(n, n)
         dm.fill_ctr(1)
-        got = G.block_iterative_ple(dm, G.PleConfig(peer_ranks=Gr))
+        got = G.block_iterative_ple(dm, G.PleConfig(peer_ranks=Gr, super_step=sup))
         ok = got.rank == ref.rank and dm.checksum() == want and np.array_equal(got.q, ref.q)
         bad += 0 if ok else 1
-        print(f"{n}^2 G={Gr}: {'ok' if ok else 'MISMATCH'} rank {got.rank}", flush=True)
+        print(f"{n}^2 G={Gr} super={sup}: {'ok' if ok else 'MISMATCH'} rank {got.rank} "
+              f"driver {got.stats['driver']}", flush=True)
         dm.close()
     base.close()
 

@@ -57,12 +57,13 @@ def test_small_shapes(m, n, kind, super_step):
     assert_same(*run_both(a, m, n, cfg), what=f"{kind} {m}x{n} super={super_step}")
 
 
+@pytest.mark.parametrize("super_step", [False, True])
 @pytest.mark.parametrize("ranks", [1, 2, 5, 8])
 @pytest.mark.parametrize("m,n", SMALL)
 @pytest.mark.parametrize("kind", ["dense", "deficient"])
-def test_small_shapes_peer_ranks(m, n, kind, ranks):
-    """The row-sharded peer-memory driver with 1-8 emulated ranks; many
-    ranks own no rows at these sizes (block-cyclic 256-row blocks)."""
+def test_small_shapes_peer_ranks(m, n, kind, ranks, super_step):
+    """The row-sharded peer-memory driver (one or two panels per sweep) with
+    1-8 emulated ranks; rows are spread over the ranks in small blocks."""
     seed = m * 1000 + n
     a = O.fill_random(m, n, 0.5, seed)
     if kind == "deficient":
@@ -70,7 +71,8 @@ def test_small_shapes_peer_ranks(m, n, kind, ranks):
         for _ in range(4):
             d, s = rng.integers(0, m, 2)
             a[d] = a[s]
-    assert_same(*run_both(a, m, n, G.PleConfig(peer_ranks=ranks)), what=f"{kind} {m}x{n} ranks={ranks}")
+    cfg = G.PleConfig(peer_ranks=ranks, super_step=super_step)
+    assert_same(*run_both(a, m, n, cfg), what=f"{kind} {m}x{n} ranks={ranks} super={super_step}")
 
 
 @pytest.mark.parametrize("m,n,density", [(1024, 1024, 0.5), (2048, 2048, 0.5), (1500, 2500, 0.5),
@@ -126,7 +128,9 @@ def test_smoke_entry():
 
 DRIVERS = {"super": (G.PleConfig(super_step=True), 2), "single": (G.PleConfig(single_panel=True), 1),
            "multi": (G.PleConfig(multi_kernel=True), 0), "peer1": (G.PleConfig(peer_ranks=1), 3),
-           "peer3": (G.PleConfig(peer_ranks=3), 3), "peer8": (G.PleConfig(peer_ranks=8), 3)}
+           "peer3": (G.PleConfig(peer_ranks=3), 3), "peer8": (G.PleConfig(peer_ranks=8), 3),
+           "peer1s": (G.PleConfig(peer_ranks=1, super_step=True), 4),
+           "peer4s": (G.PleConfig(peer_ranks=4, super_step=True), 4)}
 
 
 @pytest.mark.parametrize("driver", sorted(DRIVERS))
