@@ -305,6 +305,9 @@ def gpu_arm(args, rank, world, local_rank):
         e2e_s += time.perf_counter() - t0
         e2e_bytes += o2.stats["alg_bytes"]
     e2e_parity = (o2.rank == out.rank)
+    # the in-place L\E the host received (part of it streamed out while the
+    # kernel ran) against the device-resident run's result
+    e2e_words = (G.host_checksum(host_np, n) == checksum) if checksum is not None else None
 
     # ---- max over ranks ----
     vals = torch.tensor([dev_ms, tot_bytes, e2e_s, e2e_bytes, kern_ms, float(launches)],
@@ -389,7 +392,8 @@ def gpu_arm(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(m * Wd * 8), "d2h_bytes_per_step": int(m * Wd * 8),
                 "steps": e2e_steps, "ms_per_step": round(1e3 * e2e_max_s / e2e_steps, 3),
-                "rank_matches_device_run": bool(e2e_parity)},
+                "rank_matches_device_run": bool(e2e_parity),
+                "output_matches_device_run": e2e_words},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clk,

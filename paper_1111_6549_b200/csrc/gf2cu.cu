@@ -15,6 +15,7 @@
 #include <new>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gf2cu.h"
@@ -69,6 +70,9 @@ struct Workspace {
     u32* rbhist = nullptr;
     u32* host_r = nullptr;       // pinned, mapped
     u32* host_r_dev = nullptr;   // device alias
+    u32* out_host = nullptr;     // pinned, mapped: leading positions already final in data
+    u32* out_host_dev = nullptr;
+    cudaStream_t copy = nullptr; // streamed D2H of finished rows while the kernel runs
     u64* hashes = nullptr;       // per-row checksum scratch
     gf2cu::SyncState* sync = nullptr;
     u64* phase_ns = nullptr;     // 8 stamps per step (persistent driver)
@@ -100,6 +104,8 @@ void free_ws(Workspace& w) {
     cudaFree(w.pout_b);
     cudaFree(w.sout);
     if (w.host_r) cudaFreeHost(w.host_r);
+    if (w.out_host) cudaFreeHost(w.out_host);
+    if (w.copy) cudaStreamDestroy(w.copy);
     for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
     w = Workspace{};
 }
@@ -240,6 +246,9 @@ gf2cu_status ensure_ws(gf2cu_matrix* a) {
     CU_TRY(cudaMalloc(&w.rbhist, (a->W + 1) * sizeof(u32)));
     CU_TRY(cudaHostAlloc(&w.host_r, sizeof(u32), cudaHostAllocMapped));
     CU_TRY(cudaHostGetDevicePointer(&w.host_r_dev, w.host_r, 0));
+    CU_TRY(cudaHostAlloc(&w.out_host, sizeof(u32), cudaHostAllocMapped));
+    CU_TRY(cudaHostGetDevicePointer(&w.out_host_dev, w.out_host, 0));
+    CU_TRY(cudaStreamCreateWithFlags(&w.copy, cudaStreamNonBlocking));
     return GF2CU_OK;
 }
 
@@ -510,9 +519,15 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
 }
 
 // Launches the whole decomposition on `s`; outputs are copied to the host.
+// stream_to (an aligned host view of the matrix, may be null): with the
+// super-step driver, the rows the kernel finishes are copied into it while
+// the factorization runs; *rows_streamed = how many leading rows already
+// hold their final value there (the caller downloads the rest).
 gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
                      size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
-                     gf2cu_stats* stats) {
+                     gf2cu_stats* stats, const gf2cu_view* stream_to = nullptr,
+                     size_t* rows_streamed = nullptr) {
+    if (rows_streamed) *rows_streamed = 0;
     if (const unsigned pr = cfg ? (cfg->flags >> 16) & 15u : 0u)
         return run_ple_peer(a, cfg, pr, swaps, q, rank, col_swaps, n_col_swaps, stats);
     gf2cu_status st = ensure_ws(a);
@@ -600,6 +615,14 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
 
     *ws.host_r = 0;
+    const bool streaming = super && stream_to && rows_streamed;
+    if (streaming) {
+        *reinterpret_cast<volatile u32*>(ws.out_host) = 0;
+        p.out = a->data;
+        p.out_Wp = (u32)a->Wp;
+        p.out_host = ws.out_host_dev;
+    }
+    size_t sent = 0;
     if (super) {
         p.Wpad8 = Wpad4;  // the super-step driver's tile width is 32 bytes
         gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4);
@@ -645,6 +668,29 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
                                                dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
         }
         if (E) cudaEventRecord(E[1], s);
+        if (streaming) {
+            // copy the finished rows out while the kernel runs (copy engine,
+            // second stream), in chunks of at least m/32 rows
+            cudaEvent_t kdone;
+            CU_TRY(cudaEventCreateWithFlags(&kdone, cudaEventDisableTiming));
+            CU_TRY(cudaEventRecord(kdone, s));
+            const size_t chunk = std::max<size_t>(1024, m / 32);
+            uint64_t* host = stream_to->data + (stream_to->col_off >> 6);
+            for (;;) {
+                const bool fin = cudaEventQuery(kdone) == cudaSuccess;
+                const size_t avail = *reinterpret_cast<volatile u32*>(ws.out_host);
+                if (avail > sent && (avail - sent >= chunk || fin)) {
+                    CU_TRY(cudaMemcpy2DAsync(host + sent * stream_to->stride, stream_to->stride * 8,
+                                             a->data + sent * a->Wp, a->Wp * 8, W * 8, avail - sent,
+                                             cudaMemcpyDeviceToHost, ws.copy));
+                    sent = avail;
+                }
+                if (fin) break;
+                std::this_thread::sleep_for(std::chrono::microseconds(20));
+            }
+            cudaEventDestroy(kdone);
+            CU_TRY(cudaStreamSynchronize(ws.copy));
+        }
         gf2cu::SyncState sy{};
         CU_TRY(cudaMemcpyAsync(&sy, ws.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
         CU_TRY(cudaStreamSynchronize(s));
@@ -706,13 +752,16 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
 
     // back to the row-major public layout, rows gathered into position order
-    if (super)
+    if (super) {
         gf2cu::untile4_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
-                                                     Wpad4, p.ubuf, p.ucap, ws.qcol, (u32)rk, (u32)W);
-    else
+                                                     Wpad4, p.ubuf, p.ucap, ws.qcol, (u32)rk, (u32)W,
+                                                     (u32)sent);
+    } else {
         gf2cu::untile_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
                                                     p.Wpad8, p.ubuf, p.ucap, ws.qcol, (u32)rk, (u32)W);
+    }
     CU_TRY(cudaGetLastError());
+    if (rows_streamed) *rows_streamed = sent;
 
     std::vector<u32> sw(rk), qq(rk);
     if (rk) {
@@ -1005,13 +1054,15 @@ gf2cu_status view_upload(const gf2cu_view* v, gf2cu_matrix* a, cudaStream_t s,
 
 // Device rows -> host window (bits outside the window untouched); synchronous.
 gf2cu_status view_download(const gf2cu_view* v, const gf2cu_matrix* a, cudaStream_t s,
-                           std::vector<u64>& packed) {
+                           std::vector<u64>& packed, size_t row_lo = 0) {
     const size_t m = v->nrows, n = v->ncols, W = a->W;
     if (m == 0 || W == 0) return GF2CU_OK;
     cudaError_t e;
     if (view_aligned(v)) {
-        e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6), v->stride * 8, a->data, a->Wp * 8, W * 8,
-                              m, cudaMemcpyDeviceToHost, s);
+        if (row_lo >= m) return GF2CU_OK;
+        e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6) + row_lo * v->stride, v->stride * 8,
+                              a->data + row_lo * a->Wp, a->Wp * 8, W * 8, m - row_lo,
+                              cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     } else {
         packed.resize(m * W);
@@ -1031,7 +1082,8 @@ gf2cu_status view_download(const gf2cu_view* v, const gf2cu_matrix* a, cudaStrea
 // Host view <-> the cached device matrix of its shape: upload,
 // body(matrix, cfg), download.
 template <class Body>
-gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* stats, Body&& body) {
+gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* stats, Body&& body,
+                       size_t* rows_done = nullptr) {
     gf2cu_cfg c;
     gf2cu_default_config(&c);
     if (cfg) c = *cfg;
@@ -1046,7 +1098,7 @@ gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* s
     c.stream = s;
     st = body(a, c);
     if (st == GF2CU_OK) {
-        st = view_download(v, a, s, packed);
+        st = view_download(v, a, s, packed, rows_done ? *rows_done : 0);
         if (stats) {
             stats->h2d_bytes = double(a->m) * a->W * 8;
             stats->d2h_bytes = double(a->m) * a->W * 8;
@@ -1321,9 +1373,15 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
         if (stats) std::memset(stats, 0, sizeof(*stats));
         return GF2CU_OK;
     }
-    return with_view(v, cfg, stats, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
-        return run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats);
-    });
+    // aligned views receive the finished rows while the kernel runs
+    size_t streamed = 0;
+    const gf2cu_view* to = view_aligned(v) ? v : nullptr;
+    return with_view(
+        v, cfg, stats,
+        [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
+            return run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats, to, &streamed);
+        },
+        &streamed);
 }
 
 gf2cu_status gf2cu_matrix_mul(gf2cu_matrix* c, const gf2cu_matrix* a, const gf2cu_matrix* b,

@@ -66,7 +66,8 @@ struct SyncState {
     u32 t_count;     // worker arrivals after the whole trailing update
     u32 st_count;    // worker arrivals after staging (unused by the persistent driver)
     u32 error;       // watchdog tripped
-    u32 pad[3];
+    u32 out_count;   // super-step driver: worker arrivals after writing finished rows to `out`
+    u32 pad[2];
     u64 stamps[8];   // debug timestamps
 };
 
@@ -101,6 +102,12 @@ struct Params {
     u32 window_only; // 1: abort on a window miss instead of scanning
     u32 nranks, block;  // row distribution: row g lives on rank (g / block) % nranks
     u32 m, n, W, Wpad8;
+    // super-step driver, streamed output (may be null): the finished rows
+    // (positions below r) in row-major form, stride out_Wp, and a mapped
+    // host word holding how many leading positions of `out` are final
+    u64* out;
+    u32 out_Wp;
+    volatile u32* out_host;
 };
 
 // Panel status words written when Params::status is set.

@@ -59,22 +59,42 @@ __global__ void tile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst,
 // Back to row-major in position order; the pivot row at position i < rank of
 // super-step S = q_i / 128 takes its tiles from S's first swept tile
 // ((2S+2)/4) on from ubuf, when S swept.
+// 16 bytes (words x, x+1) of the final row at position `row`.
+__device__ __forceinline__ const u64* final4(const u64* src, const u32* perm, u32 m, const u64* ubuf,
+                                             u32 ucap, const u32* qcol, u32 rank, u32 W, u32 row, u32 x) {
+    const u64* from = tw4(const_cast<u64*>(src), m, perm[row], x);
+    if (row < rank) {
+        const u32 w2 = 2u * (qcol[row] >> 7) + 2u;  // first word after the super-step
+        if (w2 < W && (x >> 2) >= (w2 >> 2)) from = tw4(const_cast<u64*>(ubuf), ucap, row, x);
+    }
+    return from;
+}
+
+// (positions below row_lo were already written, by the kernel's streamed output)
 __global__ void untile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst,
                                const u32* __restrict__ perm, u32 m, u32 Wp, u32 Wpad4,
                                const u64* __restrict__ ubuf, u32 ucap, const u32* __restrict__ qcol,
-                               u32 rank, u32 W) {
+                               u32 rank, u32 W, u32 row_lo = 0u) {
     const u32 per_row = Wpad4 >> 1;
-    const u64 total = (u64)m * per_row;
+    const u64 total = (u64)(m - row_lo) * per_row;
     for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (u64)gridDim.x * blockDim.x) {
-        const u32 row = (u32)(e / per_row), x = 2u * (u32)(e - (u64)row * per_row);
-        const u64* from = tw4(const_cast<u64*>(src), m, perm[row], x);
-        if (row < rank) {
-            const u32 w2 = 2u * (qcol[row] >> 7) + 2u;  // first word after the super-step
-            if (w2 < W && (x >> 2) >= (w2 >> 2)) from = tw4(const_cast<u64*>(ubuf), ucap, row, x);
-        }
+        const u32 row = row_lo + (u32)(e / per_row), x = 2u * (u32)(e - (u64)(row - row_lo) * per_row);
         *reinterpret_cast<ulonglong2*>(dst + (size_t)row * Wp + x) =
-            *reinterpret_cast<const ulonglong2*>(from);
+            *reinterpret_cast<const ulonglong2*>(final4(src, perm, m, ubuf, ucap, qcol, rank, W, row, x));
+    }
+}
+
+// Streamed output: the rows at positions [lo, hi) (pivot rows of a finished
+// super-step) into p.out in row-major form; 16-byte units split as part
+// `part` of `nparts`.
+__device__ __forceinline__ void out_rows4(const Params& p, u32 lo, u32 hi, u32 part, u32 nparts) {
+    const u32 per_row = p.Wpad8 >> 1;  // Wpad4 in this driver
+    const u32 total = (hi - lo) * per_row;
+    for (u32 e = part * blockDim.x + threadIdx.x; e < total; e += nparts * blockDim.x) {
+        const u32 row = lo + e / per_row, x = 2u * (e % per_row);
+        *reinterpret_cast<ulonglong2*>(p.out + (size_t)row * p.out_Wp + x) = ldcg(reinterpret_cast<const ulonglong2*>(
+            final4(p.mat, p.perm, p.m, p.ubuf, p.ucap, p.qcol, 0xffffffffu, p.W, row, x)));
     }
 }
 
@@ -481,6 +501,20 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             s_ok = spin_geq2(&sy->t_count, nworkers * S, &p.ap_done[S], nch, &sy->error) ? 1u : 0u;
         __syncthreads();
         if (!s_ok) return;
+        if (p.out && S > 0) {
+            // S-1 is finished everywhere: its pivot rows are final; write them
+            // out row-major and tell the host (which copies them while the
+            // factorization goes on)
+            out_rows4(p, *(volatile u32*)&p.rhist[w - 2u], r, wk, nworkers);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(&sy->out_count, 1u) == nworkers * S - 1u) {
+                    __threadfence_system();
+                    *p.out_host = r;
+                }
+            }
+        }
         if (wk == 0) stamp2(p, w, 3);
         if (sweep) {
             const u32 nt = (p.Wpad8 >> 2) - ct - 1;  // Wpad8 holds Wpad4 here

@@ -213,3 +213,20 @@ def test_131072_reconstruction_sample():
             T[np.arange(sel.size), qs >> 6] |= np.uint64(1) << (qs & 63).astype(np.uint64)
             prod = np.bitwise_xor.reduce(T, axis=0)
         assert np.array_equal(prod, ctr_rows([idx[i]], n, 1)[0]), f"position {i}"
+
+
+@pytest.mark.parametrize("m,n", [(16384, 16384), (12000, 20000), (20000, 9000)])
+def test_streamed_output_matches_device(m, n):
+    """gf2cu_ple on an aligned host view with the super-step driver copies the
+    rows the kernel finishes to the host while it runs (chunks of >= m/32
+    rows); the host result must equal the device-resident run's."""
+    a = O.fill_ctr(m, n, 3)
+    a[m // 3: m // 3 + 200] = a[10:210]  # some rank deficiency
+    bm = G.BitMatrix(m, n, a.copy())
+    got = G.block_iterative_ple(bm, G.PleConfig(super_step=True))
+    d = G.DeviceMatrix(m, n)
+    d.upload(a)
+    want = G.block_iterative_ple(d, G.PleConfig(super_step=True))
+    assert got.rank == want.rank
+    assert np.array_equal(got.q, want.q) and np.array_equal(got.p.swaps, want.p.swaps)
+    assert np.array_equal(bm.words, d.download())
