@@ -156,6 +156,8 @@ __device__ __forceinline__ void peer_trail16_rows(const PeerParams& s, const uns
     const bool cap2 = cap_lane && (w + 3u < s.p.W);
     const u32 nxt = (S + 1u) & 1u;
     const u32 lane_row = wid * 16u + rw;
+    u32 lsel[4], lkoff[4];
+    lookup16_consts(rq, h, lsel, lkoff);
     u64* tbase = s.mat + (((size_t)tile * s.m_loc) << 2) + 2u * h;
     const u32 rend = row0 + cnt;
     const u32 nit = (cnt + kRows16 - 1) / kRows16;
@@ -205,13 +207,7 @@ __device__ __forceinline__ void peer_trail16_rows(const PeerParams& s, const uns
             const u32 ri = base + lane_row + (u32)k * (kTrailThreads / 2);
             const ulonglong2 d = dC[k];
             if ((d.x | d.y) != 0ull && ri < rend) {
-#pragma unroll
-                for (u32 pp = 0; pp < 16; ++pp) {
-                    const u32 t = (pp + rq) & 15u;
-                    const u64 dw = t < 8u ? d.x : d.y;
-                    const u32 e = (u32)(dw >> (8u * (t & 7u))) & 0xffu;
-                    xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab16_off(t, e, h)));
-                }
+                lookup16(valC[k], smem, d, lsel, lkoff);
                 *reinterpret_cast<ulonglong2*>(tbase + ((size_t)ri << 2)) = valC[k];
             }
             const u32 pos = pC[k];

@@ -239,6 +239,32 @@ __device__ __forceinline__ u32 tab16_off(u32 t, u32 e, u32 h) {
     return (((t >> 2) * 256u + e) << 7) + ((t & 3u) << 5) + (h << 4);
 }
 
+// The 16 lookups of one row's 16-byte half-chunk: chunk ^= T_t[byte_t(d)]
+// for t = 0..15, where d = {d~_a, d_b}. At lookup pp a lane reads table
+// t = pp ^ rq (rq = its row within the quarter-warp): the 4 rows of a
+// quarter-warp hit the 4 tables of one 32 KiB block in 4 different bank
+// quarters (conflict-free), t >> 2 = pp >> 2 is a compile-time block offset,
+// and byte t of d is byte (pp & 3) ^ rq of 32-bit word pp >> 2 -- one PRMT
+// with a per-lane selector. sel[j] = 0x4440 | (j ^ rq), koff[j] = the lane's
+// bank-quarter and half offset for j = pp & 3.
+__device__ __forceinline__ void lookup16(ulonglong2& acc, const unsigned char* smem, ulonglong2 d,
+                                         const u32 sel[4], const u32 koff[4]) {
+    const u32 wd[4] = {(u32)d.x, (u32)(d.x >> 32), (u32)d.y, (u32)(d.y >> 32)};
+#pragma unroll
+    for (u32 pp = 0; pp < 16; ++pp) {
+        const u32 e = __byte_perm(wd[pp >> 2], 0u, sel[pp & 3u]);
+        xor2(acc, *reinterpret_cast<const ulonglong2*>(smem + (pp >> 2) * 32768u + e * 128u + koff[pp & 3u]));
+    }
+}
+
+__device__ __forceinline__ void lookup16_consts(u32 rq, u32 h, u32 sel[4], u32 koff[4]) {
+#pragma unroll
+    for (u32 j = 0; j < 4; ++j) {
+        sel[j] = 0x4440u | (j ^ rq);
+        koff[j] = ((j ^ rq) << 5) | (h << 4);
+    }
+}
+
 // Gray walk (gray_code.hpp:105-112) of the 16 tables for one 32-byte tile
 // from the raw pivot rows of both panels (pa / pb = their physical rows;
 // words <= w+1 of the tile read as zero). Thread layout (512): h = tid & 1,
@@ -306,6 +332,8 @@ __device__ __forceinline__ void trail16_rows(const Params& p, const unsigned cha
     const bool cap_lane = capture && (((w + 2u) & 3u) >> 1) == h;
     const bool cap2 = cap_lane && (w + 3u < p.W);
     const u32 lane_row = wid * 16u + rw;
+    u32 lsel[4], lkoff[4];
+    lookup16_consts(rq, h, lsel, lkoff);
     u64* tbase = p.mat + (((size_t)tile * p.m) << 2) + 2u * h;
     const u32 rend = row0 + cnt;
     const u32 nit = (cnt + kRows16 - 1) / kRows16;
@@ -349,13 +377,7 @@ __device__ __forceinline__ void trail16_rows(const Params& p, const unsigned cha
             const u32 ri = base + lane_row + (u32)k * (kTrailThreads / 2);
             const ulonglong2 d = dC[k];
             if ((d.x | d.y) != 0ull || (ri < npiv && ri < rend)) {
-#pragma unroll
-                for (u32 pp = 0; pp < 16; ++pp) {
-                    const u32 t = (pp + rq) & 15u;
-                    const u64 dw = t < 8u ? d.x : d.y;
-                    const u32 e = (u32)(dw >> (8u * (t & 7u))) & 0xffu;
-                    xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab16_off(t, e, h)));
-                }
+                lookup16(valC[k], smem, d, lsel, lkoff);
                 if (ri < npiv)  // a pivot row of this super-step: its tail goes to ubuf
                     *reinterpret_cast<ulonglong2*>(
                         p.ubuf + ((((size_t)tile * p.ucap + r + ri) << 2) + 2u * h)) = valC[k];
