@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
     const u32 row_base = blockIdx.y * kGemmRows;
     const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
     const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
+    u32 lsel[4], lkoff[4];
+    lookup8_consts(par, ch, lsel, lkoff);
     const u32 r0 = row_base + wid * 8u + rg;
     const u32 Lw = (L + 63u) >> 6;
     ulonglong2 acc[kGemmRowsPerThread];
@@ -72,12 +74,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
 #pragma unroll
         for (u32 s = 0; s < kGemmRowsPerThread; ++s) {
             if (d[s] == 0ull) continue;
-#pragma unroll
-            for (u32 gi = 0; gi < kTables; ++gi) {
-                const u32 g = gi ^ par;
-                const u32 e = (u32)(d[s] >> (8u * g)) & 0xffu;
-                xor2(acc[s], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
-            }
+            lookup8(acc[s], smem, d[s], lsel, lkoff);
         }
 #pragma unroll
         for (u32 s = 0; s < kGemmRowsPerThread; ++s) d[s] = dn[s];

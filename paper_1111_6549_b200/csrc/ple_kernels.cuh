@@ -872,6 +872,29 @@ __device__ __forceinline__ void xor2(ulonglong2& a, const ulonglong2& b) {
     a.y ^= b.y;
 }
 
+// The 8 lookups of one 16-byte chunk: acc ^= T_g[byte_g(d)], g = gi ^ par
+// for gi = 0..7 (par = the row's parity in its quarter-warp). g >> 1 =
+// gi >> 1 is a compile-time table-pair offset, and byte g of d is byte
+// (gi & 3) ^ par of 32-bit word gi >> 2: one PRMT with a per-lane selector.
+// sel[j] = 0x4440 | (j ^ par), koff[j] = (((j ^ par) & 1) << 6) | (ch << 4).
+__device__ __forceinline__ void lookup8(ulonglong2& acc, const unsigned char* smem, u64 d,
+                                        const u32 sel[4], const u32 koff[4]) {
+    const u32 wd[2] = {(u32)d, (u32)(d >> 32)};
+#pragma unroll
+    for (u32 gi = 0; gi < kTables; ++gi) {
+        const u32 e = __byte_perm(wd[gi >> 2], 0u, sel[gi & 3u]);
+        xor2(acc, *reinterpret_cast<const ulonglong2*>(smem + (gi >> 1) * 32768u + e * 128u + koff[gi & 3u]));
+    }
+}
+
+__device__ __forceinline__ void lookup8_consts(u32 par, u32 ch, u32 sel[4], u32 koff[4]) {
+#pragma unroll
+    for (u32 j = 0; j < 4; ++j) {
+        sel[j] = 0x4440u | (j ^ par);
+        koff[j] = (((j ^ par) & 1u) << 6) | (ch << 4);
+    }
+}
+
 // Build the 8 Gray-code tables of one 64-byte column tile from 64 source rows
 // (row t's chunk at rowptr(t); rows t >= rb and the tile's first `zlim`
 // words read as zero). Thread layout (512): ch = tid&3, g&1 = (tid>>2)&1,
@@ -951,6 +974,8 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
     const bool cap2_hi = (cap2_word & 1u) != 0;
     const bool capture = capture1 || capture2;
     const u32 lane_row = wid * 8u + rg;
+    u32 lsel[4], lkoff[4];
+    lookup8_consts(par, ch, lsel, lkoff);
     u64* tbase = p.mat + (((size_t)tile * p.m) << 3) + 2u * ch;
     const u32 rend = row0 + cnt;
     const u32 nit = (cnt + kRowsPerIter - 1) / kRowsPerIter;
@@ -995,12 +1020,7 @@ __device__ __forceinline__ void trail_rows(const Params& p, const unsigned char*
             const u64 d = infC[k].x;
             // (pivot rows always reach ubuf, d = 0 included: U_t = raw tail)
             if (d != 0ull || (ri < npiv && ri < rend)) {
-#pragma unroll
-                for (u32 gi = 0; gi < kTables; ++gi) {
-                    const u32 g = gi ^ par;
-                    const u32 e = (u32)(d >> (8u * g)) & 0xffu;
-                    xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
-                }
+                lookup8(valC[k], smem, d, lsel, lkoff);
                 if (ri < npiv)  // a pivot row of this step: its tail goes to ubuf
                     *reinterpret_cast<ulonglong2*>(
                         p.ubuf + ((((size_t)tile * p.ucap + r + ri) << 3) + 2u * ch)) = valC[k];

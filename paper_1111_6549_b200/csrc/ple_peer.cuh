@@ -221,6 +221,8 @@ __device__ __forceinline__ void peer_trail_rows(const PeerParams& s, const unsig
     const bool capture = capture1 || capture2;
     const u32 nxt = (w + 1u) & 1u;
     const u32 lane_row = wid * 8u + rg;
+    u32 lsel[4], lkoff[4];
+    lookup8_consts(par, ch, lsel, lkoff);
     u64* tbase = s.mat + (((size_t)tile * s.m_loc) << 3) + 2u * ch;
     const u32 rend = row0 + cnt;
     const u32 nit = (cnt + kRowsPerIter - 1) / kRowsPerIter;
@@ -265,12 +267,7 @@ __device__ __forceinline__ void peer_trail_rows(const PeerParams& s, const unsig
             const u32 ri = base + lane_row + (u32)k * (kTrailThreads / 4);
             const u64 d = infC[k].x;
             if (d != 0ull && ri < rend) {
-#pragma unroll
-                for (u32 gi = 0; gi < kTables; ++gi) {
-                    const u32 g = gi ^ par;
-                    const u32 e = (u32)(d >> (8u * g)) & 0xffu;
-                    xor2(valC[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
-                }
+                lookup8(valC[k], smem, d, lsel, lkoff);
                 *reinterpret_cast<ulonglong2*>(tbase + ((infC[k].y & 0xffffffffull) << 3)) = valC[k];
             }
             const u32 pos = (u32)(infC[k].y >> 32);

@@ -147,6 +147,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1) rref_update_kernel(RrefParam
     const u64 beg = total * blockIdx.x / gridDim.x, end = total * (blockIdx.x + 1) / gridDim.x;
     const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
     const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
+    u32 lsel[4], lkoff[4];
+    lookup8_consts(par, ch, lsel, lkoff);
     const u64* ucol = p.U + (size_t)J * p.R;
     u64 u = beg;
     while (u < end) {
@@ -170,12 +172,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1) rref_update_kernel(RrefParam
 #pragma unroll
             for (int k = 0; k < kUnroll; ++k) {
                 if (!d[k]) continue;
-#pragma unroll
-                for (u32 gi = 0; gi < kTables; ++gi) {
-                    const u32 g = gi ^ par;
-                    const u32 e = (u32)(d[k] >> (8u * g)) & 0xffu;
-                    xor2(v[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
-                }
+                lookup8(v[k], smem, d[k], lsel, lkoff);
                 const u32 i = b + (u32)k * (kTrailThreads / 4);
                 *reinterpret_cast<ulonglong2*>(tbase + ((size_t)i << 3)) = v[k];
             }
@@ -243,6 +240,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1) rref_step_kernel(RrefParams 
     const u64 beg = total * bi / nb, end = total * (bi + 1) / nb;
     const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
     const u32 rg = lane >> 2, ch = lane & 3u, par = rg & 1u;
+    u32 lsel[4], lkoff[4];
+    lookup8_consts(par, ch, lsel, lkoff);
     u64 u = beg;
     while (u < end) {
         const u32 tile = (u32)(u / nrows);
@@ -265,12 +264,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1) rref_step_kernel(RrefParams 
 #pragma unroll
             for (int k = 0; k < kUnroll; ++k) {
                 if (!d[k]) continue;
-#pragma unroll
-                for (u32 gi = 0; gi < kTables; ++gi) {
-                    const u32 g = gi ^ par;
-                    const u32 e = (u32)(d[k] >> (8u * g)) & 0xffu;
-                    xor2(v[k], *reinterpret_cast<const ulonglong2*>(smem + tab_off(g, e, ch)));
-                }
+                lookup8(v[k], smem, d[k], lsel, lkoff);
                 const u32 i = b + (u32)k * (kTrailThreads / 4);
                 *reinterpret_cast<ulonglong2*>(tbase + ((size_t)i << 3)) = v[k];
             }
