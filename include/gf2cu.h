@@ -90,9 +90,10 @@ typedef struct {
     double alg_bytes;           /* sum over steps of 16*(m-r-rb)*(W-w-1)        */
     double h2d_bytes, d2h_bytes;/* host<->device bytes moved by gf2cu_ple       */
     double kernel_ms;           /* persistent kernel duration (CUDA events)     */
-    int driver;                 /* 3 = row-sharded (peer memory), 2 = super-step
-                                   (two panels per sweep), 1 = persistent
-                                   single-panel, 0 = per phase                  */
+    int driver;                 /* 4 / 3 = row-sharded over peer memory with two /
+                                   one panels per sweep, 2 = super-step (two
+                                   panels per sweep), 1 = persistent single-panel,
+                                   0 = per phase                                */
     double sweep_bytes;         /* bytes the trailing sweeps move: alg_bytes for
                                    one panel per sweep; for the super-step driver
                                    sum over super-steps of 16*(m-r-rba-rbb)*(W-w-2)
@@ -300,6 +301,11 @@ gf2cu_status gf2cu_peer_upload(gf2cu_peer* p, const uint64_t* host, size_t host_
 gf2cu_status gf2cu_peer_download(const gf2cu_peer* p, uint64_t* host, size_t host_stride,
                                  void* stream);
 gf2cu_status gf2cu_peer_fill_ctr(gf2cu_peer* p, uint64_t seed, void* stream);
+/* Diagnostic of the peer mappings (no kernel waits on another): with value
+ * != 0, store it into word `rank` of every rank's marker block through the
+ * mappings; then read this rank's markers (nranks words; 0 = not received)
+ * into seen. gf2cu_peer_reset clears them. */
+gf2cu_status gf2cu_peer_ping(gf2cu_peer* p, uint32_t value, uint32_t* seen);
 /* Zero this rank's counters; every rank must reset before any rank runs. */
 gf2cu_status gf2cu_peer_reset(gf2cu_peer* p, void* stream);
 /* The factorization of this rank's rows (stats: steps, alg_bytes of the whole

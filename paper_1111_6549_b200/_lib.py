@@ -148,6 +148,7 @@ SYMBOLS = {
     "gf2cu_peer_download": (C.c_int, [_mp, _u64p, _sz, C.c_void_p]),
     "gf2cu_peer_fill_ctr": (C.c_int, [_mp, C.c_uint64, C.c_void_p]),
     "gf2cu_peer_reset": (C.c_int, [_mp, C.c_void_p]),
+    "gf2cu_peer_ping": (C.c_int, [_mp, C.c_uint32, C.POINTER(C.c_uint32)]),
     "gf2cu_peer_run": (C.c_int, [_mp, C.c_void_p, C.POINTER(gf2cu_stats)]),
     "gf2cu_peer_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),
     "gf2cu_fill_random": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_double, C.c_uint64]),

@@ -2010,6 +2010,20 @@ gf2cu_status gf2cu_peer_connect(gf2cu_peer* p, const void* handles) {
     return GF2CU_OK;
 }
 
+gf2cu_status gf2cu_peer_ping(gf2cu_peer* p, uint32_t value, uint32_t* seen) {
+    if (!p || !seen) return fail(GF2CU_EINVAL, "null argument");
+    if (!p->connected) return fail(GF2CU_EINVAL, "gf2cu_peer_connect has not been called");
+    DeviceGuard g(p->device);
+    if (value) {
+        gf2cu::peer_ping_kernel<<<1, 1, 0, p->own>>>(p->dp, value);
+        CU_TRY(cudaGetLastError());
+        CU_TRY(cudaStreamSynchronize(p->own));
+    }
+    CU_TRY(cudaMemcpy(seen, p->hp.peer[p->hp.rank].ctr + gf2cu::kCtrPing, p->hp.nranks * 4,
+                      cudaMemcpyDeviceToHost));
+    return GF2CU_OK;
+}
+
 gf2cu_status gf2cu_peer_upload(gf2cu_peer* p, const uint64_t* host, size_t host_stride, void* stream) {
     if (!p || (!host && p->hp.m_loc)) return fail(GF2CU_EINVAL, "null argument");
     if (host_stride < p->W) return fail(GF2CU_EINVAL, "host stride smaller than the row");

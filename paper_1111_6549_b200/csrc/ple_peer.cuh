@@ -49,7 +49,8 @@ constexpr int kCtrCap = 0;  // +1 per rank per step: its look-ahead captures lan
 constexpr int kCtrLa = 1;   // +1 per rank per step: its pivots' look-ahead tiles staged
 constexpr int kCtrSt = 2;   // +1 per rank per step: its pivots' remaining tiles staged
 constexpr int kCtrErr = 3;  // watchdog tripped somewhere (set on every rank)
-constexpr int kCtrWords = 8;
+constexpr int kCtrPing = 8; // [8, 16): gf2cu_peer_ping markers, one word per sender rank
+constexpr int kCtrWords = 16;
 
 struct SuperOut;
 
@@ -509,6 +510,14 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                 peer_trail_share(s, q, smem, w, r, rb, lo, tcap + 1u, pbeg, pend, info);
         }
     }
+}
+
+// Diagnostic of the peer mappings: store `value` into word kCtrPing + rank of
+// every rank's counter block (one thread; nothing waits on anything).
+__global__ void peer_ping_kernel(const PeerParams* __restrict__ me, u32 value) {
+    const PeerParams& s = *me;
+    for (u32 j = 0; j < s.nranks; ++j) s.peer[j].ctr[kCtrPing + s.rank] = value;
+    __threadfence_system();
 }
 
 // Global row-major -> every rank's tile-major local rows (blockIdx.y = rank;

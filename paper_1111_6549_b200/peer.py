@@ -83,6 +83,13 @@ class PeerEngine:
     def fill_ctr(self, seed: int) -> None:
         check(self.L.gf2cu_peer_fill_ctr(self.h, C.c_uint64(seed), self._s()))
 
+    def ping(self, value: int) -> list:
+        """Store `value` into every rank's marker word for this rank through
+        the peer mappings (value 0: only read); returns this rank's markers."""
+        seen = (C.c_uint32 * self.nranks)()
+        check(self.L.gf2cu_peer_ping(self.h, C.c_uint32(value), seen))
+        return list(seen)
+
     def reset(self) -> None:
         check(self.L.gf2cu_peer_reset(self.h, self._s()))
 

@@ -135,3 +135,61 @@ def test_peer_multiprocess_api_world1(case, block):
     assert np.array_equal(swaps, want.swaps.astype(np.uint64))
     assert np.array_equal(qq, want.q.astype(np.uint64))
     assert np.array_equal(full, ref)
+
+
+def _ping_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1111_6549_b200.peer import PeerEngine, exchange_handles
+        eng = PeerEngine(3000, 2000, rank, world, block=64, device=0)
+        exchange_handles(eng, dist)  # cudaIpcOpenMemHandle of every other rank
+        eng.reset()
+        dist.barrier()
+        before = eng.ping(0)
+        dist.barrier()
+        eng.ping(0xC0DE00 + rank)  # stores into every rank's markers (no waiting)
+        dist.barrier()
+        after = eng.ping(0)
+        q.put((rank, before, after))
+        dist.barrier()
+        eng.close()
+    except Exception:
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+        os._exit(1)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_ipc_mappings_multiprocess(world):
+    """The multi-process exchange buffers: every rank exports its buffer with
+    CUDA IPC, the handles are all-gathered, every rank maps the others', and
+    a store through each mapping lands in the right rank's marker word (the
+    counters' offset inside the buffer included). Processes share the one
+    GPU; no kernel waits on another, so this is safe on one device."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ping_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {}
+    try:
+        for _ in range(world):
+            o = q.get(timeout=240)
+            assert o[1] != "error", o[2]
+            got[o[0]] = o
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for p in procs:
+        assert p.exitcode == 0
+    for r in range(world):
+        _, before, after = got[r]
+        assert before == [0] * world
+        assert after == [0xC0DE00 + s for s in range(world)]
