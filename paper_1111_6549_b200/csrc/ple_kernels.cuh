@@ -327,6 +327,7 @@ struct PanelShared {
     u64 dacc[kWin];     // per window slot: d (its combination) and origin
     u32 dorg[kWin];
     int cap_ok;
+    int ep_t[2], ep_j[2];  // panel epochs: pivots / columns done by the leader warp
     // super-step driver
     int super;          // 0, 1 (panel a) or 2 (panel b)
     u64 wraw2[kWin];    // window rows' pre-super-step word w+1 (as loaded)
@@ -511,7 +512,12 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         int t = 0;
         int out_next = nwin < nrem ? 0 : 64;
         bool aborted = false;
-        for (int j = 0; j < jmax && (u32)t < nrem; ++j) {
+        // One cross-warp step for column j (all 4 window warps, up to date
+        // with every pivot < t): per-warp ballots and first candidates
+        // exchanged through shared memory, the first candidate over the
+        // window taken (a window miss scans the other rows). Returns 1 if a
+        // pivot was found, 0 if column j has none, 2 if aborted.
+        auto cross_step = [&](const int j) -> int {
             const int par = j & 1;
             // candidates: live rows (position >= t) holding column j
             const bool b = inwin & (me >= (u32)t) & (((red >> j) & 1ull) != 0ull);
@@ -549,17 +555,17 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 org = mv ? tro : org;
             } else {
                 // ---- window miss: the remaining rows decide ----
-                if (j < out_next) continue;  // no row outside has this column
+                if (j < out_next) return 0;  // no row outside has this column
                 if (p.window_only) {
                     // sharded driver: the host gathers the whole panel column
                     // and runs the step again (nothing global was written)
                     aborted = true;
-                    break;
+                    return 2;
                 }
                 la_wait_cap(la, sh, 3, kWin);  // pb of the outside rows is the capture
                 if (la && sh.cap_ok < 0) {
                     aborted = true;
-                    break;
+                    return 2;
                 }
                 if (me == 0) {
                     sh.cmd = 0;
@@ -571,10 +577,10 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 const u64 best = sh.best;
                 if (best == ~0ull) {
                     out_next = 64;
-                    continue;
+                    return 0;
                 }
                 out_next = (int)(best >> 32);
-                if (out_next != j) continue;  // column j has no pivot anywhere
+                if (out_next != j) return 0;  // column j has no pivot anywhere
                 // pivot from outside the window: it takes position t; the
                 // window row t moves to the pivot's old position P
                 P = (u32)(best & 0xffffffffu);
@@ -612,6 +618,81 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 sh.sw[t] = P;
             }
             ++t;
+            return 1;
+                };
+        // Epochs: the leader warp (the one holding slot t; lower warps hold
+        // no live row) takes pivots alone -- ballot, shuffles, no barrier --
+        // as long as it has a candidate for the next column and t stays in
+        // it. Then all window warps meet, the others apply the epoch's
+        // pivots to their rows in order (they hold no pivot and no swapped
+        // row), and the column the leader had no candidate for goes through
+        // cross_step. Same pivots, swaps and outputs as column-by-column
+        // cross steps; far fewer barriers on dense panels.
+        int j = 0, epoch = 0;
+        while (j < jmax && (u32)t < nrem) {
+            const int L = t >> 5;
+            if ((int)wid == L) {
+                const u32 base = 32u * (u32)L;
+                u64 jbit = 1ull << j;          // column j
+                u64 hi = ~(jbit | (jbit - 1)); // columns > j
+                u64* sE = sh.E;
+                u64* sD = sh.D;
+                while (j < jmax && (u32)t < nrem && (t >> 5) == L) {
+                    const bool live = inwin & (me >= (u32)t);
+                    const u32 bal = __ballot_sync(0xffffffffu, live & ((red & jbit) != 0ull));
+                    if (bal == 0u) break;
+                    const u32 pl = (u32)(__ffs(bal) - 1), tl = (u32)t & 31u;
+                    const bool isP = lane == pl;
+                    // one gather: lane P fetches row t (the swap), every other
+                    // lane the pivot row (lane P holds it already)
+                    const int src = (int)(isP ? tl : pl);
+                    const u64 xr = shfl64(red, src), xa = shfl64(acc, src);
+                    const u32 xo = __shfl_sync(0xffffffffu, org, src);
+                    const u64 pred = isP ? red : xr, pacc = isP ? acc : xa;
+                    if (isP) {  // row swap t <-> P (a no-op when P == t)
+                        red = xr;
+                        acc = xa;
+                        org = xo;
+                    }
+                    if (lane == tl && !isP) org = xo;  // slot t records the pivot's origin
+                    const u64 tbit = 1ull << t;
+                    const u64 msk = 0ull - (u64)(live & (me != (u32)t) & ((red & jbit) != 0ull));
+                    const u64 Et = pred & hi, Dt = pacc ^ tbit;
+                    red ^= Et & msk;
+                    acc ^= Dt & msk;
+                    if (lane == 0) {
+                        sE[t] = Et;
+                        sD[t] = Dt;
+                        sh.q[t] = (u32)j;
+                        sh.sw[t] = base + pl;
+                    }
+                    ++t;
+                    ++j;
+                    jbit <<= 1;
+                    hi <<= 1;
+                }
+                if (lane == 0) {
+                    sh.ep_t[epoch & 1] = t;
+                    sh.ep_j[epoch & 1] = j;
+                }
+            }
+            named_bar(3, kWin);
+            const int t1 = sh.ep_t[epoch & 1], j1 = sh.ep_j[epoch & 1];
+            ++epoch;
+            if ((int)wid > L) {
+                for (int s2 = t; s2 < t1; ++s2) {
+                    const u64 msk = 0ull - ((red >> sh.q[s2]) & 1ull);
+                    red ^= sh.E[s2] & msk;
+                    acc ^= sh.D[s2] & msk;
+                }
+            }
+            t = t1;
+            j = j1;
+            if (j >= jmax || (u32)t >= nrem) break;
+            if ((t >> 5) != L) continue;  // the leader's rows are used up: next leader
+            const int st = cross_step(j);
+            if (st == 2) break;
+            ++j;
         }
         if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 7] = globaltimer();
         sh.dacc[me] = acc;
