@@ -328,6 +328,8 @@ struct PanelShared {
     u32 dorg[kWin];
     int cap_ok;
     int ep_t[2], ep_j[2];  // panel epochs: pivots / columns done by the leader warp
+    u64 lpb2[kWin];        // look-ahead inputs, fetched right after the capture wait:
+    u64 epb[64], epb2[64]; // window rows' pb2 by origin; entering rows' pb / pb2
     // super-step driver
     int super;          // 0, 1 (panel a) or 2 (panel b)
     u64 wraw2[kWin];    // window rows' pre-super-step word w+1 (as loaded)
@@ -702,6 +704,18 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         named_bar(3, kWin);
         if (!aborted) la_wait_cap(la, sh, 3, kWin);
         if (la && sh.cap_ok < 0) aborted = true;
+        // issue the next window's global inputs now, so that their latency
+        // overlaps the writeback: the window rows' pre-step word w+1 (by
+        // origin) and the words w, w+1 of the rows that may enter it
+        u64 f_pb2 = 0ull, f_epb = 0ull, f_epb2 = 0ull;
+        if (la && !aborted && sh.super != 2 && w + 1 < p.W) {
+            if (!sh.super && inwin) f_pb2 = ldcg(p.pb2 + r + me);
+            const u32 qe = r + nwin + me;
+            if (me < 64u && qe < p.m) {
+                f_epb = ldcg(p.pb + qe);
+                f_epb2 = ldcg(p.pb2 + qe);
+            }
+        }
         // the permuted window: raw panel word and physical row per position
         u64 rw = 0ull;
         u32 ph = 0u;
@@ -725,6 +739,11 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             if (sh.super) p.pb2[r + me] = rw2;
             p.perm[r + me] = ph;
             if (p.inv) p.inv[ph] = r + me;
+        }
+        sh.lpb2[me] = f_pb2;
+        if (me < 64u) {
+            sh.epb[me] = f_epb;
+            sh.epb2[me] = f_epb2;
         }
     }
     __syncthreads();
@@ -800,7 +819,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             const u32 o = sh.dorg[k];
             sh.piv2[k] = (o & 0x80000000u) ? sh.opb2[o & 63u]
                          : sh.super       ? sh.wraw2[o & 127u]
-                                          : ldcg(p.pb2 + r + o);
+                                          : sh.lpb2[o & 127u];
             if (sh.super) la->piv2_out[k] = sh.piv2[k];
         }
         __syncthreads();
@@ -809,17 +828,17 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             u64 d, pre;
             if (q - r < nwin) {
                 d = sh.dacc[q - r];
-                pre = sh.super ? sh.wraw2[sh.dorg[q - r] & 127u] : ldcg(p.pb2 + r + sh.dorg[q - r]);
+                pre = sh.super ? sh.wraw2[sh.dorg[q - r] & 127u] : sh.lpb2[sh.dorg[q - r] & 127u];
             } else {
                 // a row entering the window: its combination for step w
-                u64 v = ldcg(p.pb + q);
+                u64 v = sh.epb[q - r - nwin];
                 d = 0ull;
                 for (u32 s2 = 0; s2 < t; ++s2) {
                     const u64 msk = 0ull - ((v >> sh.q[s2]) & 1ull);
                     v ^= sh.E[s2] & msk;
                     d ^= sh.D[s2] & msk;
                 }
-                pre = ldcg(p.pb2 + q);
+                pre = sh.epb2[q - r - nwin];
             }
             u64 x = pre;
 #pragma unroll 8
