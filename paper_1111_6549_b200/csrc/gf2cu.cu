@@ -560,7 +560,9 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     p.qcol = ws.qcol;
     p.rhist = ws.rhist;
     p.rbhist = ws.rbhist;
-    p.host_r = ws.host_r_dev;
+    // (only the one-launch-per-phase driver's host loop polls the mapped r;
+    // the persistent drivers skip the per-panel system-scope fence)
+    p.host_r = (cfg && (cfg->flags & GF2CU_FLAG_MULTI_KERNEL)) ? ws.host_r_dev : nullptr;
     p.sync = ws.sync;
     p.phase_ns = timing ? ws.phase_ns : nullptr;
     p.m = (u32)m;
