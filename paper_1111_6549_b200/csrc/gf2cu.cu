@@ -35,6 +35,13 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// Panel tuning bits (gf2cu::kPanel*); GF2CU_PANEL_FLAGS overrides the default
+// for A/B measurements.
+u32 panel_flags() {
+    const char* e = std::getenv("GF2CU_PANEL_FLAGS");
+    return e ? (u32)std::strtoul(e, nullptr, 0) : gf2cu::kPanelStream;
+}
+
 gf2cu_status fail(gf2cu_status st, const std::string& msg) {
     g_last_error = msg;
     return st;
@@ -330,6 +337,7 @@ gf2cu_status peer_alloc_rank(gf2cu::PeerParams& h, std::vector<void*>& allocs, s
     p.n = (u32)n;
     p.W = (u32)W;
     p.Wpad8 = (u32)Wp8;
+    p.pflags = panel_flags();
     return GF2CU_OK;
 }
 
@@ -569,6 +577,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     p.n = (u32)n;
     p.W = (u32)W;
     p.Wpad8 = (u32)wpad8(W);
+    p.pflags = panel_flags();
 
     static bool attr_set[64] = {false};
     if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
@@ -654,7 +663,8 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         // diagnostics: per-worker sweep stamps (GF2CU_DUMP_WORKERS=<path>)
         const char* wpath = timing ? std::getenv("GF2CU_DUMP_WORKERS") : nullptr;
         u64* wns = nullptr;
-        const size_t wn_words = ((size_t)W + 1) * (size_t)(grid - 1) * 2;
+        const size_t wn_per = super ? 4 : 2;  // super: {wake, pre-work end, rest start, rest end}
+        const size_t wn_words = ((size_t)W + 1) * (size_t)(grid - 1) * wn_per;
         if (wpath) {
             CU_TRY(cudaMalloc(&wns, wn_words * sizeof(u64)));
             CU_TRY(cudaMemsetAsync(wns, 0, wn_words * sizeof(u64), s));
@@ -701,8 +711,8 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             cudaMemcpy(h.data(), wns, wn_words * sizeof(u64), cudaMemcpyDeviceToHost);
             cudaFree(wns);
             if (FILE* f = std::fopen(wpath, "wb")) {
-                const u64 hdr[2] = {(u64)W, (u64)(grid - 1)};
-                std::fwrite(hdr, sizeof(u64), 2, f);
+                const u64 hdr[3] = {(u64)W, (u64)(grid - 1), (u64)wn_per};
+                std::fwrite(hdr, sizeof(u64), super ? 3 : 2, f);
                 std::fwrite(h.data(), sizeof(u64), h.size(), f);
                 std::fclose(f);
             }
@@ -1742,6 +1752,7 @@ gf2cu_status gf2cu_shard_panel(gf2cu_shard* s, size_t w, uint64_t* pos_words, in
     p.n = (u32)s->n;
     p.W = (u32)s->W;
     p.Wpad8 = (u32)s->Wpad8;
+    p.pflags = panel_flags();
     gf2cu::panel_factor_kernel<<<1, gf2cu::kPanelThreads, 0, st>>>(p, (u32)w);
     CU_TRY(cudaGetLastError());
     if (status_out) {  // (asynchronous when the caller does not read the status)

@@ -108,7 +108,13 @@ struct Params {
     u64* out;
     u32 out_Wp;
     volatile u32* out_host;
+    // panel tuning bits (kPanel*)
+    u32 pflags;
 };
+
+// Params::pflags: the window warps behind the leader apply its pivots as it
+// publishes them (instead of all at the epoch's closing barrier).
+constexpr u32 kPanelStream = 1u;
 
 // Panel status words written when Params::status is set.
 constexpr int kStatusMiss = 0;   // 1 = aborted on a window miss (window_only)
@@ -339,7 +345,23 @@ struct PanelShared {
     u64 Ea[64], Da[64]; // panel a's outputs, kept for panel b's miss scans
     u32 qa[64];
     u32 rba;
+    u32 dbg_lead_cyc, dbg_lead_piv, dbg_cross, dbg_epochs;  // diagnostics (phase_ns slot 4)
+    int prog;    // pivots the leader has published (kPanelStream)
+    int ep_fin;  // epoch + 1 once the leader closed it (kPanelStream)
 };
+
+__device__ __forceinline__ void st_release_cta(int* a, int v) {
+    asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"((u32)__cvta_generic_to_shared(a)), "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* a) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"((u32)__cvta_generic_to_shared(a))
+                 : "memory");
+    return v;
+}
 
 // Look-ahead mode of panel_factor_body (persistent driver): the step's r is
 // tracked by the caller, the window words come from sh.nraw (computed at the
@@ -509,6 +531,12 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             }
             sh.wphys[me] = ldcg(p.perm + r + me);
         }
+        if (me == 0) {
+            sh.dbg_lead_cyc = sh.dbg_lead_piv = sh.dbg_cross = sh.dbg_epochs = 0u;
+            sh.prog = 0;
+            sh.ep_fin = 0;
+        }
+        const bool stream = (p.pflags & kPanelStream) != 0u;
         named_bar(3, kWin);
         if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 6] = globaltimer();
         int t = 0;
@@ -634,49 +662,73 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         while (j < jmax && (u32)t < nrem) {
             const int L = t >> 5;
             if ((int)wid == L) {
+                const long long dbg_c0 = clock64();
+                const int dbg_t0 = t;
                 const u32 base = 32u * (u32)L;
                 u64 jbit = 1ull << j;          // column j
                 u64 hi = ~(jbit | (jbit - 1)); // columns > j
+                u64 tbit = 1ull << t;
+                // pivots this leader can take at most: columns, rows, its slots
+                const int lim = min(jmax - j, min((int)nrem - t, 32 * (L + 1) - t));
+                const int tend = t + lim;
                 u64* sE = sh.E;
                 u64* sD = sh.D;
-                while (j < jmax && (u32)t < nrem && (t >> 5) == L) {
-                    const bool live = inwin & (me >= (u32)t);
-                    const u32 bal = __ballot_sync(0xffffffffu, live & ((red & jbit) != 0ull));
+                // Short dependent chain per pivot: row t's copy (for the lane
+                // that takes it in the swap) is gathered before the ballot; the
+                // pivot row comes from one shuffle of the ballot's first lane;
+                // the rows to eliminate are the candidates except P (row t has
+                // no bit j unless it is P); they XOR the whole pivot row (their
+                // bits <= j are never read again); every lane writes the same
+                // record (no divergent branch).
+                while (t < tend) {
+                    const u32 tl = (u32)t & 31u;
+                    const u64 rt = shfl64(red, (int)tl), at = shfl64(acc, (int)tl);
+                    const u32 ot = __shfl_sync(0xffffffffu, org, (int)tl);
+                    const bool cand = inwin & (lane >= tl) & ((red & jbit) != 0ull);
+                    const u32 bal = __ballot_sync(0xffffffffu, cand);
                     if (bal == 0u) break;
-                    const u32 pl = (u32)(__ffs(bal) - 1), tl = (u32)t & 31u;
+                    const u32 pl = (u32)(__ffs(bal) - 1);
+                    const u64 pr = shfl64(red, (int)pl), pa = shfl64(acc, (int)pl);
+                    const u32 po = __shfl_sync(0xffffffffu, org, (int)pl);
                     const bool isP = lane == pl;
-                    // one gather: lane P fetches row t (the swap), every other
-                    // lane the pivot row (lane P holds it already)
-                    const int src = (int)(isP ? tl : pl);
-                    const u64 xr = shfl64(red, src), xa = shfl64(acc, src);
-                    const u32 xo = __shfl_sync(0xffffffffu, org, src);
-                    const u64 pred = isP ? red : xr, pacc = isP ? acc : xa;
-                    if (isP) {  // row swap t <-> P (a no-op when P == t)
-                        red = xr;
-                        acc = xa;
-                        org = xo;
-                    }
-                    if (lane == tl && !isP) org = xo;  // slot t records the pivot's origin
-                    const u64 tbit = 1ull << t;
-                    const u64 msk = 0ull - (u64)(live & (me != (u32)t) & ((red & jbit) != 0ull));
-                    const u64 Et = pred & hi, Dt = pacc ^ tbit;
-                    red ^= Et & msk;
-                    acc ^= Dt & msk;
-                    if (lane == 0) {
-                        sE[t] = Et;
-                        sD[t] = Dt;
-                        sh.q[t] = (u32)j;
-                        sh.sw[t] = base + pl;
-                    }
+                    const bool el = cand & !isP;
+                    const u64 Dt = pa ^ tbit;
+                    red = isP ? rt : (el ? red ^ pr : red);
+                    acc = isP ? at : (el ? acc ^ Dt : acc);
+                    org = isP ? ot : (lane == tl ? po : org);
+                    sE[t] = pr & hi;
+                    sD[t] = Dt;
+                    sh.q[t] = (u32)j;
+                    sh.sw[t] = base + pl;
+                    if (stream) st_release_cta(&sh.prog, t + 1);
                     ++t;
                     ++j;
                     jbit <<= 1;
                     hi <<= 1;
+                    tbit <<= 1;
                 }
                 if (lane == 0) {
                     sh.ep_t[epoch & 1] = t;
                     sh.ep_j[epoch & 1] = j;
+                    sh.dbg_lead_cyc += (u32)(clock64() - dbg_c0);
+                    sh.dbg_lead_piv += (u32)(t - dbg_t0);
+                    sh.dbg_epochs += 1u;
+                    if (stream) st_release_cta(&sh.ep_fin, epoch + 1);
                 }
+            } else if (stream && (int)wid > L) {
+                // follow the leader: apply each pivot as it is published
+                int s2 = t;
+                for (;;) {
+                    const int fin = ld_acquire_cta(&sh.ep_fin);
+                    const int pr = ld_acquire_cta(&sh.prog);
+                    for (; s2 < pr; ++s2) {
+                        const u64 msk = 0ull - ((red >> sh.q[s2]) & 1ull);
+                        red ^= sh.E[s2] & msk;
+                        acc ^= sh.D[s2] & msk;
+                    }
+                    if (fin == epoch + 1) break;
+                }
+                t = s2;  // == the epoch's closing t (prog is final once fin is set)
             }
             named_bar(3, kWin);
             const int t1 = sh.ep_t[epoch & 1], j1 = sh.ep_j[epoch & 1];
@@ -693,10 +745,15 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             if (j >= jmax || (u32)t >= nrem) break;
             if ((t >> 5) != L) continue;  // the leader's rows are used up: next leader
             const int st = cross_step(j);
+            if (me == 0) sh.dbg_cross += 1u;
             if (st == 2) break;
             ++j;
         }
         if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 7] = globaltimer();
+        if (p.phase_ns) named_bar(3, kWin);
+        if (p.phase_ns && me == 0)
+            p.phase_ns[(size_t)w * 8 + 4] = ((u64)sh.dbg_lead_cyc << 32) | (sh.dbg_lead_piv << 16) |
+                                            (sh.dbg_cross << 8) | sh.dbg_epochs;
         sh.dacc[me] = acc;
         sh.dorg[me] = org;
         // the writeback below may only land after the workers are done with

@@ -402,6 +402,12 @@ __device__ __forceinline__ void stamp2(const Params& p, u32 w, u32 k) {
     if (p.phase_ns && threadIdx.x == 0) p.phase_ns[(size_t)w * 8 + k] = globaltimer();
 }
 
+// diagnostics (GF2CU_DUMP_WORKERS): per super-step x worker {wake, pre-work
+// end, rest start, rest end}
+__device__ __forceinline__ void wstamp(const Params& p, u32 S, u32 wk, u32 nworkers, u32 k) {
+    if (p.worker_ns && threadIdx.x == 0) p.worker_ns[((size_t)S * nworkers + wk) * 4 + k] = globaltimer();
+}
+
 // One launch, grid = #SMs: CTA 0 runs the panels, CTAs 1.. the sweep. `nss` =
 // number of super-steps (ceil(W / 2)). panel_done counts published super-steps.
 __global__ void __launch_bounds__(kTrailThreads, 1)
@@ -480,6 +486,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         }
         __syncthreads();
         if (wk == 0) stamp2(p, w, 2);
+        wstamp(p, S, wk, nworkers, 0);
 
         // Pre-work chunks: the look-ahead tile was the previous super-step's
         // (every row final there) unless the window just entered a new tile.
@@ -517,6 +524,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                 red_release_add(&p.ap_done[S], mine);
             }
         }
+        wstamp(p, S, wk, nworkers, 1);
         // the rest: after super-step S-1 everywhere (pivot rows' raw tails)
         // and all of S's pre-work (every row's info / compressed words)
         if (threadIdx.x == 0)
@@ -538,6 +546,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             }
         }
         if (wk == 0) stamp2(p, w, 3);
+        wstamp(p, S, wk, nworkers, 2);
         if (sweep) {
             const u32 nt = (p.Wpad8 >> 2) - ct - 1;  // Wpad8 holds Wpad4 here
             const u64 total = (u64)nt * nrows;
@@ -556,6 +565,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                 u += cnt;
             }
         }
+        wstamp(p, S, wk, nworkers, 3);
         cta_arrive(&sy->t_count);
         if (wk == 0) stamp2(p, w, 5);
     }
