@@ -155,6 +155,14 @@ __device__ __forceinline__ u64* tword(u64* mat, u32 m, u32 row, u32 x) {
 __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+// Barrier of the `nthr` threads running panel_factor_body (all of the CTA,
+// or all but the persistent drivers' signal warp).
+constexpr int kBodyBar = 4;
+// Persistent drivers: body threads -> signal warp hand-off after each panel.
+constexpr int kSignalBar = 5;
 
 __device__ __forceinline__ u64 shfl64(u64 v, int src) {
     return __shfl_sync(0xffffffffu, v, src);
@@ -346,6 +354,7 @@ struct PanelShared {
     u32 qa[64];
     u32 rba;
     u32 dbg_lead_cyc, dbg_lead_piv, dbg_cross, dbg_epochs;  // diagnostics (phase_ns slot 4)
+    int sig_step, sig_err;  // persistent drivers: body -> signal thread, error seen
     int prog;    // pivots the leader has published (kPanelStream)
     int ep_fin;  // epoch + 1 once the leader closed it (kPanelStream)
 };
@@ -474,13 +483,13 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         sh.cap_ok = la ? (la->cap_target == 0 ? 1 : 0) : 1;
         sh.super = la ? la->super_mode : 0;
     }
-    __syncthreads();
+    named_bar(kBodyBar, nthr);
     if (sh.super == 1 && !sh.cap_ok) {
         // panel a reads its window from the previous super-step's capture
         if (threadIdx.x == 0)
             sh.cap_ok = (la->sys ? spin_geq_sys(la->cap_ctr, la->cap_target, la->err)
                                  : spin_geq(la->cap_ctr, la->cap_target, la->err)) ? 1 : -1;
-        __syncthreads();
+        named_bar(kBodyBar, nthr);
     }
     const u32 r = sh.r;
     if (threadIdx.x == 0) {
@@ -499,7 +508,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             p.status[kStatusRb] = 0u;
             p.status[kStatusR] = r;
         }
-        __syncthreads();
+        named_bar(kBodyBar, nthr);
         return 0;
     }
     const u32 nrem = p.m - r;
@@ -803,7 +812,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             sh.epb2[me] = f_epb2;
         }
     }
-    __syncthreads();
+    named_bar(kBodyBar, nthr);
     if (sh.t < 0) {
         // aborted: state stays {r, 0}, so running the step again is exact
         if (threadIdx.x == 0 && p.status) {
@@ -811,14 +820,14 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             p.status[kStatusRb] = 0u;
             p.status[kStatusR] = r;
         }
-        __syncthreads();
+        named_bar(kBodyBar, nthr);
         return 0;
     }
     const u32 t = (u32)sh.t;
     if (p.status) {
         // sharded driver: which rank owns each pivot row
         for (u32 k = threadIdx.x; k < 2u * p.nranks; k += nthr) p.status[kStatusOwners + k] = 0u;
-        __syncthreads();
+        named_bar(kBodyBar, nthr);
         for (u32 k = threadIdx.x; k < t; k += nthr) {
             const u32 g = p.perm[r + k];
             const u32 o = (g / p.block) % p.nranks;
@@ -845,7 +854,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             __threadfence_system();
         }
     }
-    __syncthreads();
+    named_bar(kBodyBar, nthr);
     if (sh.super == 2) {
         // panel b: panel-a combination of each of its pivot rows
         for (u32 k = threadIdx.x; k < t; k += nthr) {
@@ -879,7 +888,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                                           : sh.lpb2[o & 127u];
             if (sh.super) la->piv2_out[k] = sh.piv2[k];
         }
-        __syncthreads();
+        named_bar(kBodyBar, nthr);
         for (u32 k = threadIdx.x; k < nwin1; k += nthr) {
             const u32 q = r1 + k;  // position
             u64 d, pre;
@@ -906,7 +915,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             sh.nraw[k] = x;
             sh.ndacc[k] = d;
         }
-        __syncthreads();
+        named_bar(kBodyBar, nthr);
     }
     return t;
 }

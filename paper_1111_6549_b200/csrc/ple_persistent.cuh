@@ -37,6 +37,44 @@ __device__ __forceinline__ void cta_arrive(u32* ctr) {
     }
 }
 
+// Panel CTA of the persistent drivers: the last warp only signals. After each
+// panel the body threads sync among themselves and thread 0 publishes the step
+// in shared memory (release, CTA scope); one signal thread acquires it, fences
+// the panel's global outputs and publishes the step to the workers
+// (panel_done), and polls the error word -- so the fence latency is off the
+// panels' critical path. Spins have the watchdog; a step index of
+// 0x80000000 | (w + 1) means "last step".
+__device__ __forceinline__ void signal_step(PanelShared& sh, int nbody, u32 w, bool last) {
+    named_bar(kBodyBar, nbody);
+    if (threadIdx.x == 0) st_release_cta(&sh.sig_step, (int)((w + 1u) | (last ? 0x80000000u : 0u)));
+}
+
+__device__ __noinline__ void signal_loop(PanelShared& sh, SyncState* sy, u32 nsteps) {
+    for (u32 w = 0; w < nsteps; ++w) {
+        const u64 t0 = globaltimer();
+        u32 st;
+        for (u32 spin = 0;; ++spin) {
+            st = (u32)ld_acquire_cta(&sh.sig_step);
+            if ((st & 0x7fffffffu) >= w + 1u) break;
+            if ((spin & 255u) == 255u) {
+                if (*(volatile u32*)&sy->error) {
+                    *(volatile int*)&sh.sig_err = 1;
+                    return;
+                }
+                if (globaltimer() - t0 > g_watchdog_ns) {
+                    atomicExch(&sy->error, 1u);
+                    *(volatile int*)&sh.sig_err = 1;
+                    return;
+                }
+            }
+        }
+        __threadfence();
+        red_release_add(&sy->panel_done, 1u);
+        if (*(volatile u32*)&sy->error) *(volatile int*)&sh.sig_err = 1;
+        if (st & 0x80000000u) return;
+    }
+}
+
 __device__ __forceinline__ void stamp(const Params& p, u32 w, u32 k) {
     if (p.phase_ns && threadIdx.x == 0) p.phase_ns[(size_t)w * 8 + k] = globaltimer();
 }
@@ -55,6 +93,19 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
         // Look-ahead: step w+1's window words are computed at the end of step
         // w, so the next factorization starts at once; only its scans and its
         // writeback wait for the workers' look-ahead capture of step w.
+        // The last warp only signals: after each panel it fences the panel's
+        // global outputs and publishes the step (and polls the error word),
+        // while the other warps go on with the next panel.
+        const int nbody = (int)blockDim.x - 32;
+        if (threadIdx.x == 0) {
+            psh.sig_step = 0;
+            psh.sig_err = 0;
+        }
+        __syncthreads();
+        if ((int)threadIdx.x >= nbody) {
+            if (threadIdx.x == (u32)nbody) signal_loop(psh, sy, nsteps);
+            return;
+        }
         LookAhead la{0u, false, p.ap_done, 0u, &sy->error};
         u32 prev_r = 0u;
         for (u32 w = 0; w < nsteps; ++w) {
@@ -63,12 +114,16 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
             la.cap_target = w > 0 ? pw_chunks(p.m - prev_r, p.pw_div) : 0u;
             prev_r = la.r;
             stamp(p, w, 0);
-            const u32 rb = panel_factor_body(p, w, psh, blockDim.x, &la);
+            const u32 rb = panel_factor_body(p, w, psh, nbody, &la);
             stamp(p, w, 1);
-            if (*(volatile u32*)&sy->error) return;
+            // (an aborted panel returns 0: then check the error word itself)
+            if (rb == 0u && *(volatile u32*)&sy->error) {
+                if (threadIdx.x == 0) st_release_cta(&psh.sig_step, (int)(0x80000000u | (w + 1u)));
+                return;
+            }
             const bool done = la.r >= p.m;
-            cta_arrive(&sy->panel_done);
-            if (done) return;
+            signal_step(psh, nbody, w, done);
+            if (done || *(volatile int*)&psh.sig_err) return;
             la.r += rb;
             la.have_window = true;
         }

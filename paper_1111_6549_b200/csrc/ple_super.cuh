@@ -28,6 +28,7 @@
 #pragma once
 
 #include "ple_kernels.cuh"
+#include "ple_persistent.cuh"
 
 namespace gf2cu {
 
@@ -422,6 +423,17 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
 
     if (blockIdx.x == 0) {
         // ------------------------------------------------------ panel CTA
+        // (the last warp only signals; see signal_step)
+        const int nbody = (int)blockDim.x - 32;
+        if (threadIdx.x == 0) {
+            psh.sig_step = 0;
+            psh.sig_err = 0;
+        }
+        __syncthreads();
+        if ((int)threadIdx.x >= nbody) {
+            if (threadIdx.x == (u32)nbody) signal_loop(psh, sy, nss);
+            return;
+        }
         LookAhead la{0u, false, p.ap_done, 0u, &sy->error};
         la.piv2_out = so->piv2;
         la.C_out = so->C;
@@ -440,8 +452,9 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             la.super_mode = 1;
             la.have_window = false;
             stamp2(p, w, 0);
-            const u32 rba = panel_factor_body(p, w, psh, blockDim.x, &la);
-            if (*(volatile u32*)&sy->error) return;
+            const u32 rba = panel_factor_body(p, w, psh, nbody, &la);
+            // (an aborted panel returns 0: then check the error word itself)
+            if (*(volatile int*)&psh.sig_err || (rba == 0u && *(volatile u32*)&sy->error)) return;
             la.r += rba;
             if (w + 1u < p.W) {
                 if (!done0 && la.r < p.m) {
@@ -450,8 +463,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                     la.super_mode = 2;
                     la.have_window = true;
                     la.cap_target = 0u;
-                    const u32 rbb = panel_factor_body(pb_par, w + 1u, psh, blockDim.x, &la);
-                    if (*(volatile u32*)&sy->error) return;
+                    const u32 rbb = panel_factor_body(pb_par, w + 1u, psh, nbody, &la);
+                    if (*(volatile int*)&psh.sig_err || (rbb == 0u && *(volatile u32*)&sy->error)) return;
                     la.r += rbb;
                 } else if (threadIdx.x == 0) {
                     p.rhist[w + 1u] = la.r;
@@ -459,8 +472,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                 }
             }
             stamp2(p, w, 1);
-            cta_arrive(&sy->panel_done);
-            if (done0) return;
+            signal_step(psh, nbody, S, done0);
+            if (done0 || *(volatile int*)&psh.sig_err) return;
         }
         return;
     }
