@@ -35,6 +35,12 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// The super-step driver (two panels per sweep) from this many matrix words up,
+// the single-panel persistent driver below: measured crossover between 6.5M
+// (20480^2: single-panel 6.0 vs 6.2 ms) and 8.4M words (16384x32768: 5.9 vs
+// 5.3 ms; 8192x65536, 32768x16384 and 65536x8192 also favour two panels).
+constexpr double kSuperStepWords = 8388608.0;
+
 // Panel tuning bits (gf2cu::kPanel*); GF2CU_PANEL_FLAGS overrides the default
 // for A/B measurements.
 u32 panel_flags() {
@@ -355,7 +361,7 @@ gf2cu_status peer_reset_rank(const gf2cu::PeerParams& h, cudaStream_t s) {
 bool peer_super(size_t m, size_t W, unsigned flags) {
     if (const char* e = std::getenv("GF2CU_PEER_SUPER")) return std::atoi(e) != 0;
     if (flags & GF2CU_FLAG_SINGLE_PANEL) return false;
-    return (flags & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= 16777216.0;
+    return (flags & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= kSuperStepWords;
 }
 
 gf2cu_status peer_launch(const gf2cu::PeerParams* dp, unsigned ranks_here, unsigned cpr, size_t W,
@@ -600,7 +606,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     // it pays from ~2^24 matrix words up (measured crossover near 32768^2).
     const unsigned fl = cfg ? cfg->flags : 0u;
     const bool super = !multi && !(fl & GF2CU_FLAG_SINGLE_PANEL) &&
-                       ((fl & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= 16777216.0);
+                       ((fl & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= kSuperStepWords);
     const u32 Wpad4 = (u32)std::max<size_t>(4, (W + 3) / 4 * 4);
     if (!multi) {
         if (!ws.ubuf) {

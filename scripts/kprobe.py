@@ -1,6 +1,7 @@
 """Median kernel time (CUDA events around the persistent launch) of the
 device-resident PLE of ctr(seed 1) matrices, with the result checksum.
 usage: python scripts/kprobe.py [n ...]   (n or MxN)"""
+import os
 import sys
 
 import numpy as np
@@ -14,7 +15,9 @@ for arg in sys.argv[1:] or ["4096", "16384", "32768", "65536"]:
     ks = []
     for it in range(6):
         a.copy_from(b)
-        o = G.block_iterative_ple(a, G.PleConfig(time_kernels=True))
+        drv = os.environ.get("KPROBE_DRIVER", "")
+        o = G.block_iterative_ple(a, G.PleConfig(time_kernels=True, single_panel=drv == "single",
+                                                 super_step=drv == "super"))
         if it:
             ks.append(o.stats["kernel_ms"])
     print(f"{m}x{n}: kernel median {np.median(ks):.3f} ms (min {min(ks):.3f}) rank {o.rank} "

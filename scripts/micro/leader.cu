@@ -243,6 +243,87 @@ __global__ void v1(const u64* in, Out* out, int reps) {
     }
 }
 
+// V5: V1 with the pivot row broadcast by redux.sync.or (no FLO/BREV on the chain). The pivot row comes from one shuffle of the ballot's
+// first lane (no lane-dependent source select), row t's copy for lane P from a
+// shuffle issued before the ballot; eliminated rows XOR the whole pivot row
+// (their bits <= j are never read again); the lanes to eliminate are the
+// ballot's candidates except P (row t had no bit j unless it is P); pivot
+// records are kept in the lane of their slot (no divergent stores).
+__global__ void v5(const u64* in, Out* out, int reps) {
+    __shared__ u64 sE[64], sD[64];
+    __shared__ u32 sq[64], ssw[64];
+    const u32 lane = threadIdx.x;
+    long long tot = 0;
+    int t = 0;
+    u64 red, acc;
+    u32 org;
+    for (int rep = 0; rep < reps; ++rep) {
+        red = in[blockIdx.x * 32 + lane];
+        acc = 0;
+        org = lane;
+        t = 0;
+        u64 myE = 0, myD = 0;
+        u32 myq = 0, mysw = 0;
+        __syncwarp();
+        const long long c0 = clock64();
+        for (int j = 0; j < 64 && t < 32; ++j) {
+            u64 jbit = 1ull << j;
+            while (j < 64 && t < 32) {
+                const u32 tl = (u32)t;
+                // row t, for the lane that will hold it after the swap
+                const u64 rt = shfl64(red, (int)tl), at = shfl64(acc, (int)tl);
+                const u32 ot = __shfl_sync(0xffffffffu, org, (int)tl);
+                const bool cand = (lane >= tl) & ((red & jbit) != 0ull);
+                const u32 bal = __ballot_sync(0xffffffffu, cand);
+                if (bal == 0u) break;
+                const bool isP = ((bal & (0u - bal)) >> lane) & 1u;
+                const u64 mine = isP ? red : 0ull;
+                const u64 pr = ((u64)__reduce_or_sync(0xffffffffu, (u32)(mine >> 32)) << 32) |
+                               __reduce_or_sync(0xffffffffu, (u32)mine);
+                const u32 pl = (u32)(__ffs(bal) - 1);
+                const u64 pa = shfl64(acc, (int)pl);
+                const u32 po = __shfl_sync(0xffffffffu, org, (int)pl);
+                const u64 Dt = pa ^ (1ull << t);
+                const bool el = cand & !isP;
+                red = isP ? rt : (el ? red ^ pr : red);
+                acc = isP ? at : (el ? acc ^ Dt : acc);
+                org = isP ? ot : (lane == tl ? po : org);
+                if (lane == tl) {  // predicated, the slot's own record
+                    myE = pr & ~(jbit | (jbit - 1));
+                    myD = Dt;
+                    myq = (u32)j;
+                    mysw = pl;
+                }
+                ++t;
+                ++j;
+                jbit <<= 1;
+            }
+        }
+        if ((int)lane < t) {
+            sE[lane] = myE;
+            sD[lane] = myD;
+            sq[lane] = myq;
+            ssw[lane] = mysw;
+        }
+        __syncwarp();
+        tot += clock64() - c0;
+    }
+    __syncwarp();
+    Out& o = out[blockIdx.x];
+    for (int k = lane; k < t; k += 32) {
+        o.E[k] = sE[k];
+        o.D[k] = sD[k];
+        o.q[k] = sq[k];
+        o.sw[k] = ssw[k];
+    }
+    o.org[lane] = org;
+    o.acc[lane] = acc;
+    if (lane == 0) {
+        o.cyc = tot;
+        o.t = t;
+    }
+}
+
 // V2: two columns per ballot round. Ballots of bits j and j+1 decide both
 // pivots with warp-uniform integer logic: after pivot P0 (column j), row i's
 // bit j+1 is b1_i ^ (e & b0_i) with e = the pivot row's bit j+1, and the old
@@ -370,6 +451,98 @@ __global__ void v2(const u64* in, Out* out, int reps) {
     }
 }
 
+// V3: decision warp + shadow warp. Warp 0 keeps only the reduced rows (red)
+// and publishes each pivot's ballot; warp 1 holds the same rows' combinations
+// (acc) and origins (org) and replays the swaps / eliminations from the
+// published ballots, off the decision chain.
+__global__ void __launch_bounds__(64, 1) v3(const u64* in, Out* out, int reps) {
+    __shared__ u64 sE[64], sD[64];
+    __shared__ u32 sq[64], ssw[64], sbal[64];
+    __shared__ volatile int sprog;
+    __shared__ int sfin;
+    const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    long long tot = 0;
+    int t = 0;
+    u64 red = 0, acc = 0;
+    u32 org = lane;
+    for (int rep = 0; rep < reps; ++rep) {
+        if (threadIdx.x == 0) { sprog = 0; sfin = -1; }
+        __syncthreads();
+        t = 0;
+        if (wid == 0) {
+            red = in[blockIdx.x * 32 + lane];
+            const long long c0 = clock64();
+            for (int j = 0; j < 64 && t < 32; ++j) {
+                u64 jbit = 1ull << j;
+                while (j < 64 && t < 32) {
+                    const u32 tl = (u32)t;
+                    const u64 rt = shfl64(red, (int)tl);
+                    const bool cand = (lane >= tl) & ((red & jbit) != 0ull);
+                    const u32 bal = __ballot_sync(0xffffffffu, cand);
+                    if (bal == 0u) break;
+                    const u32 pl = (u32)(__ffs(bal) - 1);
+                    const u64 pr = shfl64(red, (int)pl);
+                    const bool isP = lane == pl;
+                    red = isP ? rt : ((cand & !isP) ? red ^ pr : red);
+                    sE[t] = pr & ~(jbit | (jbit - 1));
+                    sq[t] = (u32)j;
+                    *(volatile u32*)&sbal[t] = bal;
+#ifndef NOFENCE
+                    __threadfence_block();
+#endif
+                    sprog = t + 1;
+                    ++t;
+                    ++j;
+                    jbit <<= 1;
+                }
+            }
+            if (lane == 0) { __threadfence_block(); *(volatile int*)&sfin = t; }
+            __syncwarp();
+            tot += clock64() - c0;
+        } else {
+            acc = 0;
+            org = lane;
+            int s = 0;
+            for (;;) {
+                const int fin = *(volatile int*)&sfin;
+                const int pr = sprog;
+                for (; s < pr; ++s) {
+                    const u32 bal = *(volatile u32*)&sbal[s];
+                    const u32 tl = (u32)s, pl = (u32)(__ffs(bal) - 1);
+                    const u64 at = shfl64(acc, (int)tl), pa = shfl64(acc, (int)pl);
+                    const u32 ot = __shfl_sync(0xffffffffu, org, (int)tl), po = __shfl_sync(0xffffffffu, org, (int)pl);
+                    const bool isP = lane == pl;
+                    const bool el = ((bal >> lane) & 1u) & !isP;
+                    const u64 Dt = pa ^ (1ull << s);
+                    acc = isP ? at : (el ? acc ^ Dt : acc);
+                    org = isP ? ot : (lane == tl ? po : org);
+                    sD[s] = Dt;
+                    ssw[s] = pl;
+                }
+                if (fin >= 0 && s >= fin) break;
+            }
+            t = s;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    Out& o = out[blockIdx.x];
+    if (wid == 1) {
+        for (int k = lane; k < t; k += 32) {
+            o.E[k] = sE[k];
+            o.D[k] = sD[k];
+            o.q[k] = sq[k];
+            o.sw[k] = ssw[k];
+        }
+        o.org[lane] = org;
+        o.acc[lane] = acc;
+    }
+    if (threadIdx.x == 0) {
+        o.cyc = tot;
+        o.t = t;
+    }
+}
+
 int main(int argc, char** argv) {
     const int nb = 64, reps = 200;
     u64* h = (u64*)malloc(nb * 32 * 8);
@@ -392,6 +565,8 @@ int main(int argc, char** argv) {
     v1<<<nb, 32>>>(d, o1, reps);
     v2<<<nb, 32>>>(d, o2, reps);
     if (getenv("V0B")) v0b<<<nb, 512>>>(d, o2, reps);
+    if (getenv("V3")) v3<<<nb, 64>>>(d, o2, reps);
+    if (getenv("V5")) v5<<<nb, 32>>>(d, o2, reps);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("cuda error %s\n", cudaGetErrorString(e)); return 1; }
     Out* a = (Out*)malloc(nb * sizeof(Out));
