@@ -10,11 +10,12 @@ import numpy as np
 
 import paper_1111_6549_b200 as G
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+arg = sys.argv[1] if len(sys.argv) > 1 else "65536"
+m, n = (int(x) for x in arg.split("x")) if "x" in arg else (int(arg), int(arg))
 out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/workers_super.bin"
 if n > 0:
-    a = G.DeviceMatrix(n, n)
-    b = G.DeviceMatrix(n, n)
+    a = G.DeviceMatrix(m, n)
+    b = G.DeviceMatrix(m, n)
     b.fill_ctr(1)
     for it in range(3):
         a.copy_from(b)

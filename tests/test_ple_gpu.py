@@ -230,3 +230,21 @@ def test_streamed_output_matches_device(m, n):
     assert got.rank == want.rank
     assert np.array_equal(got.q, want.q) and np.array_equal(got.p.swaps, want.p.swaps)
     assert np.array_equal(bm.words, d.download())
+
+
+@pytest.mark.parametrize("m,n,driver", [(8192, 65536, 2), (20480, 20480, 1), (16384, 32768, 2),
+                                        (16384, 16384, 1)])
+def test_default_driver_size_rule(m, n, driver):
+    """Without a driver flag the super-step driver runs from 2^23 matrix words
+    (m * ceil(n/64)) up, the single-panel persistent driver below (the measured
+    crossover); both give the device-resident ctr result
+    the other driver gives."""
+    d = G.DeviceMatrix(m, n)
+    d.fill_ctr(9)
+    e = G.DeviceMatrix(m, n)
+    e.copy_from(d)
+    got = G.block_iterative_ple(d)
+    assert got.stats["driver"] == driver
+    other = G.block_iterative_ple(e, G.PleConfig(single_panel=True) if driver == 2 else G.PleConfig(super_step=True))
+    assert other.rank == got.rank and np.array_equal(other.q, got.q)
+    assert d.checksum() == e.checksum()
