@@ -266,23 +266,18 @@ __device__ __forceinline__ void lookup16_consts(u32 rq, u32 h, u32 sel[4], u32 k
     }
 }
 
-// Gray walk (gray_code.hpp:105-112) of the 16 tables for one 32-byte tile
-// from the raw pivot rows of both panels (pa / pb = their physical rows;
-// words <= w+1 of the tile read as zero). Thread layout (512): h = tid & 1,
-// t & 3 = (tid >> 1) & 3, seg_lo = (tid >> 3) & 3, t >> 2 = (tid >> 5) & 3,
-// seg_hi = (tid >> 7) & 3; each thread walks 16 entries of one table half.
-__device__ __forceinline__ void build16(const Params& p, unsigned char* smem, u32 tile, u32 w,
-                                        const u32* pa, u32 rba, const u32* pb, u32 rbb) {
+// (split in two so that a pre-work chunk can issue the source loads before
+// its apply and walk after it: the load latency overlaps the apply)
+__device__ __forceinline__ void build16_load(const Params& p, u32 tile, u32 w, const u32* pa, u32 rba,
+                                             const u32* pb, u32 rbb, ulonglong2 R[8]) {
     const u32 tid = threadIdx.x;
     const u32 h = tid & 1u;
     const u32 t = (((tid >> 5) & 3u) << 2) | ((tid >> 1) & 3u);
-    const u32 sg = (((tid >> 7) & 3u) << 2) | ((tid >> 3) & 3u);
     const u32 x0 = tile * 4u;
     const u32 zlim = w + 2u > x0 ? min(w + 2u - x0, 4u) : 0u;  // words <= w+1
     const u32* src = t < 8u ? pa : pb;
     const u32 nsrc = t < 8u ? rba : rbb;
     const u32 base = 8u * (t & 7u);
-    ulonglong2 R[8];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
         ulonglong2 v = make_ulonglong2(0ull, 0ull);
@@ -292,6 +287,13 @@ __device__ __forceinline__ void build16(const Params& p, unsigned char* smem, u3
         if (2u * h + 1u < zlim) v.y = 0ull;
         R[b] = v;
     }
+}
+
+__device__ __forceinline__ void build16_walk(unsigned char* smem, const ulonglong2 R[8]) {
+    const u32 tid = threadIdx.x;
+    const u32 h = tid & 1u;
+    const u32 t = (((tid >> 5) & 3u) << 2) | ((tid >> 1) & 3u);
+    const u32 sg = (((tid >> 7) & 3u) << 2) | ((tid >> 3) & 3u);
     const u32 i0 = 16u * sg;
     const u32 e0 = i0 ^ (i0 >> 1);
     ulonglong2 acc = make_ulonglong2(0ull, 0ull);
@@ -306,6 +308,18 @@ __device__ __forceinline__ void build16(const Params& p, unsigned char* smem, u3
         const u32 i = i0 + k;
         *reinterpret_cast<ulonglong2*>(smem + tab16_off(t, i ^ (i >> 1), h)) = acc;
     }
+}
+
+// Gray walk (gray_code.hpp:105-112) of the 16 tables for one 32-byte tile
+// from the raw pivot rows of both panels (pa / pb = their physical rows;
+// words <= w+1 of the tile read as zero). Thread layout (512): h = tid & 1,
+// t & 3 = (tid >> 1) & 3, seg_lo = (tid >> 3) & 3, t >> 2 = (tid >> 5) & 3,
+// seg_hi = (tid >> 7) & 3; each thread walks 16 entries of one table half.
+__device__ __forceinline__ void build16(const Params& p, unsigned char* smem, u32 tile, u32 w,
+                                        const u32* pa, u32 rba, const u32* pb, u32 rbb) {
+    ulonglong2 R[8];
+    build16_load(p, tile, w, pa, rba, pb, rbb, R);
+    build16_walk(smem, R);
 }
 
 constexpr u32 kRows16 = kTrailThreads / 2 * kUnroll;  // 1024 rows per iteration
@@ -416,7 +430,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ PanelShared psh;
     __shared__ ApplyShared2 ash;
-    __shared__ u32 s_ok;
+    __shared__ u32 s_ok, s_claim;
     __shared__ u32 s_pa[64], s_pb[64];
     SyncState* sy = p.sync;
     const u32 nworkers = gridDim.x - 1;
@@ -482,6 +496,8 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
     const u32 wk = blockIdx.x - 1;
     for (u32 S = 0; S < nss; ++S) {
         if (!cta_wait(sy, &sy->panel_done, S + 1, s_ok)) return;
+        // the first pre-work claim now: its latency overlaps the loads below
+        if (threadIdx.x == 0) s_claim = atomicAdd(&p.ap_claim[S], 1u);
         const u32 w = 2u * S;
         const bool has_b = w + 1u < p.W;
         const u32 r = *(volatile u32*)&p.rhist[w], rba = *(volatile u32*)&p.rbhist[w];
@@ -505,14 +521,18 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         // (every row final there) unless the window just entered a new tile.
         const bool early = S == 0 || ct == (w >> 2);
         if (sweep && !early && !cta_wait(sy, &sy->t_count, nworkers * S, s_ok)) return;
+        // Per chunk: apply, then sweep the chunk's rows over the look-ahead
+        // tile. Its tables are built once per super-step (the same for every
+        // chunk).
         u32 mine = 0;
-        bool loaded = false;
-        for (;;) {
-            if (threadIdx.x == 0) s_ok = atomicAdd(&p.ap_claim[S], 1u);
+        bool loaded = false, built = false;
+        for (bool first = true;; first = false) {
+            if (!first && threadIdx.x == 0) s_claim = atomicAdd(&p.ap_claim[S], 1u);
             __syncthreads();
-            const u32 c = s_ok;
+            const u32 c = s_claim;
             __syncthreads();
             if (c >= nch) break;
+            const bool build = sweep && rba + rbb > 0 && !built;
             if (!loaded) {  // the panel outputs stay S's while any chunk of S is open
                 apply2_load(p, p.pout, pout_b, so, ash, rba, rbb);
                 __syncthreads();
@@ -522,9 +542,10 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             apply2_rows(q, ash, w, r, rba, rbb, has_b, a0, a1, threadIdx.x, blockDim.x);
             if (sweep) {
                 __syncthreads();
-                if (rba + rbb > 0) {
+                if (build) {
                     build16(q, smem, ct, w, s_pa, rba, s_pb, rbb);
                     __syncthreads();
+                    built = true;
                 }
                 trail16_rows(q, smem, w, r, ct, a0 - r, a1 - a0, rba + rbb);
             }
