@@ -16,8 +16,9 @@ for arg in sys.argv[1:] or ["4096", "16384", "32768", "65536"]:
     for it in range(6):
         a.copy_from(b)
         drv = os.environ.get("KPROBE_DRIVER", "")
+        peer = int(os.environ.get("KPROBE_PEER", "0"))  # emulated peer ranks (one launch)
         o = G.block_iterative_ple(a, G.PleConfig(time_kernels=True, single_panel=drv == "single",
-                                                 super_step=drv == "super"))
+                                                 super_step=drv == "super", peer_ranks=peer))
         if it:
             ks.append(o.stats["kernel_ms"])
     print(f"{m}x{n}: kernel median {np.median(ks):.3f} ms (min {min(ks):.3f}) rank {o.rank} "
