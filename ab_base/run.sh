@@ -7,8 +7,8 @@ mkdir -p ab_base/new
 for f in ab_base/base/*; do cp paper_1111_6549_b200/csrc/$(basename $f) ab_base/new/; done
 build() { python -c "from paper_1111_6549_b200 import _lib; _lib.build(force=True)" >/dev/null 2>&1; }
 for round in 1 2; do
-  echo "== new"; python scripts/kprobe.py $SIZES
+  echo "== new"; ${CMD:-python scripts/kprobe.py $SIZES}
   cp ab_base/base/* paper_1111_6549_b200/csrc/; build
-  echo "== base"; python scripts/kprobe.py $SIZES
+  echo "== base"; ${CMD:-python scripts/kprobe.py $SIZES}
   cp ab_base/new/* paper_1111_6549_b200/csrc/; build
 done

@@ -92,6 +92,7 @@ struct Workspace {
     u64* ubuf = nullptr;         // persistent driver: swept pivot-row tails
     size_t ucap = 0;
     u32* apctr = nullptr;        // persistent driver: per-step pre-work chunk counters
+    u32* h_out = nullptr;        // pinned host staging of swaps / q (2 x min(m, n))
     gf2cu::PanelOut* pout_b = nullptr;  // super-step driver: panel b's outputs
     gf2cu::SuperOut* sout = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -114,6 +115,7 @@ void free_ws(Workspace& w) {
     cudaFree(w.phase_ns);
     cudaFree(w.ubuf);
     cudaFree(w.apctr);
+    cudaFreeHost(w.h_out);
     cudaFree(w.pout_b);
     cudaFree(w.sout);
     if (w.host_r) cudaFreeHost(w.host_r);
@@ -769,6 +771,14 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     CU_TRY(cudaStreamSynchronize(s));
     const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
 
+    // swaps / q to pinned staging first (they do not depend on the untile)
+    if (rk && !ws.h_out) CU_TRY(cudaMallocHost(&ws.h_out, 2 * std::min(m, n) * sizeof(u32)));
+    u32* sw = ws.h_out;
+    u32* qq = ws.h_out + std::min(m, n);
+    if (rk) {
+        CU_TRY(cudaMemcpyAsync(sw, ws.swaps, rk * sizeof(u32), cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaMemcpyAsync(qq, ws.qcol, rk * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    }
     // back to the row-major public layout, rows gathered into position order
     if (super) {
         gf2cu::untile4_kernel<<<sms * 8, 256, 0, s>>>(a->alt, a->data, ws.perm, (u32)m, (u32)a->Wp,
@@ -781,11 +791,6 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     CU_TRY(cudaGetLastError());
     if (rows_streamed) *rows_streamed = sent;
 
-    std::vector<u32> sw(rk), qq(rk);
-    if (rk) {
-        CU_TRY(cudaMemcpyAsync(sw.data(), ws.swaps, rk * sizeof(u32), cudaMemcpyDeviceToHost, s));
-        CU_TRY(cudaMemcpyAsync(qq.data(), ws.qcol, rk * sizeof(u32), cudaMemcpyDeviceToHost, s));
-    }
     CU_TRY(cudaStreamSynchronize(s));
     *rank = rk;
     size_t ncs = 0;
