@@ -45,7 +45,7 @@ constexpr double kSuperStepWords = 8388608.0;
 // for A/B measurements.
 u32 panel_flags() {
     const char* e = std::getenv("GF2CU_PANEL_FLAGS");
-    return e ? (u32)std::strtoul(e, nullptr, 0) : gf2cu::kPanelStream;
+    return e ? (u32)std::strtoul(e, nullptr, 0) : (gf2cu::kPanelStream | gf2cu::kPanelSuperLA);
 }
 
 gf2cu_status fail(gf2cu_status st, const std::string& msg) {

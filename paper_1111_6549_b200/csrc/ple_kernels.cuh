@@ -115,6 +115,9 @@ struct Params {
 // Params::pflags: the window warps behind the leader apply its pivots as it
 // publishes them (instead of all at the epoch's closing barrier).
 constexpr u32 kPanelStream = 1u;
+// ... the super-step driver's panel CTA computes the next panel a's window
+// itself when the workers are ahead (ple_super.cuh, super_la_gather).
+constexpr u32 kPanelSuperLA = 2u;
 
 // Panel status words written when Params::status is set.
 constexpr int kStatusMiss = 0;   // 1 = aborted on a window miss (window_only)
@@ -355,6 +358,15 @@ struct PanelShared {
     u32 rba;
     u32 dbg_lead_cyc, dbg_lead_piv, dbg_cross, dbg_epochs;  // diagnostics (phase_ns slot 4)
     int sig_step, sig_err;  // persistent drivers: body -> signal thread, error seen
+    // super-step driver, look-ahead across super-steps (ple_super.cuh,
+    // super_la_gather / super_la_compute): the next panel a's window
+    u64 la_m2[kWin], la_m3[kWin];  // pre-super-step words w+2, w+3; then the window words
+    u64 la_e0[kWin], la_e1[kWin];  // entering rows: raw words w, w+1; window rows: d_a, d_b
+    u64 la_R2[128], la_R3[128];    // both panels' pivot rows: pre-super-step words w+2, w+3
+    u64 la_C[64];                  // panel b's pivots' panel-a combinations
+    u32 la_phys[kWin];
+    unsigned char la_ent[kWin];    // 1: the row entered (outside panel b's window)
+    int la_go;
     int prog;    // pivots the leader has published (kPanelStream)
     int ep_fin;  // epoch + 1 once the leader closed it (kPanelStream)
 };
@@ -484,8 +496,9 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         sh.super = la ? la->super_mode : 0;
     }
     named_bar(kBodyBar, nthr);
-    if (sh.super == 1 && !sh.cap_ok) {
+    if (sh.super == 1 && !sh.cap_ok && !la->have_window) {
         // panel a reads its window from the previous super-step's capture
+        // (unless the look-ahead across super-steps computed it)
         if (threadIdx.x == 0)
             sh.cap_ok = (la->sys ? spin_geq_sys(la->cap_ctr, la->cap_target, la->err)
                                  : spin_geq(la->cap_ctr, la->cap_target, la->err)) ? 1 : -1;
@@ -528,17 +541,24 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         u64 red = 0ull, acc = 0ull;
         u32 org = me;  // window offset of the row this slot holds
         if (inwin) {
-            if (sh.super) {
+            if (sh.super == 1 && la->have_window) {
+                // computed by the previous super-step's look-ahead
+                sh.wraw[me] = sh.la_m2[me];
+                sh.wraw2[me] = sh.la_m3[me];
+                red = sh.la_m2[me];
+                sh.wphys[me] = sh.la_phys[me];
+            } else if (sh.super) {
                 // keep the rows' pre-super-step words (pb, pb2): they follow
                 // the rows through the writeback for the workers' apply
                 sh.wraw[me] = ldcg(p.pb + r + me);
                 sh.wraw2[me] = ldcg(p.pb2 + r + me);
                 red = sh.super == 2 ? sh.nraw[me] : sh.wraw[me];
+                sh.wphys[me] = ldcg(p.perm + r + me);
             } else {
                 red = (la && la->have_window) ? sh.nraw[me] : ldcg(p.pb + r + me);
                 sh.wraw[me] = red;
+                sh.wphys[me] = ldcg(p.perm + r + me);
             }
-            sh.wphys[me] = ldcg(p.perm + r + me);
         }
         if (me == 0) {
             sh.dbg_lead_cyc = sh.dbg_lead_piv = sh.dbg_cross = sh.dbg_epochs = 0u;

@@ -423,6 +423,107 @@ __device__ __forceinline__ void wstamp(const Params& p, u32 S, u32 wk, u32 nwork
     if (p.worker_ns && threadIdx.x == 0) p.worker_ns[((size_t)S * nworkers + wk) * 4 + k] = globaltimer();
 }
 
+
+// ---------------------------------------------------------------------------
+// Look-ahead across super-steps (panel CTA body threads, after panel b of
+// super-step S, w = 2S). When the workers have already finished S-1 (the
+// panel chain is the bottleneck), the panel CTA computes the next panel a's
+// window -- words w+2, w+3 after S of the positions [r2, r2 + 128), r2 = the
+// rank after S -- itself, so that panel a of S+1 need not wait for S's
+// pre-work capture (its writeback and miss scans still do):
+//   x = own ^ sum_k d~_a[k] R_a[k] ^ sum_k d_b[k] R_b[k]
+// with own, R_a, R_b the pre-super-step words of the row and of both panels'
+// pivot rows (the sweep's fusion). Gather (before S is
+// published: the workers' pre-work of S rewrites pb / pb2 and sweeps tile
+// (w+2)/4 in place) reads every input into shared memory; compute (after the
+// publish) needs no global memory.
+__device__ __forceinline__ bool super_la_gather(const Params& p, PanelShared& sh, u32 w, u32 r_a, u32 rba,
+                                                u32 r_b, u32 nwin_b, u32 rbb, int nthr) {
+    const u32 r2 = r_b + rbb;
+    const u32 nwin2 = min((u32)kWin, p.m - r2);
+    const bool has3 = w + 3u < p.W;
+    for (u32 k = threadIdx.x; k < nwin2; k += nthr) {
+        const u32 q = r2 + k, slot = q - r_b;
+        u32 ph;
+        if (slot < nwin_b) {
+            const u32 o = sh.dorg[slot] & 127u;  // a non-pivot slot: an in-window origin
+            ph = sh.wphys[o];
+            sh.la_e0[k] = sh.ndacc[o];  // d_a (panel a's look-ahead, by panel-b slot)
+            sh.la_e1[k] = sh.dacc[slot];  // d_b
+            sh.la_ent[k] = 0;
+        } else {
+            ph = ldcg(p.perm + q);
+            sh.la_e0[k] = ldcg(p.pb + q);
+            sh.la_e1[k] = ldcg(p.pb2 + q);
+            sh.la_ent[k] = 1;
+        }
+        sh.la_phys[k] = ph;
+        sh.la_m2[k] = ldcg(tw4(p.mat, p.m, ph, w + 2u));
+        sh.la_m3[k] = has3 ? ldcg(tw4(p.mat, p.m, ph, w + 3u)) : 0ull;
+    }
+    for (u32 k = threadIdx.x; k < 128u; k += nthr) {
+        const bool b = k >= 64u;
+        const u32 idx = k & 63u;
+        u64 x2 = 0ull, x3 = 0ull;
+        if (idx < (b ? rbb : rba)) {
+            const u32 ph = ldcg(p.perm + (b ? r_b : r_a) + idx);
+            x2 = ldcg(tw4(p.mat, p.m, ph, w + 2u));
+            x3 = has3 ? ldcg(tw4(p.mat, p.m, ph, w + 3u)) : 0ull;
+        }
+        sh.la_R2[k] = x2;
+        sh.la_R3[k] = x3;
+        if (b && idx < rbb) {
+            const u32 o = sh.dorg[idx];
+            sh.la_C[idx] = (o & 0x80000000u) ? sh.oda[o & 63u] : sh.ndacc[o & 127u];
+        }
+    }
+    named_bar(kBodyBar, nthr);
+    return true;
+}
+
+__device__ __forceinline__ void super_la_compute(const Params& p, PanelShared& sh, u32 rba, u32 r_b,
+                                                 u32 rbb, int nthr) {
+    const u32 r2 = r_b + rbb;
+    const u32 nwin2 = min((u32)kWin, p.m - r2);
+    for (u32 k = threadIdx.x; k < nwin2; k += nthr) {
+        u64 da, db;
+        if (sh.la_ent[k]) {
+            // a row from outside panel b's window: both panels from its raw
+            // words (as panel b's miss scan does)
+            u64 v = sh.la_e0[k];
+            da = 0ull;
+            for (u32 s2 = 0; s2 < rba; ++s2) {
+                const u64 msk = 0ull - ((v >> sh.qa[s2]) & 1ull);
+                v ^= sh.Ea[s2] & msk;
+                da ^= sh.Da[s2] & msk;
+            }
+            u64 v1 = sh.la_e1[k];
+            for (u32 s2 = 0; s2 < rba; ++s2) v1 ^= sh.piv2[s2] & (0ull - ((da >> s2) & 1ull));
+            db = 0ull;
+            for (u32 s2 = 0; s2 < rbb; ++s2) {
+                const u64 msk = 0ull - ((v1 >> sh.q[s2]) & 1ull);
+                v1 ^= sh.E[s2] & msk;
+                db ^= sh.D[s2] & msk;
+            }
+        } else {
+            da = sh.la_e0[k];
+            db = sh.la_e1[k];
+        }
+        u64 dta = da;
+        for (u32 s2 = 0; s2 < rbb; ++s2) dta ^= sh.la_C[s2] & (0ull - ((db >> s2) & 1ull));
+        u64 x2 = sh.la_m2[k], x3 = sh.la_m3[k];
+#pragma unroll 4
+        for (u32 s2 = 0; s2 < 64u; ++s2) {
+            const u64 ma = 0ull - ((dta >> s2) & 1ull), mb = 0ull - ((db >> s2) & 1ull);
+            x2 ^= (sh.la_R2[s2] & ma) ^ (sh.la_R2[64u + s2] & mb);
+            x3 ^= (sh.la_R3[s2] & ma) ^ (sh.la_R3[64u + s2] & mb);
+        }
+        sh.la_m2[k] = x2;
+        sh.la_m3[k] = x3;
+    }
+    named_bar(kBodyBar, nthr);
+}
+
 // One launch, grid = #SMs: CTA 0 runs the panels, CTAs 1.. the sweep. `nss` =
 // number of super-steps (ceil(W / 2)). panel_done counts published super-steps.
 __global__ void __launch_bounds__(kTrailThreads, 1)
@@ -454,17 +555,22 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         Params pb_par = p;
         pb_par.pout = pout_b;
         u32 prev_r = 0u;
+        bool la_next = false;  // panel a's window came from the look-ahead
+        const bool la_on = (p.pflags & kPanelSuperLA) != 0u;
         for (u32 S = 0; S < nss; ++S) {
             const u32 w = 2u * S;
             // nothing left: publish an empty super-step so the workers stop
             const bool done0 = la.r >= p.m;
             // panel a: its window and scans read the previous super-step's
-            // capture (all of its pre-work chunks)
+            // capture (all of its pre-work chunks) -- the window only without
+            // the look-ahead across super-steps
             la.cap_ctr = p.ap_done + (S > 0 ? S - 1 : 0);
             la.cap_target = S > 0 ? pw_chunks(p.m - prev_r, p.pw_div) : 0u;
             prev_r = la.r;
             la.super_mode = 1;
-            la.have_window = false;
+            la.have_window = la_next;
+            la_next = false;
+            const u32 r_a = la.r;
             stamp2(p, w, 0);
             const u32 rba = panel_factor_body(p, w, psh, nbody, &la);
             // (an aborted panel returns 0: then check the error word itself)
@@ -480,6 +586,19 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                     const u32 rbb = panel_factor_body(pb_par, w + 1u, psh, nbody, &la);
                     if (*(volatile int*)&psh.sig_err || (rbb == 0u && *(volatile u32*)&sy->error)) return;
                     la.r += rbb;
+                    // look-ahead across super-steps, only while the workers
+                    // are already through S-1 (the panel chain is the
+                    // bottleneck; S-1 has also finished the tile holding
+                    // words w+2, w+3 everywhere)
+                    if (la_on && w + 2u < p.W && la.r < p.m) {
+                        if (threadIdx.x == 0) psh.la_go = ld_acquire(&sy->t_count) >= nworkers * S ? 1 : 0;
+                        named_bar(kBodyBar, nbody);
+                        if (psh.la_go) {
+                            const u32 r_b = r_a + rba;
+                            la_next = super_la_gather(p, psh, w, r_a, rba, r_b, min((u32)kWin, p.m - r_b),
+                                                      rbb, nbody);
+                        }
+                    }
                 } else if (threadIdx.x == 0) {
                     p.rhist[w + 1u] = la.r;
                     p.rbhist[w + 1u] = 0u;
@@ -488,6 +607,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             stamp2(p, w, 1);
             signal_step(psh, nbody, S, done0);
             if (done0 || *(volatile int*)&psh.sig_err) return;
+            if (la_next) super_la_compute(p, psh, rba, r_a + rba, la.r - r_a - rba, nbody);
         }
         return;
     }
