@@ -66,7 +66,7 @@ typedef struct {
                                       64-column panel per trailing sweep     */
 #define GF2CU_FLAG_SUPER_STEP 8u   /* force the super-step kernel: two panels
                                       per sweep (default: chosen by size --
-                                      super-step from 2^23 matrix words)     */
+                                      super-step from 5*2^20 matrix words)     */
 
 /* The device-driven row-sharded driver (ple_peer.cuh)
  * with g = 1..8 ranks emulated on the one device: one cooperative launch,

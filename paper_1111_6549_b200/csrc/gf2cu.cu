@@ -36,10 +36,11 @@ namespace {
 thread_local std::string g_last_error;
 
 // The super-step driver (two panels per sweep) from this many matrix words up,
-// the single-panel persistent driver below: measured crossover between 6.5M
-// (20480^2: single-panel 6.0 vs 6.2 ms) and 8.4M words (16384x32768: 5.9 vs
-// 5.3 ms; 8192x65536, 32768x16384 and 65536x8192 also favour two panels).
-constexpr double kSuperStepWords = 8388608.0;
+// the single-panel persistent driver below. Measured with the super-step
+// look-ahead: 16384^2 (4.2M words) single 4.24 vs super 4.28 ms, 12288^2
+// single better; 16384x24576 (6.3M) 4.98 vs 4.61, 20480^2 (6.5M) 6.02 vs 5.73
+// super better (8192x32768, 4.2M: 2.32 vs 2.22, the crossover's fuzz).
+constexpr double kSuperStepWords = 5242880.0;
 
 // Panel tuning bits (gf2cu::kPanel*); GF2CU_PANEL_FLAGS overrides the default
 // for A/B measurements.

@@ -232,10 +232,10 @@ def test_streamed_output_matches_device(m, n):
     assert np.array_equal(bm.words, d.download())
 
 
-@pytest.mark.parametrize("m,n,driver", [(8192, 65536, 2), (20480, 20480, 1), (16384, 32768, 2),
-                                        (16384, 16384, 1)])
+@pytest.mark.parametrize("m,n,driver", [(8192, 65536, 2), (20480, 20480, 2), (16384, 24576, 2),
+                                        (16384, 16384, 1), (12288, 12288, 1)])
 def test_default_driver_size_rule(m, n, driver):
-    """Without a driver flag the super-step driver runs from 2^23 matrix words
+    """Without a driver flag the super-step driver runs from 5 * 2^20 matrix words
     (m * ceil(n/64)) up, the single-panel persistent driver below (the measured
     crossover); both give the device-resident ctr result
     the other driver gives."""
