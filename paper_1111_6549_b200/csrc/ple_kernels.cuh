@@ -347,6 +347,11 @@ struct PanelShared {
     int ep_t[2], ep_j[2];  // panel epochs: pivots / columns done by the leader warp
     u64 lpb2[kWin];        // look-ahead inputs, fetched right after the capture wait:
     u64 epb[64], epb2[64]; // window rows' pb2 by origin; entering rows' pb / pb2
+    u32 eph[64];           // entering rows' physical rows
+    // the next window's physical rows and (super-step panel b) pre-super-step
+    // words, by slot: no global loads at the next panel's start
+    u32 nphys[kWin];
+    u64 nwr[kWin], nwr2[kWin];
     // super-step driver
     int super;          // 0, 1 (panel a) or 2 (panel b)
     u64 wraw2[kWin];    // window rows' pre-super-step word w+1 (as loaded)
@@ -547,15 +552,26 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 sh.wraw2[me] = sh.la_m3[me];
                 red = sh.la_m2[me];
                 sh.wphys[me] = sh.la_phys[me];
+            } else if (sh.super == 2) {
+                // panel a's look-ahead: word w+1 after panel a, and the rows'
+                // pre-super-step words and physical rows
+                sh.wraw[me] = sh.nwr[me];
+                sh.wraw2[me] = sh.nwr2[me];
+                red = sh.nraw[me];
+                sh.wphys[me] = sh.nphys[me];
             } else if (sh.super) {
                 // keep the rows' pre-super-step words (pb, pb2): they follow
                 // the rows through the writeback for the workers' apply
                 sh.wraw[me] = ldcg(p.pb + r + me);
                 sh.wraw2[me] = ldcg(p.pb2 + r + me);
-                red = sh.super == 2 ? sh.nraw[me] : sh.wraw[me];
+                red = sh.wraw[me];
                 sh.wphys[me] = ldcg(p.perm + r + me);
+            } else if (la && la->have_window) {
+                red = sh.nraw[me];
+                sh.wraw[me] = red;
+                sh.wphys[me] = sh.nphys[me];
             } else {
-                red = (la && la->have_window) ? sh.nraw[me] : ldcg(p.pb + r + me);
+                red = ldcg(p.pb + r + me);
                 sh.wraw[me] = red;
                 sh.wphys[me] = ldcg(p.perm + r + me);
             }
@@ -794,12 +810,14 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         // overlaps the writeback: the window rows' pre-step word w+1 (by
         // origin) and the words w, w+1 of the rows that may enter it
         u64 f_pb2 = 0ull, f_epb = 0ull, f_epb2 = 0ull;
+        u32 f_eph = 0u;
         if (la && !aborted && sh.super != 2 && w + 1 < p.W) {
             if (!sh.super && inwin) f_pb2 = ldcg(p.pb2 + r + me);
             const u32 qe = r + nwin + me;
             if (me < 64u && qe < p.m) {
                 f_epb = ldcg(p.pb + qe);
                 f_epb2 = ldcg(p.pb2 + qe);
+                f_eph = ldcg(p.perm + qe);
             }
         }
         // the permuted window: raw panel word and physical row per position
@@ -830,6 +848,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         if (me < 64u) {
             sh.epb[me] = f_epb;
             sh.epb2[me] = f_epb2;
+            sh.eph[me] = f_eph;
         }
     }
     named_bar(kBodyBar, nthr);
@@ -913,9 +932,16 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             const u32 q = r1 + k;  // position
             u64 d, pre;
             if (q - r < nwin) {
+                const u32 o = sh.dorg[q - r] & 127u;  // (a non-pivot slot: an in-window origin)
                 d = sh.dacc[q - r];
-                pre = sh.super ? sh.wraw2[sh.dorg[q - r] & 127u] : sh.lpb2[sh.dorg[q - r] & 127u];
+                pre = sh.super ? sh.wraw2[o] : sh.lpb2[o];
+                sh.nphys[k] = sh.wphys[o];
+                sh.nwr[k] = sh.wraw[o];
+                sh.nwr2[k] = sh.wraw2[o];
             } else {
+                sh.nphys[k] = sh.eph[q - r - nwin];
+                sh.nwr[k] = sh.epb[q - r - nwin];
+                sh.nwr2[k] = sh.epb2[q - r - nwin];
                 // a row entering the window: its combination for step w
                 u64 v = sh.epb[q - r - nwin];
                 d = 0ull;
