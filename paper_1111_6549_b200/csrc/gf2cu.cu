@@ -695,11 +695,13 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             cudaEvent_t kdone;
             CU_TRY(cudaEventCreateWithFlags(&kdone, cudaEventDisableTiming));
             CU_TRY(cudaEventRecord(kdone, s));
-            const size_t chunk = std::max<size_t>(1024, m / 32);
+            // (chunks shrink toward the end, where the late super-steps finish
+            // few rows each, so that little is left to copy after the kernel)
             uint64_t* host = stream_to->data + (stream_to->col_off >> 6);
             for (;;) {
                 const bool fin = cudaEventQuery(kdone) == cudaSuccess;
                 const size_t avail = *reinterpret_cast<volatile u32*>(ws.out_host);
+                const size_t chunk = std::max<size_t>(256, std::min<size_t>(m / 32, (m - sent) / 8));
                 if (avail > sent && (avail - sent >= chunk || fin)) {
                     CU_TRY(cudaMemcpy2DAsync(host + sent * stream_to->stride, stream_to->stride * 8,
                                              a->data + sent * a->Wp, a->Wp * 8, W * 8, avail - sent,
