@@ -248,3 +248,29 @@ def test_default_driver_size_rule(m, n, driver):
     other = G.block_iterative_ple(e, G.PleConfig(single_panel=True) if driver == 2 else G.PleConfig(super_step=True))
     assert other.rank == got.rank and np.array_equal(other.q, got.q)
     assert d.checksum() == e.checksum()
+
+
+@pytest.mark.parametrize("m,n,gen", [(3000, 3000, "dense"), (2500, 2500, "dup"), (1500, 4000, "ctr"),
+                                     (4000, 1500, "p256")])
+def test_panel_tuning_bits_exact(m, n, gen, monkeypatch):
+    """The panel tuning bits (GF2CU_PANEL_FLAGS: 1 = followers apply the
+    leader's pivots as published, 2 = the super-step look-ahead across
+    super-steps) change the schedule, never the result: every combination is
+    bit-exact against the oracle on both persistent drivers."""
+    if gen == "dense":
+        a = O.fill_random(m, n, 0.5, 21)
+    elif gen == "p256":
+        a = O.fill_random(m, n, 1 / 256, 21)
+    elif gen == "ctr":
+        a = O.fill_ctr(m, n, 21)
+    else:
+        a = O.fill_ctr(m, n, 22)
+        a[100:900] = a[1000:1800]  # pivotless columns, window misses
+    ref = a.copy()
+    want = O.ple(ref, m, n)
+    for flags in ("0", "1", "2", "3"):
+        monkeypatch.setenv("GF2CU_PANEL_FLAGS", flags)
+        for cfg in (G.PleConfig(super_step=True), G.PleConfig(single_panel=True)):
+            bm = G.BitMatrix(m, n, a.copy())
+            got = G.block_iterative_ple(bm, cfg)
+            assert_same(ref, want, bm, got, what=f"{gen} {m}x{n} flags={flags}")
