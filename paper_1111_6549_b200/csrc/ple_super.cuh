@@ -86,6 +86,8 @@ __global__ void untile4_kernel(const u64* __restrict__ src, u64* __restrict__ ds
     }
 }
 
+constexpr u32 kOutEvery = 8;  // streamed output: super-steps per batch
+
 // Streamed output: the rows at positions [lo, hi) (pivot rows of a finished
 // super-step) into p.out in row-major form; 16-byte units split as part
 // `part` of `nparts`.
@@ -685,15 +687,17 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             s_ok = spin_geq2(&sy->t_count, nworkers * S, &p.ap_done[S], nch, &sy->error) ? 1u : 0u;
         __syncthreads();
         if (!s_ok) return;
-        if (p.out && S > 0) {
-            // S-1 is finished everywhere: its pivot rows are final; write them
-            // out row-major and tell the host (which copies them while the
-            // factorization goes on)
-            out_rows4(p, *(volatile u32*)&p.rhist[w - 2u], r, wk, nworkers);
+        if (p.out && S > 0 && S % kOutEvery == 0u) {
+            // S-1 is finished everywhere: the pivot rows of the last kOutEvery
+            // super-steps are final; write them out row-major and tell the
+            // host (which copies them while the factorization goes on). In
+            // batches, so that the fence before the count is paid every
+            // kOutEvery super-steps only.
+            out_rows4(p, *(volatile u32*)&p.rhist[w - 2u * kOutEvery], r, wk, nworkers);
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();
-                if (atomicAdd(&sy->out_count, 1u) == nworkers * S - 1u) {
+                if (atomicAdd(&sy->out_count, 1u) == nworkers * (S / kOutEvery) - 1u) {
                     __threadfence_system();
                     *p.out_host = r;
                 }
