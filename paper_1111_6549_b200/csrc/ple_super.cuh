@@ -675,10 +675,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         }
         if (mine) {
             __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                red_release_add(&p.ap_done[S], mine);
-            }
+            if (threadIdx.x == 0) red_release_add(&p.ap_done[S], mine);  // (see cta_arrive)
         }
         wstamp(p, S, wk, nworkers, 1);
         // the rest: after super-step S-1 everywhere (pivot rows' raw tails)
