@@ -24,9 +24,9 @@ cpu_baseline = the reference itself (oracle/_ref/libgf2ref.so, compiled from
 
 --impl reference runs that reference arm alone (rank 0; other ranks exit 0).
 Multi-GPU (torchrun, N>1): the device-driven row-sharded PLE (peer.py,
-csrc/ple_peer.cuh) on the weak-scaling size n = 65536 * N^(1/3) (N = 8 is
-BASELINE config 5's 131072^2); value = the matrix's algorithmic bytes / the
-max-over-ranks device time. --host-sharded: the NCCL host-orchestrated path;
+csrc/ple_peer.cuh) on BASELINE config 5's 131072^2 at every N (strong
+scaling); value = the matrix's algorithmic bytes / the max-over-ranks device
+time. --host-sharded: the NCCL host-orchestrated path;
 --replicas: independent single-GPU instances.
 """
 from __future__ import annotations
@@ -72,17 +72,21 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(driver: int = 2):
-    """DRAM bytes per algorithmic (sweep) byte of the dominant kernel from its
-    committed ncu --set full capture (super-step or single-panel driver)."""
+def load_capture(driver: int = 2):
+    """The dominant kernel's committed ncu --set full capture summary
+    (profiles/super_traffic.json or persistent_traffic.json)."""
     name = "super_traffic.json" if driver == 2 else "persistent_traffic.json"
-    p = os.path.join(ROOT, "profiles", name)
     try:
-        with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_k64_alg_byte", d.get("dram_bytes_per_alg_byte"))
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
     except Exception:
-        return None
+        return {}
+
+
+def load_traffic(driver: int = 2):
+    """DRAM bytes per algorithmic (K = 64) byte of the dominant kernel."""
+    d = load_capture(driver)
+    return d.get("dram_bytes_per_k64_alg_byte", d.get("dram_bytes_per_alg_byte"))
 
 
 class ClockSampler:
@@ -140,21 +144,32 @@ class ClockSampler:
 
 
 def make_host_ctr(m, n, seed):
-    import paper_1111_6549_b200 as G
-    a = G.BitMatrix(m, n)
-    G.fill_ctr(a, seed)
-    return a.words
+    """The ctr input on the host from the TEST-ONLY generator in oracle/
+    (liboracle.so), so the CPU legs map no library of the product."""
+    import oracle as O
+    return O.fill_ctr(m, n, seed)
+
+
+def ref_alg_bytes(m, cols, q):
+    """SURVEY.md 8(d)'s algorithmic bytes (K = 64 panels) of a PLE with pivot
+    columns q -- the same definition the device arm reports."""
+    q = np.asarray(q, dtype=np.int64)
+    rh, rbh, r = [], [], 0
+    for w in range((cols + 63) // 64):
+        rb = int(np.count_nonzero((q >= 64 * w) & (q < 64 * w + 64)))
+        rh.append(r)
+        rbh.append(rb)
+        r += rb
+    return alg_bytes_from_history(m, cols, rh, rbh)
 
 
 # ------------------------------------------------------------------ CPU legs
 def run_reference_sample(m, cols, seed, reps=1):
     """The compiled reference on the leading m x cols block of the ctr matrix."""
     import oracle as O
-    full_W = (N_DEFAULT + 63) // 64
     Wc = (cols + 63) // 64
     # the ctr generator is keyed on the full row width: generate full rows, slice
     big = make_host_ctr(m, N_DEFAULT, seed)
-    assert big.shape[1] == full_W
     base = np.ascontiguousarray(big[:, :Wc])
     del big
     secs, last = [], None
@@ -163,20 +178,25 @@ def run_reference_sample(m, cols, seed, reps=1):
         out, s = O.ref_ple(a, m, cols)
         secs.append(s)
         last = out
-    # algorithmic bytes of the sample with the same definition (K = 64 panels)
-    rh, rbh = [], []
-    q = np.asarray(last.q, dtype=np.int64)
-    W = Wc
-    r = 0
-    for w in range(W):
-        rb = int(np.count_nonzero((q >= 64 * w) & (q < 64 * w + 64)))
-        rh.append(r)
-        rbh.append(rb)
-        r += rb
-    return secs, alg_bytes_from_history(m, cols, rh, rbh), last.rank
+    return secs, ref_alg_bytes(m, cols, last.q), last.rank
+
+
+def run_reference_full(n, seed):
+    """The compiled reference on the whole n x n ctr matrix (BASELINE config
+    5 at 65536^2: the GPU arm's exact workload). One run, ~4.5 min."""
+    import oracle as O
+    a = make_host_ctr(n, n, seed)
+    out, secs = O.ref_ple(a, n, n)
+    return secs, ref_alg_bytes(n, n, out.q), out.rank
 
 
 def reference_arm(args, rank):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref/libgf2ref.so = gf2::block_iterative_ple compiled from the
+    reference headers with its Release flags; it is single-threaded, so 1
+    core). W warm-up + K timed steps on the bounded sample, then ONE run of
+    the full 65536^2 config, which is the line's `value` (same config as the
+    device arm); the sample's figure is kept in cpu_baseline."""
     if rank != 0:
         return
     m, cols = N_DEFAULT, REF_SAMPLE_COLS
@@ -194,21 +214,34 @@ def reference_arm(args, rank):
         secs, b, rk = run_reference_sample(m, cols, SEED)
         secs_all += secs
         bytes_all += b
-    wall = time.perf_counter() - t0
     tsum = sum(secs_all)
-    val = bytes_all / tsum / 1e9
-    sample = f"leading {m}x{cols} column block of the 65536^2 ctr(seed {SEED}) matrix, rank {rk}"
+    sample_val = bytes_all / tsum / 1e9
+    full = None
+    if not args.ref_sample_only:
+        fsecs, fbytes, frk = run_reference_full(N_DEFAULT, SEED)
+        full = {"seconds": round(fsecs, 3), "alg_bytes": int(fbytes), "rank": int(frk),
+                "value": round(fbytes / fsecs / 1e9, 4)}
+    wall = time.perf_counter() - t0
+    val = full["value"] if full else sample_val
+    sample = (f"{args.steps} x leading {m}x{cols} column block of the 65536^2 ctr(seed {SEED}) matrix "
+              f"(rank {rk}), {tsum / args.steps:.2f} s each, single-threaded gf2::block_iterative_ple")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": UNIT,
+        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * tsum / args.steps, 3), "higher_is_better": True,
+        "ms_per_step": round(1e3 * (full["seconds"] if full else tsum / args.steps), 3),
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"block_iterative_ple {N_DEFAULT}x{N_DEFAULT} (BASELINE config 5, 1 GPU)",
-                   "sample": f"{m}x{cols} leading column block per step (bounded CPU sample)",
-                   "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "panel_bits": 64},
-        "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": 1, "kind": "reference",
-                         "sample": sample},
-        "e2e": {"value": round(val, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "timed": ("value = ONE full 65536^2 run (the device arm's exact config); the K "
+                             "steps are the bounded sample, reported in cpu_baseline.sample_value")
+                   if full else "value = the bounded sample (--ref-sample-only)",
+                   "generator": "ctr (SURVEY.md 8(d)), oracle/liboracle.so", "seed": SEED,
+                   "panel_bits": 64},
+        "full_size": full,
+        "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": sample, "sample_value": round(sample_val, 4),
+                         "host_cores": os.cpu_count()},
+        "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": round(wall, 2),
     }))
@@ -305,6 +338,21 @@ def gpu_arm(args, rank, world, local_rank):
         e2e_s += time.perf_counter() - t0
         e2e_bytes += o2.stats["alg_bytes"]
     e2e_parity = (o2.rank == out.rank)
+    # the same drop-in call on PAGEABLE host memory (what a C++ caller's
+    # gf2::BitMatrix, a std::vector, hands the wrapper)
+    page_np = np.empty((m, Wd), dtype=np.uint64)
+    pview = G.MatrixView(page_np, Wd, 0, m, n)
+    np.copyto(page_np, src)
+    G.block_iterative_ple(pview, cfg)
+    pg_s, pg_bytes, pg_steps = 0.0, 0.0, max(1, min(args.steps, 2))
+    for _ in range(pg_steps):
+        np.copyto(page_np, src)
+        t0 = time.perf_counter()
+        o3 = G.block_iterative_ple(pview, cfg)
+        pg_s += time.perf_counter() - t0
+        pg_bytes += o3.stats["alg_bytes"]
+    pg_words = (G.host_checksum(page_np, n) == checksum) if checksum is not None else None
+    del page_np, pview
     # the in-place L\E the host received (part of it streamed out while the
     # kernel ran) against the device-resident run's result
     e2e_words = (G.host_checksum(host_np, n) == checksum) if checksum is not None else None
@@ -342,11 +390,24 @@ def gpu_arm(args, rank, world, local_rank):
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else None
     traffic_ratio = load_traffic(driver)
     super_step = driver == 2
+    cap = load_capture(driver)
+    dram_phys = None
+    if cap.get("dram_bytes_read") and cap.get("duration_ms_under_ncu"):
+        dram_phys = ((cap["dram_bytes_read"] + cap["dram_bytes_write"]) / (cap["duration_ms_under_ncu"] * 1e-3)
+                     / 1e9 / peak)
     roofline = {
-        "kernel": "ple_super_kernel" if super_step else "ple_persistent_kernel", "bound": "hbm",
+        # The limiter is the L1TEX data pipe (Gray-table lookups in shared
+        # memory + the global load/store), not DRAM: `frac` is the metric's
+        # EFFECTIVE figure (K = 64 algorithmic bytes over the HBM peak); the
+        # physical DRAM use and the L1TEX load come from the committed capture.
+        "kernel": "ple_super_kernel" if super_step else "ple_persistent_kernel", "bound": "l1tex",
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": (round(per_launch_bytes * traffic_ratio) if traffic_ratio else None),
+        "frac_kind": "effective (SURVEY 8(d) K=64 algorithmic bytes / measured HBM peak)",
+        "dram_frac_physical": round(dram_phys, 4) if dram_phys else None,
+        "l1tex_pct": cap.get("l1tex_throughput_pct_of_peak_active"),
+        "capture": cap.get("source"),
         "alg_bytes_per_launch": round(per_launch_bytes),
         "panel_columns_per_sweep": 128 if super_step else 64,
         "sweep_bytes_per_launch": round(per_launch_sweep),
@@ -393,7 +454,11 @@ def gpu_arm(args, rank, world, local_rank):
                 "h2d_bytes_per_step": int(m * Wd * 8), "d2h_bytes_per_step": int(m * Wd * 8),
                 "steps": e2e_steps, "ms_per_step": round(1e3 * e2e_max_s / e2e_steps, 3),
                 "rank_matches_device_run": bool(e2e_parity),
-                "output_matches_device_run": e2e_words},
+                "output_matches_device_run": e2e_words,
+                "host_memory": "pinned (torch pin_memory)",
+                "pageable": {"value": round(pg_bytes / pg_s / 1e9, 2), "unit": UNIT, "steps": pg_steps,
+                             "ms_per_step": round(1e3 * pg_s / pg_steps, 3),
+                             "output_matches_device_run": pg_words}},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -405,10 +470,14 @@ def gpu_arm(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def weak_n(world: int) -> int:
-    """Per-GPU work fixed as N grows: total work ~ n^3, so n = 65536 * N^(1/3)
-    (N = 8 -> 131072, BASELINE config 5's large case)."""
-    return int(round(N_DEFAULT * world ** (1.0 / 3.0) / 64.0)) * 64
+N_SCALE = 131072
+
+
+def scale_n(world: int, n_arg: int) -> int:
+    """The N > 1 workload: BASELINE config 5's 131072^2 at every N (strong
+    scaling, north_star: "near-linear row-slab scaling to 8 GPUs on
+    131072x131072"); --size overrides it."""
+    return n_arg if n_arg != N_DEFAULT else (N_SCALE if world > 1 else N_DEFAULT)
 
 
 def q_to_bytes(m, n, q):
@@ -425,7 +494,7 @@ def q_to_bytes(m, n, q):
 
 def gpu_sharded_arm(args, rank, world, local_rank):
     """N > 1: the row-sharded PLE (paper_1111_6549_b200/shard.py), one process
-    per GPU over NCCL, on the weak-scaling size n = 65536 * N^(1/3)."""
+    per GPU over NCCL, on 131072^2 (strong scaling)."""
     import torch
     import torch.distributed as dist
     from paper_1111_6549_b200 import shard as S
@@ -436,7 +505,7 @@ def gpu_sharded_arm(args, rank, world, local_rank):
         os.environ.setdefault("MASTER_PORT", "29561")
         os.environ["RANK"], os.environ["WORLD_SIZE"] = "0", "1"
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    n = args.n if args.n != N_DEFAULT else weak_n(world)
+    n = scale_n(world, args.n)
     m = n
     eng = S.GpuShardEngine(m, n, rank, world, block=256, device=local_rank)
 
@@ -490,9 +559,9 @@ def gpu_sharded_arm(args, rank, world, local_rank):
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"block_iterative_ple {m}x{n} row-sharded over {world} GPUs "
-                                   f"(weak scaling: n = 65536*N^(1/3); N=8 is BASELINE config 5's 131072^2)",
+                                   f"(BASELINE config 5, strong scaling: the same matrix at every N)",
                        "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "rank": int(res.rank),
                        "panel_bits": 64, "parallelism": f"row-sharded x{world} (block-cyclic 256-row blocks, NCCL)",
                        "l2": "per-GPU shard > 126 MB L2"},
@@ -517,8 +586,8 @@ def gpu_peer_arm(args, rank, world, local_rank):
     csrc/ple_peer.cuh): one process and ONE persistent kernel per GPU for the
     whole factorization, the ranks exchanging the panel column and pivot-row
     tails through NVLink peer memory (CUDA IPC) with device-side counters --
-    no host call or collective per step. Weak scaling: n = 65536 * N^(1/3)
-    (N = 8 is BASELINE config 5's 131072^2)."""
+    no host call or collective per step. Strong scaling on BASELINE config
+    5's 131072^2."""
     import torch
     import torch.distributed as dist
     from paper_1111_6549_b200.peer import PeerEngine, exchange_handles
@@ -529,7 +598,7 @@ def gpu_peer_arm(args, rank, world, local_rank):
         os.environ.setdefault("MASTER_PORT", "29563")
         os.environ["RANK"], os.environ["WORLD_SIZE"] = "0", "1"
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    n = args.n if args.n != N_DEFAULT else weak_n(world)
+    n = scale_n(world, args.n)
     m = n
     stream = torch.cuda.current_stream()
     eng = PeerEngine(m, n, rank, world, block=256, device=local_rank, stream=stream.cuda_stream)
@@ -541,6 +610,9 @@ def gpu_peer_arm(args, rank, world, local_rank):
         eng.reset()
         dist.barrier()
         st = eng.run()
+        # no rank resets for the next run before every kernel is done (the
+        # last step's signals into the peers' counters have landed)
+        dist.barrier()
         kernel_ms.append(st["kernel_ms"])
         return st
 
@@ -580,13 +652,22 @@ def gpu_peer_arm(args, rank, world, local_rank):
         eng.reset()
         dist.barrier()
         eng.run()
+        dist.barrier()
         out2 = eng.finish()  # replicated outcome + this rank's rows to the host
         torch.cuda.synchronize()
         t_e2e += time.perf_counter() - t0
         assert out2.rank == res.rank
-    vals = torch.tensor([dev_ms, t_e2e, max(kernel_ms)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    max_ms, e2e_max_s, kmax = float(vals[0]), float(vals[1]), float(vals[2])
+    vals = torch.tensor([dev_ms, t_e2e, max(kernel_ms), statistics.median(kernel_ms)],
+                        dtype=torch.float64, device="cuda")
+    allv = [torch.zeros_like(vals) for _ in range(world)]
+    dist.all_gather(allv, vals)
+    allv = torch.stack(allv).cpu().numpy()
+    max_ms, e2e_max_s, kmax = float(allv[:, 0].max()), float(allv[:, 1].max()), float(allv[:, 2].max())
+    per_rank = [{"rank": i, "device_ms": round(float(allv[i, 0]), 3),
+                 "kernel_ms_median": round(float(allv[i, 3]), 3), "kernel_ms_max": round(float(allv[i, 2]), 3)}
+                for i in range(world)]
+    print(f"[bench rank {rank}/{world}] device {torch.cuda.get_device_name(local_rank)} "
+          f"kernel_ms median {statistics.median(kernel_ms):.3f} max {max(kernel_ms):.3f}", file=sys.stderr)
     if rank == 0:
         value = bytes_per_step * args.steps / (max_ms * 1e-3) / 1e9
         peak, peak_kind = load_peaks()
@@ -595,9 +676,9 @@ def gpu_peer_arm(args, rank, world, local_rank):
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"block_iterative_ple {m}x{n} row-sharded over {world} GPUs "
-                                   f"(weak scaling: n = 65536*N^(1/3); N=8 is BASELINE config 5's 131072^2)",
+                                   f"(BASELINE config 5, strong scaling: the same matrix at every N)",
                        "generator": "ctr (SURVEY.md 8(d))", "seed": SEED, "rank": int(res.rank),
                        "panel_bits": 64,
                        "parallelism": f"row-sharded x{world} (block-cyclic 256-row blocks), one persistent "
@@ -611,6 +692,7 @@ def gpu_peer_arm(args, rank, world, local_rank):
                          "frac": round(per_gpu_kernel / peak, 4), "traffic": None,
                          "avg_launch_ms": round(kmax, 3),
                          "note": "per GPU: the matrix's algorithmic bytes / N over the slowest rank's kernel",
+                         "per_rank": per_rank,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             "cpu_baseline": None,
             "clocks": clk,
@@ -629,6 +711,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--size", dest="n", type=int, default=N_DEFAULT)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sample-only", action="store_true",
+                    help="--impl reference: skip the full-size 65536^2 run (value = the sample)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded PLE even at N=1 (testing)")
     ap.add_argument("--replicas", action="store_true",

@@ -113,6 +113,23 @@ gf2cu_status gf2cu_ple(const gf2cu_view* a, const gf2cu_cfg* cfg, size_t* swaps,
                        size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
                        gf2cu_stats* stats);
 
+/* Replaces gf2::partial_ple(MatrixView a) (ple.hpp:57-130), the lazy
+ * single-pass PLE, in place on a HOST view. rank, q, swaps and col_swaps are
+ * the reference's; *processed = its watermark (rows [processed, nrows) are
+ * left untouched, which happens only when every column finds a pivot and
+ * rank == ncols < nrows; otherwise processed = nrows and the in-place result
+ * equals gf2cu_ple's; rank 0 gives processed 0). Capacities as gf2cu_ple. */
+gf2cu_status gf2cu_partial_ple(const gf2cu_view* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
+                               size_t* rank, size_t* processed, gf2cu_colswap* col_swaps,
+                               size_t* n_col_swaps);
+
+/* Replaces gf2::undo_column_swaps(MatrixView a, const std::vector<ColSwap>&)
+ * (ple.hpp:293-296): replays the compression swaps backwards,
+ * swap_cols_from_row(a, b, from_row) each (bit_matrix.hpp:302-318), on the
+ * device. GF2CU_ERANGE if a swap lies outside the view. */
+gf2cu_status gf2cu_undo_column_swaps(const gf2cu_view* a, const gf2cu_colswap* col_swaps,
+                                     size_t n_col_swaps, const gf2cu_cfg* cfg);
+
 /* Thread-local message of the last failing call ("" if none). */
 const char* gf2cu_last_error(void);
 
@@ -152,6 +169,10 @@ gf2cu_status gf2cu_matrix_checksum(const gf2cu_matrix* a, uint64_t* out, void* s
 gf2cu_status gf2cu_ple_device(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
                               size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
                               gf2cu_stats* stats);
+
+/* undo_column_swaps on a device-resident matrix. */
+gf2cu_status gf2cu_undo_column_swaps_device(gf2cu_matrix* a, const gf2cu_colswap* col_swaps,
+                                            size_t n_col_swaps, void* stream);
 
 /* ------------------------------------------------------------------ */
 /* Echelon forms and the upper-triangular solve     */

@@ -51,6 +51,8 @@ def lib():
         L.orc_ple.restype = _sz
         L.orc_canonical_col_swaps.argtypes = [_szp, _sz, _szp]
         L.orc_canonical_col_swaps.restype = _sz
+        L.orc_partial_ple.argtypes = [_u64p, _sz, _sz, _sz, _szp, _szp, _szp]
+        L.orc_partial_ple.restype = _sz
         L.orc_undo_col_swaps.argtypes = [_u64p, _sz, _sz, _szp, _sz]
         L.orc_undo_col_swaps.restype = None
         L.orc_mul.argtypes = [_u64p, _sz, _sz, _sz, _u64p, _sz, _sz, _u64p, _sz]
@@ -176,6 +178,31 @@ def ple(a: np.ndarray, m: int, n: int) -> Outcome:
     rank = lib().orc_ple(_u64(a), m, n, a.shape[1], _szarr(swaps), _szarr(q))
     q = q[:rank].copy()
     return Outcome(rank, swaps[:rank].copy(), q, canonical_col_swaps(q))
+
+
+def partial_ple(a: np.ndarray, m: int, n: int):
+    """The C restatement of partial_ple (ple.hpp:57-130), in place on ``a``.
+    Returns (Outcome, processed)."""
+    cap = max(1, min(m, n))
+    swaps = np.zeros(cap, dtype=np.uintp)
+    q = np.zeros(cap, dtype=np.uintp)
+    rank = np.zeros(1, dtype=np.uintp)
+    processed = lib().orc_partial_ple(_u64(a), m, n, a.shape[1], _szarr(swaps), _szarr(q), _szarr(rank))
+    r = int(rank[0])
+    q = q[:r].copy()
+    return Outcome(r, swaps[:r].copy(), q, canonical_col_swaps(q)), int(processed)
+
+
+def ref_partial_ple(a: np.ndarray, m: int, n: int):
+    """The compiled reference's partial_ple, in place. Returns (Outcome, processed)."""
+    cap = max(1, min(m, n))
+    swaps = np.zeros(cap, dtype=np.uintp)
+    q = np.zeros(cap, dtype=np.uintp)
+    rank = np.zeros(1, dtype=np.uintp)
+    processed = ref().ref_partial_ple(_u64(a), m, n, a.shape[1], _szarr(swaps), _szarr(q), _szarr(rank))
+    r = int(rank[0])
+    q = q[:r].copy()
+    return Outcome(r, swaps[:r].copy(), q, canonical_col_swaps(q)), int(processed)
 
 
 def undo_col_swaps(a: np.ndarray, m: int, cs: np.ndarray) -> None:

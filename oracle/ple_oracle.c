@@ -244,6 +244,85 @@ size_t orc_ple(word* A, size_t m, size_t n, size_t stride, size_t* swaps, size_t
     return r;
 }
 
+/* Row dst ^= row src over columns [c0, n) (row_add_from, bit_matrix.hpp:273-279). */
+static void add_row_from(word* A, size_t stride, size_t n, size_t dst, size_t src, size_t c0) {
+    if (c0 >= n) return;
+    word* d = A + dst * stride;
+    const word* s = A + src * stride;
+    const size_t W = (n + 63) / 64, w0 = c0 >> 6;
+    d[w0] ^= s[w0] & ~low_mask(c0 & 63);
+    for (size_t w = w0 + 1; w < W; ++w) d[w] ^= s[w];
+}
+
+/* The lazy single pass partial_ple (ple.hpp:57-130), restated with its
+ * watermarks: wm[l] = the last row that carries pivot l's update. A row is
+ * brought up to date (every pivot whose watermark lies above it, in pivot
+ * order, each added from one past its pivot column) the first time the scan
+ * reads it; the pivot of a column is the first row >= r holding a 1 after
+ * that; the rows between a pivot's watermark and the deepest row read get a
+ * catch-up at the end; then the multiplier columns are compressed. rank in
+ * *rank_out; returns processed = max(rank, deepest row read + 1), or 0 when
+ * no pivot exists. swaps / q need capacity min(m, n). */
+size_t orc_partial_ple(word* A, size_t m, size_t n, size_t stride, size_t* swaps, size_t* q,
+                       size_t* rank_out) {
+    const size_t cap = m < n ? m : n;
+    size_t* wm = (size_t*)malloc((cap ? cap : 1) * sizeof(size_t));
+    size_t r = 0, c = 0;
+    while (r < m && c < n) {
+        int found = 0;
+        size_t pi = 0, pj = 0;
+        for (size_t j = c; j < n && !found; ++j) {
+            for (size_t i = r; i < m; ++i) {
+                if (r > 0 && i > wm[r - 1]) {
+                    size_t lo = 0, hi = r; /* first l with wm[l] < i (wm non-increasing) */
+                    while (lo < hi) {
+                        const size_t mid = (lo + hi) / 2;
+                        if (wm[mid] >= i) lo = mid + 1; else hi = mid;
+                    }
+                    for (size_t l = lo; l < r; ++l) {
+                        if ((A[i * stride + (q[l] >> 6)] >> (q[l] & 63)) & 1)
+                            add_row_from(A, stride, n, i, l, q[l] + 1);
+                        wm[l] = i;
+                    }
+                }
+                if ((A[i * stride + (j >> 6)] >> (j & 63)) & 1) {
+                    found = 1;
+                    pi = i;
+                    pj = j;
+                    break;
+                }
+            }
+        }
+        if (!found) break;
+        swaps[r] = pi;
+        q[r] = pj;
+        if (pi != r) {
+            word* x = A + r * stride;
+            word* y = A + pi * stride;
+            for (size_t w = 0; w < (n + 63) / 64; ++w) {
+                const word t = x[w];
+                x[w] = y[w];
+                y[w] = t;
+            }
+        }
+        wm[r] = pi;
+        ++r;
+        c = pj + 1;
+    }
+    *rank_out = r;
+    if (r == 0) {
+        free(wm);
+        return 0;
+    }
+    const size_t deepest = wm[0];
+    for (size_t j = 0; j < r; ++j)
+        for (size_t i = (wm[j] + 1 > r ? wm[j] + 1 : r); i <= deepest; ++i)
+            if ((A[i * stride + (q[j] >> 6)] >> (q[j] & 63)) & 1) add_row_from(A, stride, n, i, j, q[j] + 1);
+    for (size_t j = 0; j < r; ++j) swap_cols_from_row(A, m, stride, j, q[j], j);
+    free(wm);
+    return deepest + 1 > r ? deepest + 1 : r;
+}
+
 /* The canonical compression list {j, q[j], j} for q[j] != j, in application
  * order; the same swaps block_iterative_ple records at ple.hpp:232-236 when
  * its stripe width is 1. Returns the count; out holds 3 entries per swap. */

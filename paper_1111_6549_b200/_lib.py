@@ -98,6 +98,11 @@ SYMBOLS = {
     "gf2cu_default_config": (None, [C.POINTER(gf2cu_cfg)]),
     "gf2cu_ple": (C.c_int, [C.POINTER(gf2cu_view), C.POINTER(gf2cu_cfg), _szp, _szp, _szp,
                             C.POINTER(gf2cu_colswap), _szp, C.POINTER(gf2cu_stats)]),
+    "gf2cu_partial_ple": (C.c_int, [C.POINTER(gf2cu_view), C.POINTER(gf2cu_cfg), _szp, _szp, _szp, _szp,
+                                    C.POINTER(gf2cu_colswap), _szp]),
+    "gf2cu_undo_column_swaps": (C.c_int, [C.POINTER(gf2cu_view), C.POINTER(gf2cu_colswap), _sz,
+                                          C.POINTER(gf2cu_cfg)]),
+    "gf2cu_undo_column_swaps_device": (C.c_int, [_mp, C.POINTER(gf2cu_colswap), _sz, C.c_void_p]),
     "gf2cu_last_error": (C.c_char_p, []),
     "gf2cu_device_count": (C.c_int, []),
     "gf2cu_version": (C.c_char_p, []),

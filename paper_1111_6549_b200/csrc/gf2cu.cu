@@ -70,6 +70,7 @@ size_t wpad8(size_t W) { return std::max<size_t>(8, (W + 7) / 8 * 8); }
 size_t padded_stride(size_t n) { return std::max<size_t>(16, (words_of(n) + 15) / 16 * 16); }
 
 struct Workspace {
+    bool ready = false;  // every buffer below allocated (ensure_ws)
     size_t m = 0, Wp = 0, W = 0;
     u32* perm = nullptr;
     u64* pb = nullptr;
@@ -237,9 +238,25 @@ cudaStream_t pick_stream(gf2cu_matrix* a, void* s) {
     return s ? reinterpret_cast<cudaStream_t>(s) : a->own;
 }
 
+gf2cu_status alloc_ws(gf2cu_matrix* a);
+
+// The workspace is all-or-nothing: a failed allocation frees whatever was
+// already allocated, so the next call on the (cached) matrix retries from
+// scratch instead of launching on null buffers.
 gf2cu_status ensure_ws(gf2cu_matrix* a) {
+    if (a->ws.ready) return GF2CU_OK;
+    free_ws(a->ws);
+    const gf2cu_status st = alloc_ws(a);
+    if (st != GF2CU_OK) {
+        free_ws(a->ws);
+        return st;
+    }
+    a->ws.ready = true;
+    return GF2CU_OK;
+}
+
+gf2cu_status alloc_ws(gf2cu_matrix* a) {
     Workspace& w = a->ws;
-    if (w.perm) return GF2CU_OK;
     const size_t m = a->m, mn = std::max<size_t>(1, std::min(a->m, a->n));
     w.m = m;
     w.Wp = a->Wp;
@@ -268,9 +285,12 @@ gf2cu_status ensure_ws(gf2cu_matrix* a) {
     return GF2CU_OK;
 }
 
+// PleConfig never makes the reference throw: pick_table_bits clamps any
+// k_scale (<= 0, tiny, huge) to k in [1, 16] (gray_code.hpp:171-177) and the
+// driver clamps k and table_count (ple.hpp:168-169, 201). The device output
+// does not depend on k, so every configuration is accepted here as well.
 gf2cu_status check_cfg(const gf2cu_cfg* cfg) {
-    if (!cfg) return GF2CU_OK;
-    if (!(cfg->k_scale > 0.0) && cfg->k == 0) return fail(GF2CU_EINVAL, "k_scale must be > 0");
+    (void)cfg;
     return GF2CU_OK;
 }
 
@@ -472,20 +492,32 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
     if (G < 1 || G > (unsigned)gf2cu::kMaxRanks || (unsigned)sms / G < 2)
         return fail(GF2CU_EINVAL, "peer driver: 1..8 ranks, at least 2 CTAs each");
     PeerWs& pw = a->pw;
-    if (pw.G != G || pw.block != block) {
+    if (!pw.dp || pw.G != G || pw.block != block) {
+        // all-or-nothing: (G, block) are recorded only once every buffer is
+        // allocated, so a failed setup is retried by the next call
         free_peer(pw);
+        const auto setup = [&]() -> gf2cu_status {
+            pw.hp.assign(G, gf2cu::PeerParams{});
+            for (unsigned k = 0; k < G; ++k) {
+                void* xbuf = nullptr;
+                gf2cu_status st = peer_alloc_rank(pw.hp[k], pw.allocs, m, n, k, G, block, &xbuf);
+                if (st != GF2CU_OK) return st;
+            }
+            for (unsigned k = 0; k < G; ++k)
+                for (unsigned j = 0; j < G; ++j) pw.hp[k].peer[j] = pw.hp[j].peer[j];
+            gf2cu::PeerParams* dp = nullptr;
+            CU_TRY(cudaMalloc(&dp, G * sizeof(gf2cu::PeerParams)));
+            pw.dp = dp;
+            CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
+            return GF2CU_OK;
+        };
+        const gf2cu_status st = setup();
+        if (st != GF2CU_OK) {
+            free_peer(pw);
+            return st;
+        }
         pw.G = G;
         pw.block = block;
-        pw.hp.assign(G, gf2cu::PeerParams{});
-        for (unsigned k = 0; k < G; ++k) {
-            void* xbuf = nullptr;
-            gf2cu_status st = peer_alloc_rank(pw.hp[k], pw.allocs, m, n, k, G, block, &xbuf);
-            if (st != GF2CU_OK) return st;
-        }
-        for (unsigned k = 0; k < G; ++k)
-            for (unsigned j = 0; j < G; ++j) pw.hp[k].peer[j] = pw.hp[j].peer[j];
-        CU_TRY(cudaMalloc(&pw.dp, G * sizeof(gf2cu::PeerParams)));
-        CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
     }
     const bool super = peer_super(m, W, cfg ? cfg->flags : 0u);
     const u32 wpad = super ? (u32)std::max<size_t>(4, (W + 3) / 4 * 4) : (u32)wpad8(W);
@@ -564,7 +596,11 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
 
     gf2cu::Params p{};
-    if (!a->alt) CU_TRY(cudaMalloc(&a->alt, std::max<size_t>(1, m) * wpad8(W) * sizeof(u64)));
+    if (!a->alt) {  // (assigned only on success: a failed call leaves it null)
+        u64* alt = nullptr;
+        CU_TRY(cudaMalloc(&alt, std::max<size_t>(1, m) * wpad8(W) * sizeof(u64)));
+        a->alt = alt;
+    }
     p.mat = a->alt;
     p.perm = ws.perm;
     p.pb = ws.pb;
@@ -613,12 +649,19 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     const u32 Wpad4 = (u32)std::max<size_t>(4, (W + 3) / 4 * 4);
     if (!multi) {
         if (!ws.ubuf) {
-            ws.ucap = std::max<size_t>(1, std::min(m, n));
-            CU_TRY(cudaMalloc(&ws.ubuf, ws.ucap * p.Wpad8 * sizeof(u64)));
+            const size_t cap = std::max<size_t>(1, std::min(m, n));
+            u64* ub = nullptr;
+            CU_TRY(cudaMalloc(&ub, cap * p.Wpad8 * sizeof(u64)));
+            ws.ubuf = ub;
+            ws.ucap = cap;
         }
         p.ubuf = ws.ubuf;
         p.ucap = (u32)ws.ucap;
-        if (!ws.apctr) CU_TRY(cudaMalloc(&ws.apctr, 2 * (W + 1) * sizeof(u32)));
+        if (!ws.apctr) {
+            u32* ap = nullptr;
+            CU_TRY(cudaMalloc(&ap, 2 * (W + 1) * sizeof(u32)));
+            ws.apctr = ap;
+        }
         p.ap_claim = ws.apctr;
         p.ap_done = ws.apctr + W + 1;
         const char* dv = std::getenv("GF2CU_PW_DIV");
@@ -699,7 +742,14 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             // few rows each, so that little is left to copy after the kernel)
             uint64_t* host = stream_to->data + (stream_to->col_off >> 6);
             for (;;) {
-                const bool fin = cudaEventQuery(kdone) == cudaSuccess;
+                const cudaError_t qe = cudaEventQuery(kdone);
+                if (qe != cudaSuccess && qe != cudaErrorNotReady) {
+                    // a faulted kernel never completes the event: fail
+                    // instead of polling the row count forever
+                    cudaEventDestroy(kdone);
+                    return cuda_fail(qe, "persistent PLE kernel (streamed output)");
+                }
+                const bool fin = qe == cudaSuccess;
                 const size_t avail = *reinterpret_cast<volatile u32*>(ws.out_host);
                 const size_t chunk = std::max<size_t>(256, std::min<size_t>(m / 32, (m - sent) / 8));
                 if (avail > sent && (avail - sent >= chunk || fin)) {
@@ -775,7 +825,11 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     const size_t rk = std::min<size_t>((size_t)fin.r + fin.rb, std::min(m, n));
 
     // swaps / q to pinned staging first (they do not depend on the untile)
-    if (rk && !ws.h_out) CU_TRY(cudaMallocHost(&ws.h_out, 2 * std::min(m, n) * sizeof(u32)));
+    if (rk && !ws.h_out) {
+        u32* ho = nullptr;
+        CU_TRY(cudaMallocHost(&ho, 2 * std::min(m, n) * sizeof(u32)));
+        ws.h_out = ho;
+    }
     u32* sw = ws.h_out;
     u32* qq = ws.h_out + std::min(m, n);
     if (rk) {
@@ -1080,8 +1134,8 @@ gf2cu_status view_upload(const gf2cu_view* v, gf2cu_matrix* a, cudaStream_t s,
 
 // Device rows -> host window (bits outside the window untouched); synchronous.
 gf2cu_status view_download(const gf2cu_view* v, const gf2cu_matrix* a, cudaStream_t s,
-                           std::vector<u64>& packed, size_t row_lo = 0) {
-    const size_t m = v->nrows, n = v->ncols, W = a->W;
+                           std::vector<u64>& packed, size_t row_lo = 0, size_t row_hi = ~size_t(0)) {
+    const size_t m = std::min(v->nrows, row_hi), n = v->ncols, W = a->W;
     if (m == 0 || W == 0) return GF2CU_OK;
     cudaError_t e;
     if (view_aligned(v)) {
@@ -1109,7 +1163,7 @@ gf2cu_status view_download(const gf2cu_view* v, const gf2cu_matrix* a, cudaStrea
 // body(matrix, cfg), download.
 template <class Body>
 gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* stats, Body&& body,
-                       size_t* rows_done = nullptr) {
+                       size_t* rows_done = nullptr, const size_t* rows_limit = nullptr) {
     gf2cu_cfg c;
     gf2cu_default_config(&c);
     if (cfg) c = *cfg;
@@ -1124,7 +1178,8 @@ gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* s
     c.stream = s;
     st = body(a, c);
     if (st == GF2CU_OK) {
-        st = view_download(v, a, s, packed, rows_done ? *rows_done : 0);
+        st = view_download(v, a, s, packed, rows_done ? *rows_done : 0,
+                           rows_limit ? *rows_limit : ~size_t(0));
         if (stats) {
             stats->h2d_bytes = double(a->m) * a->W * 8;
             stats->d2h_bytes = double(a->m) * a->W * 8;
@@ -1381,6 +1436,98 @@ gf2cu_status gf2cu_ple_device(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swa
     if (st != GF2CU_OK) return st;
     DeviceGuard g(a->device);
     return run_ple(a, cfg, swaps, q, rank, col_swaps, n_col_swaps, stats);
+}
+
+// partial_ple (ple.hpp:57-130). Its pivot search reads every row of a column
+// before giving up on it, so it finds the same pivots as the complete
+// decomposition (rank, q, p.swaps equal), and every row it reads ends fully
+// updated. Only its laziness differs: when every column 0..n-1 finds a pivot
+// (rank == n < m; q is then the identity and no compression swap exists), the
+// rows past the deepest pivot row were never read and stay untouched, and
+// processed = max(rank, max swaps + 1) (the watermark s[0] + 1, :128). In
+// every other case a pivotless column (or r reaching m) made the scan read
+// all rows: processed = m, and the in-place result is the complete PLE's.
+// rank 0 leaves processed = 0 (:113-116) and the matrix unchanged.
+static size_t partial_processed(size_t m, size_t n, size_t rank, const size_t* swaps) {
+    if (rank == 0) return 0;
+    if (!(rank == n && n < m)) return m;
+    size_t smax = 0;
+    for (size_t l = 0; l < rank; ++l) smax = std::max(smax, swaps[l]);
+    return std::max(rank, smax + 1);
+}
+
+gf2cu_status gf2cu_partial_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
+                               size_t* rank, size_t* processed, gf2cu_colswap* col_swaps,
+                               size_t* n_col_swaps) {
+    if (!v || !rank || !processed) return fail(GF2CU_EINVAL, "null argument");
+    gf2cu_status st = check_view(v);
+    if (st != GF2CU_OK) return st;
+    const size_t m = v->nrows, n = v->ncols;
+    if ((!swaps || !q) && std::min(m, n) > 0) return fail(GF2CU_EINVAL, "null outputs");
+    st = check_cfg(cfg);
+    if (st != GF2CU_OK) return st;
+    *processed = 0;
+    if (m == 0 || n == 0) {
+        *rank = 0;
+        if (n_col_swaps) *n_col_swaps = 0;
+        return GF2CU_OK;
+    }
+    size_t limit = m;
+    st = with_view(
+        v, cfg, nullptr,
+        [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
+            gf2cu_status s2 = run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, nullptr);
+            if (s2 == GF2CU_OK) limit = partial_processed(m, n, *rank, swaps);
+            return s2;
+        },
+        nullptr, &limit);
+    if (st == GF2CU_OK) *processed = limit;
+    return st;
+}
+
+static gf2cu_status run_undo_col_swaps(gf2cu_matrix* a, const gf2cu_colswap* cs, size_t ncs, cudaStream_t s) {
+    if (ncs == 0 || a->m == 0) return GF2CU_OK;
+    std::vector<ulonglong2> h(ncs);  // {a | b << 32, from_row}
+    for (size_t i = 0; i < ncs; ++i) h[i] = make_ulonglong2((u64)cs[i].a | ((u64)cs[i].b << 32), cs[i].from_row);
+    ulonglong2* d = nullptr;
+    CU_TRY(cudaMallocAsync(&d, ncs * sizeof(ulonglong2), s));
+    cudaError_t e = cudaMemcpyAsync(d, h.data(), ncs * sizeof(ulonglong2), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        const unsigned blocks = (unsigned)std::min<size_t>((a->m + 255) / 256, 65535u * 16);
+        gf2cu::undo_col_swaps_kernel<<<blocks, 256, 0, s>>>(a->data, (u32)a->m, (u32)a->Wp, d, (u32)ncs);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // (h outlives the copy)
+    cudaFreeAsync(d, s);
+    return e == cudaSuccess ? GF2CU_OK : cuda_fail(e, "undo_column_swaps");
+}
+
+static gf2cu_status check_col_swaps(size_t m, size_t n, const gf2cu_colswap* cs, size_t ncs) {
+    if (ncs && !cs) return fail(GF2CU_EINVAL, "null col_swaps");
+    for (size_t i = 0; i < ncs; ++i)
+        if (cs[i].a >= n || cs[i].b >= n || cs[i].from_row > m || m >= (1ull << 32) || n >= (1ull << 32))
+            return fail(GF2CU_ERANGE, "column swap outside the matrix");
+    return GF2CU_OK;
+}
+
+gf2cu_status gf2cu_undo_column_swaps_device(gf2cu_matrix* a, const gf2cu_colswap* col_swaps,
+                                            size_t n_col_swaps, void* stream) {
+    if (!a) return fail(GF2CU_EINVAL, "null matrix");
+    gf2cu_status st = check_col_swaps(a->m, a->n, col_swaps, n_col_swaps);
+    if (st != GF2CU_OK) return st;
+    DeviceGuard g(a->device);
+    return run_undo_col_swaps(a, col_swaps, n_col_swaps, pick_stream(a, stream));
+}
+
+gf2cu_status gf2cu_undo_column_swaps(const gf2cu_view* v, const gf2cu_colswap* col_swaps,
+                                     size_t n_col_swaps, const gf2cu_cfg* cfg) {
+    gf2cu_status st = check_view(v);
+    if (st != GF2CU_OK) return st;
+    st = check_col_swaps(v->nrows, v->ncols, col_swaps, n_col_swaps);
+    if (st != GF2CU_OK || n_col_swaps == 0 || v->nrows == 0 || v->ncols == 0) return st;
+    return with_view(v, cfg, nullptr, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
+        return run_undo_col_swaps(a, col_swaps, n_col_swaps, reinterpret_cast<cudaStream_t>(c.stream));
+    });
 }
 
 gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,

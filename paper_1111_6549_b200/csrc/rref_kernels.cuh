@@ -328,6 +328,24 @@ __global__ void rref_echelon_kernel(u64* a, const u32* q, u32 m, u32 W, u32 Wp, 
     }
 }
 
+// undo_column_swaps (ple.hpp:293-296): the compression swaps replayed
+// backwards, swap_cols_from_row(a, b, from_row) (bit_matrix.hpp:302-318) on
+// every row >= from_row. One thread per row, the swap list (<= min(m, n)
+// entries, {a | b << 32, from_row}) read through the uniform cache.
+__global__ void undo_col_swaps_kernel(u64* mat, u32 m, u32 Wp, const ulonglong2* cs, u32 ncs) {
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        u64* row = mat + (size_t)i * Wp;
+        for (u32 k = ncs; k-- > 0;) {
+            const ulonglong2 c = __ldg(cs + k);
+            if (i < c.y) continue;
+            const u32 ca = (u32)c.x, cb = (u32)(c.x >> 32);
+            const u64 x = ((row[ca >> 6] >> (ca & 63u)) ^ (row[cb >> 6] >> (cb & 63u))) & 1ull;
+            row[ca >> 6] ^= x << (ca & 63u);
+            row[cb >> 6] ^= x << (cb & 63u);
+        }
+    }
+}
+
 // trsm_upper_left_unit: X (tile-major N) back to the row-major B buffer.
 __global__ void trsm_store_kernel(RrefParams p) {
     const u64 total = (u64)p.r * p.W;

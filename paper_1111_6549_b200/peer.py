@@ -147,6 +147,12 @@ def run_peer(engine, dist, group=None) -> ShardResult:
     engine.reset()
     dist.barrier(group=group)
     engine.run()
+    # On its last step every rank still signals into every peer's counters
+    # and no rank waits for those signals; a rank that reset for its next run
+    # before a slow peer's late signal landed would start one count ahead.
+    # run() returns once this rank's kernel has completed, so after this
+    # barrier every kernel (and every store it issued) is done.
+    dist.barrier(group=group)
     return engine.finish()
 
 

@@ -142,6 +142,18 @@ class MatrixView:
         self.col_off = int(col_off)
         self._nrows = int(nrows)
         self._ncols = int(ncols)
+        if min(self.stride, self.col_off, self._nrows, self._ncols) < 0:
+            raise IndexError("negative view geometry")
+        if self._nrows and self._ncols:
+            # the device path writes L\E back through the raw pointer: the
+            # window must lie inside the array (bit_matrix.hpp:214-221 raise
+            # std::out_of_range for windows outside the matrix)
+            end = self.col_off + self._ncols
+            if end > 64 * self.stride:
+                raise IndexError("view window wider than its stride")
+            need = (self._nrows - 1) * self.stride + (end + 63) // 64
+            if words.size < need:
+                raise IndexError(f"view needs {need} words, array holds {words.size}")
 
     def nrows(self) -> int:
         return self._nrows
@@ -390,6 +402,51 @@ def block_iterative_ple(a, cfg: Optional[PleConfig] = None) -> PleOutcome:
         v = view._c()
         check(L.gf2cu_ple(C.byref(v), C.byref(c), sp, qp, C.byref(rank), cp, C.byref(ncs), C.byref(st)))
     return _outcome(rank, swaps, q, cs, ncs, m, st)
+
+
+def partial_ple(a, cfg: Optional[PleConfig] = None) -> PleOutcome:
+    """gf2::partial_ple (ple.hpp:57-130) on the B200: the lazy single pass.
+    Same rank / q / p.swaps / col_swaps as the reference; ``processed`` is
+    its watermark and rows past it are left untouched (only possible when
+    every column finds a pivot and rank == ncols < nrows). Host views only,
+    as the reference's MatrixView."""
+    if isinstance(a, DeviceMatrix):
+        raise TypeError("partial_ple takes a host BitMatrix / MatrixView")
+    cfg = cfg or PleConfig()
+    L = _lib.load()
+    c = cfg.to_c()
+    view = _host_view(a)
+    m, n = view.nrows(), view.ncols()
+    cap = max(1, min(m, n))
+    swaps = np.empty(cap, dtype=np.uintp)
+    q = np.empty(cap, dtype=np.uintp)
+    cs = np.empty((cap, 3), dtype=np.uintp)
+    rank, processed, ncs = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    szp = C.POINTER(C.c_size_t)
+    v = view._c()
+    check(L.gf2cu_partial_ple(C.byref(v), C.byref(c), swaps.ctypes.data_as(szp), q.ctypes.data_as(szp),
+                              C.byref(rank), C.byref(processed),
+                              C.cast(cs.ctypes.data, C.POINTER(gf2cu_colswap)), C.byref(ncs)))
+    r = int(rank.value)
+    return PleOutcome(rank=r, processed=int(processed.value), p=RowPermutation(swaps[:r].astype(np.uint64)),
+                      q=q[:r].astype(np.uint64), col_swaps_array=cs[: int(ncs.value)].astype(np.uint64))
+
+
+def undo_column_swaps(a, col_swaps, cfg: Optional[PleConfig] = None) -> None:
+    """gf2::undo_column_swaps (ple.hpp:293-296) on the B200: the compression
+    swaps (a list of ColSwap or a (k, 3) array) replayed backwards."""
+    if isinstance(col_swaps, np.ndarray):
+        arr = np.ascontiguousarray(col_swaps.reshape(-1, 3), dtype=np.uintp)
+    else:
+        arr = np.array([[c.a, c.b, c.from_row] for c in col_swaps], dtype=np.uintp).reshape(-1, 3)
+    L = _lib.load()
+    cp = C.cast(arr.ctypes.data, C.POINTER(gf2cu_colswap)) if len(arr) else None
+    if isinstance(a, DeviceMatrix):
+        check(L.gf2cu_undo_column_swaps_device(a.handle, cp, len(arr), None))
+        return
+    c = (cfg or PleConfig()).to_c()
+    v = _host_view(a)._c()
+    check(L.gf2cu_undo_column_swaps(C.byref(v), cp, len(arr), C.byref(c)))
 
 
 def _host_view(a) -> MatrixView:

@@ -93,6 +93,7 @@ FULL = [
     ("c3_32768_p256", 32768, 32768, "fill_random", 1 / 256, 1),
     ("c4_32768_xy", 32768, 32768, "xy", 24576, (11, 12)),
     ("c5_65536_ctr", 65536, 65536, "ctr", None, 1),
+    ("c5_131072_ctr", 131072, 131072, "ctr", None, 1),
 ]
 
 

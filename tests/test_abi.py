@@ -58,9 +58,14 @@ def test_argument_validation_maps_to_reference_exceptions():
     a = G.BitMatrix(4, 4)
     with pytest.raises(ValueError):
         G.fill_random(a, 1.5, 1)  # std::invalid_argument (bit_matrix.hpp:460)
-    v = G.MatrixView(a.words, 1, 10, 4, 60)  # window past the row stride
-    with pytest.raises(IndexError):
-        G.block_iterative_ple(v)
+    with pytest.raises(IndexError):  # window past the row stride
+        G.block_iterative_ple(G.MatrixView(a.words, 1, 10, 4, 60))
+    with pytest.raises(IndexError):  # more rows than the array holds
+        G.MatrixView(a.words, 1, 0, 5, 4)
+    with pytest.raises(IndexError):  # a stride that walks off the array
+        G.MatrixView(np.zeros(10, dtype=np.uint64), 3, 0, 5, 64)
+    ok = G.MatrixView(np.zeros(10, dtype=np.uint64), 3, 0, 4, 63)  # (4-1)*3 + 1 = 10 words
+    assert ok.nrows() == 4
     with pytest.raises(IndexError):
         a.view().sub(1, 0, 4, 4)  # std::out_of_range (bit_matrix.hpp:218-221)
 

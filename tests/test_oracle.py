@@ -119,3 +119,52 @@ def test_oracle_properties_medium():
     b = a.copy()
     oa = O.ple(b, m, n)
     assert O.ref_reconstructs(a, b, m, n, oa)
+
+
+def partial_processed_rule(m, n, rank, swaps):
+    """The rule gf2cu_partial_ple applies (csrc/gf2cu.cu partial_processed):
+    processed < m only when every column finds a pivot and rank == n < m."""
+    if rank == 0:
+        return 0
+    if not (rank == n and n < m):
+        return m
+    return max(rank, int(max(swaps)) + 1)
+
+
+def _partial_cases():
+    rng = np.random.default_rng(2026)
+    for i in range(300):
+        m, n = int(rng.integers(1, 140)), int(rng.integers(1, 140))
+        if i % 3 == 0:  # tall: full column rank is likely, so the lazy pass stops early
+            n = int(rng.integers(1, 40))
+            m = n + int(rng.integers(1, 100))
+        kind = i % 7
+        yield m, n, S.build(m, n, kind, int(rng.integers(0, 2**62)))
+
+
+def test_partial_ple_restatement_vs_reference():
+    """orc_partial_ple (the watermark restatement) == the compiled reference's
+    partial_ple: words, rank, swaps, q, processed; and the processed rule the
+    device path uses reproduces the reference's watermark."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    early = 0
+    for m, n, a in _partial_cases():
+        x, y = a.copy(), a.copy()
+        got, gp = O.partial_ple(x, m, n)
+        want, wp = O.ref_partial_ple(y, m, n)
+        assert (got.rank, gp) == (want.rank, wp), (m, n)
+        assert np.array_equal(got.swaps, want.swaps) and np.array_equal(got.q, want.q), (m, n)
+        assert np.array_equal(x, y), (m, n)
+        assert partial_processed_rule(m, n, want.rank, want.swaps) == wp, (m, n)
+        if wp < m:
+            early += 1
+            # rows past the watermark are untouched (acceptance_main.cpp:127-139)
+            assert np.array_equal(y[wp:], a[wp:])
+        # rank / q / swaps are the complete decomposition's
+        z = a.copy()
+        full = O.ple(z, m, n)
+        assert full.rank == want.rank and np.array_equal(full.q, want.q)
+        assert np.array_equal(full.swaps, want.swaps)
+        assert np.array_equal(z[:wp], y[:wp])
+    assert early > 20  # the lazy early stop is exercised

@@ -274,3 +274,83 @@ def test_panel_tuning_bits_exact(m, n, gen, monkeypatch):
             bm = G.BitMatrix(m, n, a.copy())
             got = G.block_iterative_ple(bm, cfg)
             assert_same(ref, want, bm, got, what=f"{gen} {m}x{n} flags={flags}")
+
+
+@pytest.mark.parametrize("k,k_scale,tables", [(0, 0.0, 4), (0, -3.0, 4), (0, float("nan"), 1),
+                                             (0, 1e-9, 0), (0, 1e9, 4), (99, -1.0, 100)])
+def test_any_pleconfig_is_accepted(k, k_scale, tables):
+    """pick_table_bits clamps any k_scale to k in [1, 16] (gray_code.hpp:171-177)
+    and the driver clamps k / table_count (ple.hpp:168-169, 201): the reference
+    never throws on a PleConfig, and the output does not depend on it."""
+    a = O.fill_random(300, 200, 0.5, 5)
+    cfg = G.PleConfig(k=k, k_scale=k_scale, table_count=tables)
+    assert_same(*run_both(a, 300, 200, cfg), what=f"k={k} k_scale={k_scale} tables={tables}")
+
+
+def test_partial_ple_device_matches_reference():
+    """gf2cu_partial_ple (ple.hpp:57-130) against the compiled reference's
+    partial_ple: in-place words (rows past the watermark untouched), rank,
+    p.swaps, q, processed, col_swaps."""
+    rng = np.random.default_rng(4242)
+    early = 0
+    cases = [(0, 5), (5, 0), (1, 1), (70, 64), (200, 64), (300, 65), (64, 64), (129, 63)]
+    cases += [(int(rng.integers(1, 300)), int(rng.integers(1, 300))) for _ in range(40)]
+    cases += [(n + int(rng.integers(1, 200)), n) for n in rng.integers(1, 130, 40)]
+    for i, (m, n) in enumerate(cases):
+        a = S.build(m, n, i % 7, int(rng.integers(0, 2**62))) if m and n else np.zeros((m, 1), np.uint64)
+        want_words = a.copy()
+        if m and n:
+            want, wp = O.partial_ple(want_words, m, n)
+        else:
+            want, wp = O.Outcome(0, np.zeros(0), np.zeros(0)), 0
+        bm = G.BitMatrix(m, n, a.copy()) if m and n else G.BitMatrix(m, n)
+        got = G.partial_ple(bm)
+        assert (got.rank, got.processed) == (want.rank, wp), (m, n)
+        assert np.array_equal(got.p.swaps, np.asarray(want.swaps, np.uint64)), (m, n)
+        assert np.array_equal(got.q, np.asarray(want.q, np.uint64)), (m, n)
+        if m and n:
+            assert np.array_equal(bm.words, want_words), (m, n)
+        early += wp < m
+    assert early > 10
+
+
+def test_undo_column_swaps_device():
+    """gf2cu_undo_column_swaps (ple.hpp:293-296) vs the restatement, on a
+    rank-deficient PLE's canonical list and on arbitrary swap lists, host
+    view (unaligned sub-view) and device-resident."""
+    m, n = 300, 260
+    a = O.mul(O.fill_ctr(m, 200, 9), 200, O.fill_ctr(200, n, 10), n)  # rank <= 200 < n
+    bm = G.BitMatrix(m, n, a.copy())
+    out = G.block_iterative_ple(bm)
+    assert len(out.col_swaps) > 0
+    want = bm.words.copy()
+    O.undo_col_swaps(want, m, out.col_swaps_array.astype(np.uintp))
+    G.undo_column_swaps(bm, out.col_swaps)
+    assert np.array_equal(bm.words, want)
+    rng = np.random.default_rng(5)
+    cs = np.stack([rng.integers(0, 190, 40), rng.integers(0, 190, 40), rng.integers(0, 120, 40)], 1)
+    par = O.fill_random(120, 320, 0.5, 10)
+    win = G.MatrixView(par, par.shape[1], 70, 120, 190)
+    sub = np.zeros((120, 3), dtype=np.uint64)
+    for i in range(120):  # the window as a packed 120 x 190 matrix
+        for j in range(190):
+            if (int(par[i, (70 + j) >> 6]) >> ((70 + j) & 63)) & 1:
+                sub[i, j >> 6] |= np.uint64(1) << np.uint64(j & 63)
+    O.undo_col_swaps(sub, 120, cs.astype(np.uintp))
+    before = par.copy()
+    G.undo_column_swaps(win, cs)
+    for i in range(120):
+        for j in range(320):
+            bit = (int(par[i, j >> 6]) >> (j & 63)) & 1
+            if 70 <= j < 260:
+                assert bit == (int(sub[i, (j - 70) >> 6]) >> ((j - 70) & 63)) & 1
+            else:
+                assert bit == (int(before[i, j >> 6]) >> (j & 63)) & 1
+    d = G.DeviceMatrix(m, n)
+    d.upload(a)
+    G.undo_column_swaps(d, cs)
+    want = a.copy()
+    O.undo_col_swaps(want, m, cs.astype(np.uintp))
+    assert np.array_equal(d.download(), want)
+    with pytest.raises(IndexError):
+        G.undo_column_swaps(G.BitMatrix(4, 4), [G.ColSwap(0, 4, 0)])
