@@ -158,6 +158,55 @@ void trsm_upper_left_unit(CView u, View b, const DeviceOptions& dev = {}) {
     detail::throw_status(gf2cu_trsm_upper_left_unit(&uv, &bv, &c));
 }
 
+// partial_ple (ple.hpp:57-130) on the B200: the lazy single pass. Same rank,
+// q, p.swaps and col_swaps as the reference; out.processed is its watermark
+// and the rows past it are left untouched (gf2cu_partial_ple).
+template <class View = gf2::MatrixView>
+gf2::PleOutcome partial_ple(View a, const DeviceOptions& dev = {}) {
+    gf2cu_view v = detail::to_view(a);
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    c.device = dev.device;
+    c.stream = dev.stream;
+    const std::size_t cap = std::max<std::size_t>(1, std::min(v.nrows, v.ncols));
+    std::vector<std::size_t> swaps(cap), q(cap);
+    std::vector<gf2cu_colswap> cs(cap);
+    std::size_t rank = 0, processed = 0, ncs = 0;
+    detail::throw_status(gf2cu_partial_ple(&v, &c, swaps.data(), q.data(), &rank, &processed, cs.data(), &ncs));
+    gf2::PleOutcome out;
+    out.rank = rank;
+    out.processed = processed;
+    out.p.swaps.assign(swaps.begin(), swaps.begin() + rank);
+    out.q.assign(q.begin(), q.begin() + rank);
+    for (std::size_t i = 0; i < ncs; ++i) out.col_swaps.push_back({cs[i].a, cs[i].b, cs[i].from_row});
+    return out;
+}
+
+// undo_column_swaps (ple.hpp:293-296) on the B200.
+template <class View = gf2::MatrixView>
+void undo_column_swaps(View a, const std::vector<gf2::ColSwap>& swaps, const DeviceOptions& dev = {}) {
+    gf2cu_view v = detail::to_view(a);
+    gf2cu_cfg c;
+    gf2cu_default_config(&c);
+    c.device = dev.device;
+    c.stream = dev.stream;
+    std::vector<gf2cu_colswap> cs;
+    cs.reserve(swaps.size());
+    for (const auto& x : swaps) cs.push_back(gf2cu_colswap{x.a, x.b, x.from_row});
+    detail::throw_status(gf2cu_undo_column_swaps(&v, cs.data(), cs.size(), &c));
+}
+
+// echelonize(a, strategy, full, cfg) (m4ri.hpp:87-106) on the B200. Every
+// strategy's result is the same matrix -- the reduced form is unique, and the
+// non-reduced forms of naive / m4ri / ple_iterative / ple_recursive coincide
+// (pinned in tests/test_rref_host.py::test_strategy_equivalences_pinned) --
+// so all of them are served by the device PLE + rref_from_ple.
+template <class View, class Strategy, class Cfg = gf2::PleConfig>
+std::size_t echelonize(View a, Strategy, bool full = true, const Cfg& cfg = {},
+                       const DeviceOptions& dev = {}) {
+    return echelonize_ple_iterative(a, full, cfg, dev);
+}
+
 // recursive_ple (ple.hpp:246-289): its in-place result, rank, q and p.swaps
 // equal block_iterative_ple's (pinned in tests/test_rref_host.py), so the
 // device path serves it.

@@ -10,6 +10,8 @@ second device run; multiply: (AB)v = A(Bv) for random v).
     python -m paper_1111_6549_b200.tool ple a.gf2b --verify --out e.gf2b
     python -m paper_1111_6549_b200.tool echelonize a.gf2b [--ref] [--verify]
     python -m paper_1111_6549_b200.tool multiply a.gf2b b.gf2b --out c.gf2b [--verify]
+    python -m paper_1111_6549_b200.tool bench --suite table1|table2|fig3 --sizes 4096 --seeds 1 2 3
+                                              [--memory-budget B] [--device-metrics] [--out f.csv]
 
 --strategy, --k, --tables and --crossover are accepted for compatibility:
 every strategy computes the same result (the device path serves them all;
@@ -153,6 +155,128 @@ def run_multiply(o) -> int:
     return EXIT_OK
 
 
+# ---- bench (gf2tool.cpp:260-423) ------------------------------------------
+BENCH_COLUMNS = ["algorithm", "nrows", "ncols", "density", "k", "tables", "crossover", "seed",
+                 "seconds", "row_adds", "rank"]
+DEVICE_COLUMNS = ["gpus", "K", "bytes_alg", "kernel_seconds", "GBps_eff", "roofline_frac"]
+
+
+class BudgetError(ValueError):
+    pass
+
+
+def check_budget(n: int, budget: int) -> None:
+    """gf2tool.cpp:314-322: matrix plus working copies, 4 * ceil(n/64)*8 * n bytes."""
+    need = 4 * ((n + 63) // 64 * 8) * n
+    if need > budget:
+        raise BudgetError(f"refusing n={n}: estimated {need} bytes exceeds --memory-budget {budget}")
+
+
+def _hbm_peak() -> float:
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+def run_bench(o) -> int:
+    """The reference's timing suites on the device. Every PLE / echelon
+    strategy is the same computation here (one device path serves them all),
+    so each cell times that path through the host API (upload + factor +
+    download: what a caller of the drop-in waits for). row_adds is the
+    reference's CPU op counter (op_count.hpp), which the device does not
+    maintain: 0. --device-metrics appends gpus, K (panel columns), the
+    SURVEY 8(d) algorithmic bytes, the kernel time and effective GB/s, and
+    the fraction of the measured HBM peak."""
+    from .ple import PleConfig
+    k = 0 if o.k == "auto" else int(o.k)
+    cfg = PleConfig(k=k, table_count=o.tables, time_kernels=True)
+    peak = _hbm_peak()
+    rows = []
+
+    def gen(n, seed, nnz):
+        a = BitMatrix(n, n)
+        if nnz == 0:
+            fill_random(a, 0.5, seed)
+        else:
+            fill_random_rows(a, nnz, seed)
+        return a
+
+    def cell(name, a, density, seed, what):
+        work = a.copy()
+        t0 = time.perf_counter()
+        if what == "ple":
+            out = block_iterative_ple(work, cfg)
+            rank, st = out.rank, out.stats
+        else:
+            full = what == "rref"
+            rank = echelonize(work, full, cfg)
+            st = None
+        secs = time.perf_counter() - t0
+        rec = [name, a.nrows(), a.ncols(), density, k, o.tables, o.crossover, seed, secs, 0, rank]
+        if o.device_metrics:
+            ab = st["alg_bytes"] if st else ""
+            ks = st["kernel_ms"] * 1e-3 if st and st["kernel_ms"] else ""
+            gb = (ab / ks / 1e9) if (st and ks) else ""
+            rec += [1, 64, ab, ks, gb, (gb / peak) if gb != "" else ""]
+        rows.append(rec)
+
+    if o.suite == "table1":
+        for n in o.sizes:
+            check_budget(n, o.memory_budget)
+            for seed in o.seeds:
+                a = gen(n, seed, 0)
+                cell("ple-recursive-striped-base", a, "uniform:0.5", seed, "ple")
+                cell("ple-recursive-cubic-base", a, "uniform:0.5", seed, "ple")
+    elif o.suite == "table2":
+        for n in o.sizes:
+            check_budget(n, o.memory_budget)
+            for seed in o.seeds:
+                a = gen(n, seed, 0)
+                cell("m4ri", a, "uniform:0.5", seed, "rref")
+                cell("ple-recursive", a, "uniform:0.5", seed, "rref")
+    else:  # fig3
+        n = o.sizes[0]
+        check_budget(n, o.memory_budget)
+        for seed in o.seeds:
+            cell("ple-recursive", gen(n, seed, 0), "uniform:0.5", seed, "ple")
+            for nnz in range(1, 21):
+                a = gen(n, seed, nnz)
+                cell("ple-recursive", a, f"nnz:{nnz}", seed, "ple")
+                cell("m4ri", a, f"nnz:{nnz}", seed, "ref")
+    cols = BENCH_COLUMNS + (DEVICE_COLUMNS if o.device_metrics else [])
+    text = ",".join(cols) + "\n" + "".join(",".join(_fmt(x) for x in r) + "\n" for r in rows)
+    if o.out:
+        try:
+            with open(o.out, "w") as f:
+                f.write(text)
+        except OSError as e:
+            raise gio.IoError(f"cannot open {o.out} for writing") from e
+    else:
+        sys.stdout.write(text)
+    # one median line per (algorithm, shape, density) cell, on stderr (:291-312)
+    seen = []
+    for r in rows:
+        key = (r[0], r[1], r[3])
+        if key in seen:
+            continue
+        seen.append(key)
+        t = [x[8] for x in rows if (x[0], x[1], x[3]) == key]
+        print(f"median algorithm={r[0]} n={r[1]} density={r[3]} seconds={float(np.median(t))}",
+              file=sys.stderr)
+    return EXIT_OK
+
+
+def _fmt(x) -> str:
+    if isinstance(x, float):
+        return f"{x:.6g}"
+    return str(x)
+
+
 def _common(p, strategy: str) -> None:
     p.add_argument("--strategy", default=strategy,
                    choices=["naive", "m4ri", "ple-iterative", "ple-recursive", "m4rm", "strassen",
@@ -189,6 +313,17 @@ def parser() -> argparse.ArgumentParser:
     m.add_argument("b")
     _common(m, "auto")
     m.set_defaults(out=None)
+    b = sub.add_parser("bench", help="timing suites, CSV on stdout")
+    b.add_argument("--suite", required=True, choices=["table1", "table2", "fig3"])
+    b.add_argument("--sizes", type=int, nargs="+", default=[4096])
+    b.add_argument("--seeds", type=int, nargs="+", default=[1, 2, 3, 4, 5])
+    b.add_argument("--memory-budget", type=int, default=2 << 30)
+    b.add_argument("--k", default="auto")
+    b.add_argument("--tables", type=int, default=1, choices=[1, 2, 4, 8])
+    b.add_argument("--crossover", type=int, default=0)
+    b.add_argument("--out", default="")
+    b.add_argument("--device-metrics", action="store_true",
+                   help="append gpus, K, bytes_alg, kernel_seconds, GBps_eff, roofline_frac")
     return ap
 
 
@@ -200,7 +335,7 @@ def main(argv=None) -> int:
     if o.cmd == "multiply" and not o.out:
         print("error: --out is required", file=sys.stderr)
         return EXIT_USAGE
-    if o.cmd in ("ple", "echelonize", "multiply") and o.k != "auto":
+    if o.cmd in ("ple", "echelonize", "multiply", "bench") and o.k != "auto":
         try:
             if not 1 <= int(o.k) <= 20:  # KValidator, gf2tool.cpp:51-66
                 raise ValueError
@@ -209,7 +344,7 @@ def main(argv=None) -> int:
             return EXIT_USAGE
     try:
         return {"gen": run_gen, "ple": run_ple, "echelonize": run_echelonize,
-                "multiply": run_multiply}[o.cmd](o)
+                "multiply": run_multiply, "bench": run_bench}[o.cmd](o)
     except VerifyError as e:
         print(f"verification failed: {e}", file=sys.stderr)
         return EXIT_VERIFY

@@ -48,3 +48,40 @@ def test_multiply(tmp_path):
     assert np.array_equal(gio.load_gf2b(c_path).words, O.mul(a, 200, b, 250))
     assert tool.main(["multiply", a_path, b_path, "--out", c_path, "--verify", "--inject-fault"]) == 3
     assert tool.main(["multiply", a_path, a_path, "--out", c_path]) == 1  # dimension mismatch
+
+
+def _csv(text):
+    return [line.split(",") for line in text.strip().splitlines()]
+
+
+def test_bench_suites_emit_the_reference_csv(tmp_path, capsys):
+    """gf2tool bench (gf2tool.cpp:260-423), as the reference's own CLI tests
+    drive it (test_io_cli.cpp:330-374): the 11-column CSV, one row per cell,
+    medians on stderr; --device-metrics appends the device columns."""
+    csv = str(tmp_path / "bench.csv")
+    assert tool.main(["bench", "--suite", "table2", "--sizes", "64", "--seeds", "1", "2", "3",
+                      "--out", csv]) == 0
+    rows = _csv(open(csv).read())
+    assert rows[0] == tool.BENCH_COLUMNS
+    assert all(len(r) == 11 and r[1] == "64" and float(r[8]) > 0 and int(r[10]) <= 64 for r in rows[1:])
+    assert sum(r[0] == "m4ri" for r in rows) == 3 and sum(r[0] == "ple-recursive" for r in rows) == 3
+    capsys.readouterr()
+    assert tool.main(["bench", "--suite", "table1", "--sizes", "48", "--seeds", "1"]) == 0
+    out = capsys.readouterr()
+    rows = _csv(out.out)
+    assert len(rows) == 3 and rows[1][0] == "ple-recursive-striped-base"
+    assert rows[2][0] == "ple-recursive-cubic-base" and "median algorithm=" in out.err
+    assert tool.main(["bench", "--suite", "fig3", "--sizes", "48", "--seeds", "1"]) == 0
+    rows = _csv(capsys.readouterr().out)
+    assert sum(r[3].startswith("nnz:") for r in rows[1:]) == 40
+    assert sum(r[3] == "uniform:0.5" for r in rows[1:]) == 1
+    # ranks agree with the oracle
+    a = O.fill_random(1024, 1024, 0.5, 3)
+    want = O.echelonize(a.copy(), 1024, 1024, False)
+    assert tool.main(["bench", "--suite", "table1", "--sizes", "1024", "--seeds", "3",
+                      "--device-metrics"]) == 0
+    rows = _csv(capsys.readouterr().out)
+    assert rows[0] == tool.BENCH_COLUMNS + tool.DEVICE_COLUMNS
+    for r in rows[1:]:
+        assert int(r[10]) == want and int(r[11]) == 1 and int(r[12]) == 64
+        assert float(r[13]) > 0 and float(r[15]) > 0 and 0 < float(r[16]) < 1.5
