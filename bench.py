@@ -90,7 +90,10 @@ def load_traffic(driver: int = 2):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+    nvidia-smi can take a second to start on a fresh box, so it is started
+    (and its first sample awaited) before the timed region; begin()/stop()
+    bracket the region and only the samples taken inside it are kept."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -99,7 +102,8 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (monotonic time, line)
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -109,24 +113,34 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.monotonic() + 10.0
+            while not self.lines and time.monotonic() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
+    def begin(self):
+        self.t0 = time.monotonic()
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
     def stop(self):
+        self.t1 = time.monotonic()
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)  # the sample that covers the region's end
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [ln for (ts, ln) in self.lines if t0 <= ts <= self.t1 + 0.03]
         sms, maxs, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in inside:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -140,7 +154,8 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sms) if sms else None,
                 "sm_max_mhz": max(maxs) if maxs else None,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "reasons": sorted(reasons), "samples": len(sms),
+                "window_s": round(self.t1 - t0, 3)}
 
 
 def make_host_ctr(m, n, seed):
@@ -278,6 +293,8 @@ def gpu_arm(args, rank, world, local_rank):
     cfg = G.PleConfig(device=dev, stream=sptr)
     cfg_t = G.PleConfig(device=dev, stream=sptr, time_kernels=True)
 
+    clocks = ClockSampler(dev)
+    clocks.start()
     # warm-up (also yields the rank / checksum for the parity handle)
     for _ in range(args.warmup):
         work.copy_from(pristine, stream=sptr)
@@ -285,9 +302,8 @@ def gpu_arm(args, rank, world, local_rank):
     checksum = work.checksum(stream=sptr) if args.warmup else None
 
     # ---- timed region: K steps, device-resident inputs ----
-    clocks = ClockSampler(dev)
     barrier()
-    clocks.start()
+    clocks.begin()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -520,6 +536,7 @@ def gpu_sharded_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
+    clocks.begin()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with eng.stream_ctx():
@@ -624,6 +641,7 @@ def gpu_peer_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
+    clocks.begin()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
