@@ -94,6 +94,17 @@ FULL = [
     ("c4_32768_xy", 32768, 32768, "xy", 24576, (11, 12)),
     ("c5_65536_ctr", 65536, 65536, "ctr", None, 1),
     ("c5_131072_ctr", 131072, 131072, "ctr", None, 1),
+    # the sizes around the driver switch (tests/test_ple_gpu.py
+    # test_default_driver_size_rule: ctr seed 9) and the streamed-output
+    # cases (ctr seed 3 with rows m/3 .. m/3+200 copied from rows 10..210)
+    ("m_8192x65536_ctr9", 8192, 65536, "ctr", None, 9),
+    ("m_20480_ctr9", 20480, 20480, "ctr", None, 9),
+    ("m_16384x24576_ctr9", 16384, 24576, "ctr", None, 9),
+    ("m_16384_ctr9", 16384, 16384, "ctr", None, 9),
+    ("m_12288_ctr9", 12288, 12288, "ctr", None, 9),
+    ("s_16384_dup3", 16384, 16384, "ctr_dup", None, 3),
+    ("s_12000x20000_dup3", 12000, 20000, "ctr_dup", None, 3),
+    ("s_20000x9000_dup3", 20000, 9000, "ctr_dup", None, 3),
 ]
 
 
@@ -102,6 +113,10 @@ def full_input(gen, m, n, param, seed):
         return O.fill_random(m, n, param, seed)
     if gen == "ctr":
         return O.fill_ctr(m, n, seed)
+    if gen == "ctr_dup":
+        a = O.fill_ctr(m, n, seed)
+        a[m // 3: m // 3 + 200] = a[10:210]
+        return a
     if gen == "xy":
         l = param
         x = O.fill_ctr(m, l, seed[0])

@@ -72,7 +72,8 @@ def full_input(cfg):
 
 
 @pytest.mark.parametrize("name", ["c1_4096_dense", "c2_16384_dense", "c2_16384x65536_dense",
-                                  "c3_32768_p64", "c3_32768_p256", "c4_32768_xy", "c5_65536_ctr"])
+                                  "c3_32768_p64", "c3_32768_p256", "c4_32768_xy", "c5_65536_ctr",
+                                  "c5_131072_ctr"])
 def test_full_config_bit_exact(name):
     cfgs = {c["name"]: c for c in load("full_configs.json")["configs"]}
     if name not in cfgs:
@@ -90,7 +91,8 @@ def test_full_config_bit_exact(name):
 
 
 @pytest.mark.parametrize("name,ranks", [("c2_16384x65536_dense", 4), ("c3_32768_p256", 4),
-                                        ("c3_32768_p64", 2), ("c4_32768_xy", 3), ("c5_65536_ctr", 8)])
+                                        ("c3_32768_p64", 2), ("c4_32768_xy", 3), ("c5_65536_ctr", 8),
+                                        ("c5_131072_ctr", 8)])
 def test_full_config_peer_ranks(name, ranks):
     """The row-sharded peer-memory driver (ple_peer.cuh) with `ranks` ranks
     emulated on the one GPU, bit-exact on full-size BASELINE configs: sparse

@@ -215,11 +215,23 @@ def test_131072_reconstruction_sample():
         assert np.array_equal(prod, ctr_rows([idx[i]], n, 1)[0]), f"position {i}"
 
 
-@pytest.mark.parametrize("m,n", [(16384, 16384), (12000, 20000), (20000, 9000)])
-def test_streamed_output_matches_device(m, n):
+def golden(name):
+    """A full-size entry of tests/golden/full_configs.json (the compiled
+    reference's rank and outcome hash), or None."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "full_configs.json")
+    with open(p) as f:
+        return {c["name"]: c for c in json.load(f)["configs"]}.get(name)
+
+
+@pytest.mark.parametrize("m,n,name", [(16384, 16384, "s_16384_dup3"), (12000, 20000, "s_12000x20000_dup3"),
+                                      (20000, 9000, "s_20000x9000_dup3")])
+def test_streamed_output_matches_device(m, n, name):
     """gf2cu_ple on an aligned host view with the super-step driver copies the
     rows the kernel finishes to the host while it runs (chunks of >= m/32
-    rows); the host result must equal the device-resident run's."""
+    rows); the host result must equal the device-resident run's, and both the
+    compiled reference's (golden outcome hash)."""
     a = O.fill_ctr(m, n, 3)
     a[m // 3: m // 3 + 200] = a[10:210]  # some rank deficiency
     bm = G.BitMatrix(m, n, a.copy())
@@ -230,15 +242,20 @@ def test_streamed_output_matches_device(m, n):
     assert got.rank == want.rank
     assert np.array_equal(got.q, want.q) and np.array_equal(got.p.swaps, want.p.swaps)
     assert np.array_equal(bm.words, d.download())
+    g = golden(name)
+    assert g is not None, f"{name} missing from tests/golden/full_configs.json"
+    assert got.rank == g["rank"]
+    assert S.outcome_hash(bm.words, n, got.rank, got.p.swaps, got.q) == g["sha256"]
 
 
-@pytest.mark.parametrize("m,n,driver", [(8192, 65536, 2), (20480, 20480, 2), (16384, 24576, 2),
-                                        (16384, 16384, 1), (12288, 12288, 1)])
-def test_default_driver_size_rule(m, n, driver):
+@pytest.mark.parametrize("m,n,driver,name", [(8192, 65536, 2, "m_8192x65536_ctr9"), (20480, 20480, 2, "m_20480_ctr9"),
+                                             (16384, 24576, 2, "m_16384x24576_ctr9"),
+                                             (16384, 16384, 1, "m_16384_ctr9"), (12288, 12288, 1, "m_12288_ctr9")])
+def test_default_driver_size_rule(m, n, driver, name):
     """Without a driver flag the super-step driver runs from 5 * 2^20 matrix words
     (m * ceil(n/64)) up, the single-panel persistent driver below (the measured
-    crossover); both give the device-resident ctr result
-    the other driver gives."""
+    crossover); both drivers give the compiled
+    reference's result (golden outcome hash of the ctr(seed 9) matrix)."""
     d = G.DeviceMatrix(m, n)
     d.fill_ctr(9)
     e = G.DeviceMatrix(m, n)
@@ -248,6 +265,10 @@ def test_default_driver_size_rule(m, n, driver):
     other = G.block_iterative_ple(e, G.PleConfig(single_panel=True) if driver == 2 else G.PleConfig(super_step=True))
     assert other.rank == got.rank and np.array_equal(other.q, got.q)
     assert d.checksum() == e.checksum()
+    g = golden(name)
+    assert g is not None, f"{name} missing from tests/golden/full_configs.json"
+    assert got.rank == g["rank"]
+    assert S.outcome_hash(d.download(), n, got.rank, got.p.swaps, got.q) == g["sha256"]
 
 
 @pytest.mark.parametrize("m,n,gen", [(3000, 3000, "dense"), (2500, 2500, "dup"), (1500, 4000, "ctr"),
@@ -255,7 +276,8 @@ def test_default_driver_size_rule(m, n, driver):
 def test_panel_tuning_bits_exact(m, n, gen, monkeypatch):
     """The panel tuning bits (GF2CU_PANEL_FLAGS: 1 = followers apply the
     leader's pivots as published, 2 = the super-step look-ahead across
-    super-steps) change the schedule, never the result: every combination is
+    super-steps, 4 = the transposed leader epochs) change the schedule, never
+    the result: every combination is
     bit-exact against the oracle on both persistent drivers."""
     if gen == "dense":
         a = O.fill_random(m, n, 0.5, 21)
@@ -268,7 +290,7 @@ def test_panel_tuning_bits_exact(m, n, gen, monkeypatch):
         a[100:900] = a[1000:1800]  # pivotless columns, window misses
     ref = a.copy()
     want = O.ple(ref, m, n)
-    for flags in ("0", "1", "2", "3"):
+    for flags in ("0", "1", "2", "3", "4", "5", "6", "7"):
         monkeypatch.setenv("GF2CU_PANEL_FLAGS", flags)
         for cfg in (G.PleConfig(super_step=True), G.PleConfig(single_panel=True)):
             bm = G.BitMatrix(m, n, a.copy())
