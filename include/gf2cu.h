@@ -31,7 +31,8 @@ typedef enum {
     GF2CU_ERANGE = 2,    /* view/window outside matrix: std::out_of_range         */
     GF2CU_ENOMEM = 3,    /* device or host allocation failed: std::bad_alloc      */
     GF2CU_ECUDA = 4,     /* CUDA runtime error (no device, launch failure, ...)   */
-    GF2CU_ENODEVICE = 5  /* no sm_100 device visible                              */
+    GF2CU_ENODEVICE = 5, /* no sm_100 device visible                              */
+    GF2CU_ECHECK = 6     /* GF2CU_FLAG_CHECK: a device invariant was violated     */
 } gf2cu_status;
 
 /* Mirrors gf2::MatrixView (bit_matrix.hpp:223-227, 245-250): row-major uint64
@@ -67,6 +68,14 @@ typedef struct {
 #define GF2CU_FLAG_SUPER_STEP 8u   /* force the super-step kernel: two panels
                                       per sweep (default: chosen by size --
                                       super-step from 5*2^20 matrix words)     */
+#define GF2CU_FLAG_CHECK 32u       /* check mode (also: environment variable
+                                      GF2CU_CHECK=1): every step asserts
+                                      SURVEY 8(c) invariant (iv) on every row's
+                                      panel word, the result invariants (i),
+                                      (ii); a violation returns GF2CU_ECHECK
+                                      naming the first violating step. Single-
+                                      device drivers (emulated peer ranks
+                                      included); slower.                      */
 
 /* The device-driven row-sharded driver (ple_peer.cuh)
  * with g = 1..8 ranks emulated on the one device: one cooperative launch,
@@ -115,10 +124,11 @@ gf2cu_status gf2cu_ple(const gf2cu_view* a, const gf2cu_cfg* cfg, size_t* swaps,
 
 /* Replaces gf2::partial_ple(MatrixView a) (ple.hpp:57-130), the lazy
  * single-pass PLE, in place on a HOST view. rank, q, swaps and col_swaps are
- * the reference's; *processed = its watermark (rows [processed, nrows) are
- * left untouched, which happens only when every column finds a pivot and
- * rank == ncols < nrows; otherwise processed = nrows and the in-place result
- * equals gf2cu_ple's; rank 0 gives processed 0). Capacities as gf2cu_ple. */
+ * the reference's; *processed = its watermark: rows [processed, nrows) are
+ * left untouched, which happens only when rank < nrows and the pivot columns
+ * run consecutively from q[0] to column ncols-1 (no pivotless column after
+ * the first pivot); otherwise processed = nrows and the in-place result
+ * equals gf2cu_ple's; rank 0 gives processed 0. Capacities as gf2cu_ple. */
 gf2cu_status gf2cu_partial_ple(const gf2cu_view* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
                                size_t* rank, size_t* processed, gf2cu_colswap* col_swaps,
                                size_t* n_col_swaps);
@@ -348,6 +358,21 @@ gf2cu_status gf2cu_fill_random(uint64_t* words, size_t m, size_t n, size_t strid
 gf2cu_status gf2cu_fill_random_rows(uint64_t* words, size_t m, size_t n, size_t stride, size_t nnz,
                                     uint64_t seed);
 gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, uint64_t seed);
+
+/* ------------------------------------------------------------------ */
+/* Diagnostics                                                          */
+/* ------------------------------------------------------------------ */
+/* Message-passing litmus runs of the persistent drivers' cross-CTA
+ * hand-offs, built from the same primitives (csrc/litmus.cuh): kind 0 = CTA
+ * arrival (bar.sync + red.release.gpu) -> ld.acquire.gpu spin -> ldcg reads
+ * (pre-work -> panel capture); 1 = the same awaited with the two-counter spin
+ * (t_count + chunk count -> table sources); 2 = system scope (the peer
+ * drivers' fence.sc.sys + red.release.sys -> ld.acquire.sys); 3 = streamed
+ * output to the host (threadfence + last arrival's threadfence_system +
+ * mapped-memory flag -> host poll -> async copy). `rounds` rounds on every
+ * SM; *checked = payload words verified, *failures = stale or torn words. */
+gf2cu_status gf2cu_litmus(int kind, unsigned rounds, int device, unsigned long long* checked,
+                          unsigned long long* failures);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ from .ple import (  # noqa: F401
     mul,
     mul_into,
     partial_ple,
+    litmus,
     undo_column_swaps,
     recursive_ple,
     echelonize,
@@ -40,5 +41,5 @@ __all__ = [
     "RowPermutation", "block_iterative_ple", "device_count", "fill_ctr", "fill_random",
     "host_checksum", "words_per_row", "build", "load", "echelonize", "extract_e", "extract_l",
     "rref_from_ple", "trsm_upper_left_unit", "fill_random_rows", "addmul", "mul", "mul_into", "recursive_ple",
-    "echelonize_strategy", "partial_ple", "undo_column_swaps",
+    "echelonize_strategy", "partial_ple", "undo_column_swaps", "litmus",
 ]

@@ -84,6 +84,7 @@ FLAG_TIME_KERNELS = 1
 FLAG_MULTI_KERNEL = 2
 FLAG_SINGLE_PANEL = 4
 FLAG_SUPER_STEP = 8
+FLAG_CHECK = 32
 PEER_HANDLE_BYTES = 64  # GF2CU_PEER_HANDLE_BYTES
 
 
@@ -156,6 +157,8 @@ SYMBOLS = {
     "gf2cu_peer_ping": (C.c_int, [_mp, C.c_uint32, C.POINTER(C.c_uint32)]),
     "gf2cu_peer_run": (C.c_int, [_mp, C.c_void_p, C.POINTER(gf2cu_stats)]),
     "gf2cu_peer_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),
+    "gf2cu_litmus": (C.c_int, [C.c_int, C.c_uint, C.c_int, C.POINTER(C.c_ulonglong),
+                               C.POINTER(C.c_ulonglong)]),
     "gf2cu_fill_random": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_double, C.c_uint64]),
     "gf2cu_fill_ctr": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_uint64]),
     "gf2cu_fill_random_rows": (C.c_int, [_u64p, _sz, _sz, _sz, _sz, C.c_uint64]),
@@ -186,6 +189,10 @@ class Gf2cuError(RuntimeError):
     pass
 
 
+class Gf2cuCheckError(Gf2cuError):
+    """GF2CU_ECHECK: check mode found a violated device invariant."""
+
+
 def check(status: int) -> None:
     """Map a gf2cu_status to the exception the reference would raise."""
     if status == 0:
@@ -197,4 +204,6 @@ def check(status: int) -> None:
         raise IndexError(msg)          # std::out_of_range
     if status == 3:
         raise MemoryError(msg)         # std::bad_alloc
+    if status == 6:
+        raise Gf2cuCheckError(msg)
     raise Gf2cuError(f"gf2cu status {status}: {msg}")

@@ -27,6 +27,7 @@
 #include "ple_peer_super.cuh"
 #include "rref_kernels.cuh"
 #include "gemm_kernels.cuh"
+#include "litmus.cuh"
 
 using gf2cu::u32;
 using gf2cu::u64;
@@ -97,6 +98,7 @@ struct Workspace {
     u32* h_out = nullptr;        // pinned host staging of swaps / q (2 x min(m, n))
     gf2cu::PanelOut* pout_b = nullptr;  // super-step driver: panel b's outputs
     gf2cu::SuperOut* sout = nullptr;
+    u32* check = nullptr;        // check mode: Params::check words
     std::vector<cudaEvent_t> ev;
 };
 
@@ -120,6 +122,7 @@ void free_ws(Workspace& w) {
     cudaFreeHost(w.h_out);
     cudaFree(w.pout_b);
     cudaFree(w.sout);
+    cudaFree(w.check);
     if (w.host_r) cudaFreeHost(w.host_r);
     if (w.out_host) cudaFreeHost(w.out_host);
     if (w.copy) cudaStreamDestroy(w.copy);
@@ -282,8 +285,31 @@ gf2cu_status alloc_ws(gf2cu_matrix* a) {
     CU_TRY(cudaHostAlloc(&w.out_host, sizeof(u32), cudaHostAllocMapped));
     CU_TRY(cudaHostGetDevicePointer(&w.out_host_dev, w.out_host, 0));
     CU_TRY(cudaStreamCreateWithFlags(&w.copy, cudaStreamNonBlocking));
+    CU_TRY(cudaMalloc(&w.check, 4 * sizeof(u32)));
     return GF2CU_OK;
 }
+
+// Check mode (GF2CU_FLAG_CHECK or GF2CU_CHECK=1 in the environment).
+bool check_mode(const gf2cu_cfg* cfg) {
+    if (cfg && (cfg->flags & GF2CU_FLAG_CHECK)) return true;
+    const char* e = std::getenv("GF2CU_CHECK");
+    return e && e[0] && std::strcmp(e, "0") != 0;
+}
+
+u32 check_inject_env() {
+    const char* e = std::getenv("GF2CU_CHECK_INJECT");  // test hook: step + 1 to corrupt
+    return e ? (u32)std::strtoul(e, nullptr, 0) : 0u;
+}
+
+gf2cu_status check_reset(u32* chk, cudaStream_t s) {
+    static const u32 init[4] = {0xffffffffu, 0u, 0xffffffffu, 0u};
+    CU_TRY(cudaMemcpyAsync(chk, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    return GF2CU_OK;
+}
+
+// After the factorization: the result invariants on the row-major matrix,
+// then the verdict of both checks.
+gf2cu_status check_verdict(gf2cu_matrix* a, u32* chk, size_t rank, int sms, cudaStream_t s);
 
 // PleConfig never makes the reference throw: pick_table_bits clamps any
 // k_scale (<= 0, tiny, huge) to k in [1, 16] (gray_code.hpp:171-177) and the
@@ -521,8 +547,20 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
     }
     const bool super = peer_super(m, W, cfg ? cfg->flags : 0u);
     const u32 wpad = super ? (u32)std::max<size_t>(4, (W + 3) / 4 * 4) : (u32)wpad8(W);
-    if (pw.hp[0].p.Wpad8 != wpad) {
-        for (unsigned k = 0; k < G; ++k) pw.hp[k].p.Wpad8 = wpad;
+    const bool checking = check_mode(cfg);
+    u32* chk = nullptr;
+    if (checking) {
+        gf2cu_status cst = ensure_ws(a);
+        if (cst != GF2CU_OK) return cst;
+        chk = a->ws.check;
+        cst = check_reset(chk, s);
+        if (cst != GF2CU_OK) return cst;
+    }
+    if (pw.hp[0].p.Wpad8 != wpad || pw.hp[0].p.check != chk) {
+        for (unsigned k = 0; k < G; ++k) {
+            pw.hp[k].p.Wpad8 = wpad;
+            pw.hp[k].p.check = chk;
+        }
         CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
     }
     for (unsigned k = 0; k < G; ++k) {
@@ -555,6 +593,7 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
         if (c[gf2cu::kCtrErr]) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
     }
     st = peer_outputs(pw.hp[0], super, s, swaps, q, rank, col_swaps, n_col_swaps, nullptr, stats);
+    if (st == GF2CU_OK && checking) st = check_verdict(a, chk, *rank, sms, s);
     if (st == GF2CU_OK && stats && timing) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[0], ev[1]);
@@ -623,6 +662,13 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     p.W = (u32)W;
     p.Wpad8 = (u32)wpad8(W);
     p.pflags = panel_flags();
+    const bool checking = check_mode(cfg);
+    if (checking) {
+        p.check = ws.check;
+        p.check_inject = check_inject_env();
+        st = check_reset(ws.check, pick_stream(a, cfg ? cfg->stream : nullptr));
+        if (st != GF2CU_OK) return st;
+    }
 
     static bool attr_set[64] = {false};
     if (a->device >= 0 && a->device < 64 && !attr_set[a->device]) {
@@ -849,6 +895,10 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     if (rows_streamed) *rows_streamed = sent;
 
     CU_TRY(cudaStreamSynchronize(s));
+    if (checking) {
+        st = check_verdict(a, ws.check, rk, sms, s);
+        if (st != GF2CU_OK) return st;
+    }
     *rank = rk;
     size_t ncs = 0;
     for (size_t i = 0; i < rk; ++i) {
@@ -934,6 +984,27 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             stats->coef_ms = tc;
             stats->trailing_ms = tt;
         }
+    }
+    return GF2CU_OK;
+}
+
+gf2cu_status check_verdict(gf2cu_matrix* a, u32* chk, size_t rank, int sms, cudaStream_t s) {
+    gf2cu::check_final_kernel<<<sms * 4, 256, 0, s>>>(a->data, (u32)a->m, (u32)a->n, (u32)a->Wp, (u32)rank, chk);
+    CU_TRY(cudaGetLastError());
+    u32 h[4];
+    CU_TRY(cudaMemcpyAsync(h, chk, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CU_TRY(cudaStreamSynchronize(s));
+    if (h[1]) {
+        char msg[160];
+        std::snprintf(msg, sizeof(msg), "check mode: invariant (iv) violated at step %u (%u panel words)",
+                      h[0], h[1]);
+        return fail(GF2CU_ECHECK, msg);
+    }
+    if (h[3]) {
+        char msg[160];
+        std::snprintf(msg, sizeof(msg), "check mode: invariant (i)/(ii) violated at row %u (%u rows)", h[2],
+                      h[3]);
+        return fail(GF2CU_ECHECK, msg);
     }
     return GF2CU_OK;
 }
@@ -1441,16 +1512,21 @@ gf2cu_status gf2cu_ple_device(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swa
 // partial_ple (ple.hpp:57-130). Its pivot search reads every row of a column
 // before giving up on it, so it finds the same pivots as the complete
 // decomposition (rank, q, p.swaps equal), and every row it reads ends fully
-// updated. Only its laziness differs: when every column 0..n-1 finds a pivot
-// (rank == n < m; q is then the identity and no compression swap exists), the
-// rows past the deepest pivot row were never read and stay untouched, and
-// processed = max(rank, max swaps + 1) (the watermark s[0] + 1, :128). In
-// every other case a pivotless column (or r reaching m) made the scan read
-// all rows: processed = m, and the in-place result is the complete PLE's.
-// rank 0 leaves processed = 0 (:113-116) and the matrix unchanged.
-static size_t partial_processed(size_t m, size_t n, size_t rank, const size_t* swaps) {
+// updated. Only its laziness differs: the watermark s[0] (:69-87, :128)
+// records the rows read once a first pivot exists. A pivotless column after
+// the first pivot column -- between pivots or after the last one (the final
+// scan, :60-97) -- reads every row, so processed = m and the in-place result
+// is the complete PLE's. Otherwise (pivot columns consecutive from q[0] up to
+// column n-1; empty columns before q[0] are read while r = 0 and do not move
+// the watermark) the deepest row read is the deepest pivot row, the rows past
+// it were never read and stay untouched, and processed = max(rank, max swaps
+// + 1). r = m also gives m; rank 0 gives processed 0 (:113-116).
+static gf2cu_status run_undo_col_swaps(gf2cu_matrix* a, const gf2cu_colswap* cs, size_t ncs, cudaStream_t s,
+                                       bool forward, size_t row_lo);
+
+static size_t partial_processed(size_t m, size_t n, size_t rank, const size_t* swaps, const size_t* q) {
     if (rank == 0) return 0;
-    if (!(rank == n && n < m)) return m;
+    if (rank >= m || q[rank - 1] != n - 1 || q[rank - 1] - q[0] != rank - 1) return m;
     size_t smax = 0;
     for (size_t l = 0; l < rank; ++l) smax = std::max(smax, swaps[l]);
     return std::max(rank, smax + 1);
@@ -1473,20 +1549,43 @@ gf2cu_status gf2cu_partial_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t
         return GF2CU_OK;
     }
     size_t limit = m;
-    st = with_view(
-        v, cfg, nullptr,
-        [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
-            gf2cu_status s2 = run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, nullptr);
-            if (s2 == GF2CU_OK) limit = partial_processed(m, n, *rank, swaps);
-            return s2;
-        },
-        nullptr, &limit);
+    std::vector<gf2cu_colswap> cs(std::max<size_t>(1, std::min(m, n)));
+    st = with_view(v, cfg, nullptr, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
+        size_t ncs = 0;
+        gf2cu_status s2 = run_ple(a, &c, swaps, q, rank, cs.data(), &ncs, nullptr);
+        if (s2 != GF2CU_OK) return s2;
+        limit = partial_processed(m, n, *rank, swaps, q);
+        if (col_swaps) std::copy(cs.begin(), cs.begin() + ncs, col_swaps);
+        if (n_col_swaps) *n_col_swaps = ncs;
+        if (limit < m) {
+            // rows [limit, m) were never read: back to the input (the host view
+            // still holds it), then only the compression swaps (ple.hpp:122-126)
+            cudaStream_t s = reinterpret_cast<cudaStream_t>(c.stream);
+            gf2cu_view tail = *v;
+            tail.data = v->data + limit * v->stride;
+            tail.nrows = m - limit;
+            gf2cu_matrix shifted;
+            shifted.m = m - limit;
+            shifted.n = a->n;
+            shifted.W = a->W;
+            shifted.Wp = a->Wp;
+            shifted.device = a->device;
+            shifted.data = a->data + limit * a->Wp;
+            std::vector<u64> packed;
+            s2 = view_upload(&tail, &shifted, s, packed);
+            shifted.data = nullptr;  // (not owned)
+            if (s2 == GF2CU_OK) s2 = run_undo_col_swaps(a, cs.data(), ncs, s, true, limit);
+            if (s2 == GF2CU_OK) CU_TRY(cudaStreamSynchronize(s));  // (packed outlives the upload)
+        }
+        return s2;
+    });
     if (st == GF2CU_OK) *processed = limit;
     return st;
 }
 
-static gf2cu_status run_undo_col_swaps(gf2cu_matrix* a, const gf2cu_colswap* cs, size_t ncs, cudaStream_t s) {
-    if (ncs == 0 || a->m == 0) return GF2CU_OK;
+static gf2cu_status run_undo_col_swaps(gf2cu_matrix* a, const gf2cu_colswap* cs, size_t ncs, cudaStream_t s,
+                                       bool forward, size_t row_lo) {
+    if (ncs == 0 || a->m <= row_lo) return GF2CU_OK;
     std::vector<ulonglong2> h(ncs);  // {a | b << 32, from_row}
     for (size_t i = 0; i < ncs; ++i) h[i] = make_ulonglong2((u64)cs[i].a | ((u64)cs[i].b << 32), cs[i].from_row);
     ulonglong2* d = nullptr;
@@ -1494,7 +1593,8 @@ static gf2cu_status run_undo_col_swaps(gf2cu_matrix* a, const gf2cu_colswap* cs,
     cudaError_t e = cudaMemcpyAsync(d, h.data(), ncs * sizeof(ulonglong2), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) {
         const unsigned blocks = (unsigned)std::min<size_t>((a->m + 255) / 256, 65535u * 16);
-        gf2cu::undo_col_swaps_kernel<<<blocks, 256, 0, s>>>(a->data, (u32)a->m, (u32)a->Wp, d, (u32)ncs);
+        gf2cu::undo_col_swaps_kernel<<<blocks, 256, 0, s>>>(a->data, (u32)a->m, (u32)a->Wp, d, (u32)ncs,
+                                                            forward ? 1 : 0, (u32)row_lo);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // (h outlives the copy)
@@ -1516,7 +1616,7 @@ gf2cu_status gf2cu_undo_column_swaps_device(gf2cu_matrix* a, const gf2cu_colswap
     gf2cu_status st = check_col_swaps(a->m, a->n, col_swaps, n_col_swaps);
     if (st != GF2CU_OK) return st;
     DeviceGuard g(a->device);
-    return run_undo_col_swaps(a, col_swaps, n_col_swaps, pick_stream(a, stream));
+    return run_undo_col_swaps(a, col_swaps, n_col_swaps, pick_stream(a, stream), false, 0);
 }
 
 gf2cu_status gf2cu_undo_column_swaps(const gf2cu_view* v, const gf2cu_colswap* col_swaps,
@@ -1526,7 +1626,7 @@ gf2cu_status gf2cu_undo_column_swaps(const gf2cu_view* v, const gf2cu_colswap* c
     st = check_col_swaps(v->nrows, v->ncols, col_swaps, n_col_swaps);
     if (st != GF2CU_OK || n_col_swaps == 0 || v->nrows == 0 || v->ncols == 0) return st;
     return with_view(v, cfg, nullptr, [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
-        return run_undo_col_swaps(a, col_swaps, n_col_swaps, reinterpret_cast<cudaStream_t>(c.stream));
+        return run_undo_col_swaps(a, col_swaps, n_col_swaps, reinterpret_cast<cudaStream_t>(c.stream), false, 0);
     });
 }
 
@@ -2404,6 +2504,120 @@ gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, 
         }
         if (W) row[W - 1] &= last;
     }
+    return GF2CU_OK;
+}
+
+// Message-passing litmus runs of the drivers' hand-offs (litmus.cuh).
+gf2cu_status gf2cu_litmus(int kind, unsigned rounds, int device, unsigned long long* checked,
+                          unsigned long long* failures) {
+    if (!checked || !failures || kind < 0 || kind > 3) return fail(GF2CU_EINVAL, "bad litmus arguments");
+    *checked = *failures = 0;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(GF2CU_ENODEVICE, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(GF2CU_EINVAL, "bad device ordinal");
+    DeviceGuard g(device);
+    apply_watchdog_env(device);
+    const int sms = num_sms(device);
+    gf2cu::LitmusParams L{};
+    L.rounds = rounds;
+    L.kind = (u32)kind;
+    std::vector<void*> allocs;
+    auto alloc = [&](void** ptr, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(ptr, bytes);
+        if (e == cudaSuccess) {
+            allocs.push_back(*ptr);
+            e = cudaMemset(*ptr, 0, bytes);
+        }
+        return e;
+    };
+    auto cleanup = [&]() {
+        for (void* x : allocs) cudaFree(x);
+    };
+    cudaError_t e = cudaSuccess;
+    const u32 G = kind == 3 ? (u32)sms * 2u : (u32)sms;
+    if (kind == 3) {
+        e = alloc((void**)&L.out, (size_t)rounds * G * gf2cu::kLitmusWords * 8);
+    } else {
+        e = alloc((void**)&L.data, (size_t)2 * G * gf2cu::kLitmusWords * 8);
+        if (e == cudaSuccess) e = alloc((void**)&L.ctr, (size_t)rounds * 4 + 4);
+        if (e == cudaSuccess) e = alloc((void**)&L.ctr2, (size_t)rounds * 4 + 4);
+        if (e == cudaSuccess) e = alloc((void**)&L.done, (size_t)rounds * 4 + 4);
+    }
+    if (e == cudaSuccess) e = alloc((void**)&L.err, 4);
+    if (e == cudaSuccess) e = alloc((void**)&L.checked, 8);
+    if (e == cudaSuccess) e = alloc((void**)&L.failures, 8);
+    if (e == cudaSuccess) e = alloc((void**)&L.out_count, 4);
+    if (e != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "litmus allocation");
+    }
+    unsigned long long h_checked = 0, h_fail = 0;
+    if (kind < 3) {
+        void* args[] = {&L};
+        e = cudaLaunchCooperativeKernel((void*)gf2cu::litmus_kernel, dim3(G), dim3(512), args, 0, nullptr);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        u32 err = 0;
+        if (e == cudaSuccess) e = cudaMemcpy(&err, L.err, 4, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(&h_checked, L.checked, 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(&h_fail, L.failures, 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && err) {
+            cleanup();
+            return fail(GF2CU_ECUDA, "litmus watchdog tripped");
+        }
+    } else {
+        // the host side of the streamed output: poll the mapped word, copy
+        // each published round on a second stream, compare
+        u32* flag = nullptr;
+        u32* flag_dev = nullptr;
+        cudaStream_t ks = nullptr, cs = nullptr;
+        e = cudaHostAlloc(&flag, 4, cudaHostAllocMapped);
+        if (e == cudaSuccess) {
+            *reinterpret_cast<volatile u32*>(flag) = 0;
+            e = cudaHostGetDevicePointer(&flag_dev, flag, 0);
+        }
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        std::vector<u64> host((size_t)G * gf2cu::kLitmusWords);
+        if (e == cudaSuccess) {
+            L.host_flag = flag_dev;
+            gf2cu::litmus_host_kernel<<<G, 256, 0, ks>>>(L);
+            e = cudaGetLastError();
+        }
+        u32 seen = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        while (e == cudaSuccess && seen < rounds) {
+            const u32 avail = *reinterpret_cast<volatile u32*>(flag);
+            for (; seen < avail; ++seen) {
+                e = cudaMemcpyAsync(host.data(), L.out + (size_t)seen * G * gf2cu::kLitmusWords,
+                                    host.size() * 8, cudaMemcpyDeviceToHost, cs);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+                if (e != cudaSuccess) break;
+                for (u32 c = 0; c < G; ++c)
+                    for (u32 i = 0; i < gf2cu::kLitmusWords; ++i) {
+                        const u64 x = (u64)seen << 40 ^ (u64)c << 20 ^ (u64)i ^ 0x9e3779b97f4a7c15ull;
+                        u64 z = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+                        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+                        z ^= z >> 31;
+                        h_fail += host[(size_t)c * gf2cu::kLitmusWords + i] != z;
+                    }
+                h_checked += (unsigned long long)G * gf2cu::kLitmusWords;
+            }
+            const cudaError_t q = cudaStreamQuery(ks);
+            if (q != cudaSuccess && q != cudaErrorNotReady) e = q;
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) {
+                e = cudaErrorLaunchTimeout;
+                break;
+            }
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ks);
+        if (ks) cudaStreamDestroy(ks);
+        if (cs) cudaStreamDestroy(cs);
+        if (flag) cudaFreeHost(flag);
+    }
+    cleanup();
+    if (e != cudaSuccess) return cuda_fail(e, "litmus");
+    *checked = h_checked;
+    *failures = h_fail;
     return GF2CU_OK;
 }
 

@@ -110,6 +110,10 @@ struct Params {
     volatile u32* out_host;
     // panel tuning bits (kPanel*)
     u32 pflags;
+    // GF2CU_CHECK mode (null otherwise): {first violating step, violations,
+    // first bad final row, final violations}, see check_panel_word
+    u32* check;
+    u32 check_inject;  // test hook (check mode): step + 1 whose first non-pivot row is corrupted
 };
 
 // Params::pflags: the window warps behind the leader apply its pivots as it
@@ -1180,6 +1184,53 @@ __device__ __forceinline__ void apply_load(const Params& p, ApplyShared& s, u32 
     }
 }
 
+// GF2CU_CHECK (Params::check != null): invariant (iv) of SURVEY.md 8(c),
+// "once columns [0, c] are finished with r pivots, rows >= r are zero in
+// columns [r, c]", on a row's panel word v after its forward elimination
+// against the panel's first tl pivots (columns q[0..tl)): a non-pivot row
+// (tl = rb) may hold bits only at pivot columns (its multipliers) -- every
+// other column of the panel was finished with no pivot left for it -- and a
+// pivot row (index tl) only at pivot columns left of its own pivot column,
+// plus its pivot bit. A violation means the row's word was not the current
+// one (a stale capture, a race): the first (lowest) step goes to check[0],
+// the count to check[1].
+__device__ __noinline__ void check_panel_word(u32* chk, u32 step, u64 v, u32 tl, bool pivot,
+                                              const u32* q) {
+    u64 pm = 0ull;
+    for (u32 k = 0; k < tl; ++k) pm |= 1ull << q[k];
+    u64 bad = v & ~pm;
+    if (pivot) bad = (bad & low_mask64((int)q[tl])) | (((v >> q[tl]) & 1ull) ^ 1ull);
+    if (bad) {
+        atomicMin(chk, step);
+        atomicAdd(chk + 1, 1u);
+    }
+}
+
+// Invariants (i) and (ii) of SURVEY.md 8(c) on the finished row-major L\E:
+// bit (i, i) = 1 for every i < rank; rows >= rank are zero in every column
+// >= rank. First bad row to check[2] (atomicMin), count to check[3].
+__global__ void check_final_kernel(const u64* a, u32 m, u32 n, u32 Wp, u32 rank, u32* chk) {
+    const u32 W = (n + 63u) >> 6;
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const u64* row = a + (size_t)i * Wp;
+        bool bad = false;
+        if (i < rank) {
+            bad = ((row[i >> 6] >> (i & 63u)) & 1ull) == 0ull;
+        } else {
+            const u32 w0 = rank >> 6;
+            for (u32 x = w0; x < W && !bad; ++x) {
+                u64 v = row[x];
+                if (x == w0) v &= ~low_mask64((int)(rank & 63u));
+                bad = v != 0ull;
+            }
+        }
+        if (bad) {
+            atomicMin(chk + 2, i);
+            atomicAdd(chk + 3, 1u);
+        }
+    }
+}
+
 // Positions [lo, hi) (all >= r): multipliers, combination, compressed write.
 __device__ __forceinline__ void apply_rows(const Params& p, const ApplyShared& s, u32 w, u32 r,
                                            u32 rb, u32 lo, u32 hi, u32 tid, u32 nthr) {
@@ -1200,6 +1251,10 @@ __device__ __forceinline__ void apply_rows(const Params& p, const ApplyShared& s
             c |= bit << k;
         }
         u64 epart = 0;
+        if (p.check) {
+            if (p.check_inject == w + 1u && off == rb) v ^= 1ull << 63;  // (the checker's own test)
+            check_panel_word(p.check, w, v, tl, off < rb, s.q);
+        }
         if (off < rb) {
             c |= 1ull << off;
             epart = v & ~low_mask64((int)s.q[off] + 1);

@@ -119,6 +119,7 @@ __device__ __forceinline__ void peer_apply_rows(const PeerParams& s, const Apply
             c |= bit << k;
         }
         u64 epart = 0;
+        if (s.p.check) check_panel_word(s.p.check, w, v, tl, off < rb, a.q);
         if (off < rb) {
             c |= 1ull << off;
             epart = v & ~low_mask64((int)a.q[off] + 1);

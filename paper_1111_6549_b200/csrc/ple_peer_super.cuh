@@ -57,6 +57,7 @@ __device__ __forceinline__ void peer_apply2_rows(const PeerParams& s, const Appl
             da ^= a.Da[k] & msk;
             c |= bit << k;
         }
+        if (s.p.check) check_panel_word(s.p.check, w, v, tla, off < rba, a.qa);
         if (off < rba) {
             c |= 1ull << off;
             epa = v & ~low_mask64((int)a.qa[off] + 1);
@@ -85,6 +86,7 @@ __device__ __forceinline__ void peer_apply2_rows(const PeerParams& s, const Appl
                     db ^= a.Db[k] & msk;
                     cb |= bit << k;
                 }
+                if (s.p.check) check_panel_word(s.p.check, w + 1u, v1, tlb, offb < rbb, a.qb);
                 if (offb < rbb) {
                     cb |= 1ull << offb;
                     epb = v1 & ~low_mask64((int)a.qb[offb] + 1);

@@ -189,6 +189,10 @@ __device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2&
             da ^= s.Da[k] & msk;
             c |= bit << k;
         }
+        if (p.check) {
+            if (p.check_inject == w + 1u && off == rba) v ^= 1ull << 63;  // (the checker's own test)
+            check_panel_word(p.check, w, v, tla, off < rba, s.qa);
+        }
         if (off < rba) {
             c |= 1ull << off;
             epa = v & ~low_mask64((int)s.qa[off] + 1);
@@ -218,6 +222,7 @@ __device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2&
                     db ^= s.Db[k] & msk;
                     cb |= bit << k;
                 }
+                if (p.check) check_panel_word(p.check, w + 1u, v1, tlb, offb < rbb, s.qb);
                 if (offb < rbb) {
                     cb |= 1ull << offb;
                     epb = v1 & ~low_mask64((int)s.qb[offb] + 1);

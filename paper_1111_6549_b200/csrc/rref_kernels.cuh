@@ -332,10 +332,14 @@ __global__ void rref_echelon_kernel(u64* a, const u32* q, u32 m, u32 W, u32 Wp, 
 // backwards, swap_cols_from_row(a, b, from_row) (bit_matrix.hpp:302-318) on
 // every row >= from_row. One thread per row, the swap list (<= min(m, n)
 // entries, {a | b << 32, from_row}) read through the uniform cache.
-__global__ void undo_col_swaps_kernel(u64* mat, u32 m, u32 Wp, const ulonglong2* cs, u32 ncs) {
-    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+// (forward = 1: the swaps in application order instead, rows [row_lo, m):
+// partial_ple's compression of the rows it never read, ple.hpp:122-126.)
+__global__ void undo_col_swaps_kernel(u64* mat, u32 m, u32 Wp, const ulonglong2* cs, u32 ncs,
+                                      int forward = 0, u32 row_lo = 0u) {
+    for (u32 i = row_lo + blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         u64* row = mat + (size_t)i * Wp;
-        for (u32 k = ncs; k-- > 0;) {
+        for (u32 kk = 0; kk < ncs; ++kk) {
+            const u32 k = forward ? kk : ncs - 1u - kk;
             const ulonglong2 c = __ldg(cs + k);
             if (i < c.y) continue;
             const u32 ca = (u32)c.x, cb = (u32)(c.x >> 32);

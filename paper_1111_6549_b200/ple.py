@@ -53,6 +53,7 @@ class PleConfig:
     super_step: bool = False       # force the super-step driver (two panels per sweep)
     peer_ranks: int = 0            # >0: the row-sharded peer-memory driver with this many
                                    # ranks emulated on the one device (ple_peer.cuh)
+    check: bool = False            # check mode: device invariants asserted every step
 
     def to_c(self) -> gf2cu_cfg:
         c = gf2cu_cfg()
@@ -66,6 +67,7 @@ class PleConfig:
             (_lib.FLAG_MULTI_KERNEL if self.multi_kernel else 0) | \
             (_lib.FLAG_SINGLE_PANEL if self.single_panel else 0) | \
             (_lib.FLAG_SUPER_STEP if self.super_step else 0) | \
+            (_lib.FLAG_CHECK if self.check else 0) | \
             ((int(self.peer_ranks) & 15) << 16)
         return c
 
@@ -447,6 +449,15 @@ def undo_column_swaps(a, col_swaps, cfg: Optional[PleConfig] = None) -> None:
     c = (cfg or PleConfig()).to_c()
     v = _host_view(a)._c()
     check(L.gf2cu_undo_column_swaps(C.byref(v), cp, len(arr), C.byref(c)))
+
+
+def litmus(kind: int, rounds: int = 64, device: int = 0):
+    """gf2cu_litmus: message-passing litmus run of one of the drivers'
+    cross-CTA hand-offs (0 arrival/acquire, 1 two-counter spin, 2 system
+    scope, 3 streamed output to the host). Returns (words checked, failures)."""
+    checked, failures = C.c_ulonglong(), C.c_ulonglong()
+    check(_lib.load().gf2cu_litmus(int(kind), int(rounds), int(device), C.byref(checked), C.byref(failures)))
+    return int(checked.value), int(failures.value)
 
 
 def _host_view(a) -> MatrixView:

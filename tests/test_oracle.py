@@ -121,25 +121,51 @@ def test_oracle_properties_medium():
     assert O.ref_reconstructs(a, b, m, n, oa)
 
 
-def partial_processed_rule(m, n, rank, swaps):
+def partial_processed_rule(m, n, rank, swaps, q):
     """The rule gf2cu_partial_ple applies (csrc/gf2cu.cu partial_processed):
-    processed < m only when every column finds a pivot and rank == n < m."""
+    processed < m only when rank < m and the pivot columns run consecutively
+    from q[0] to column n-1 (empty columns before q[0] do not count)."""
     if rank == 0:
         return 0
-    if not (rank == n and n < m):
+    q = [int(x) for x in q]
+    if rank >= m or q[-1] != n - 1 or q[-1] - q[0] != rank - 1:
         return m
     return max(rank, int(max(swaps)) + 1)
 
 
 def _partial_cases():
     rng = np.random.default_rng(2026)
-    for i in range(300):
+    for i in range(600):
         m, n = int(rng.integers(1, 140)), int(rng.integers(1, 140))
         if i % 3 == 0:  # tall: full column rank is likely, so the lazy pass stops early
             n = int(rng.integers(1, 40))
             m = n + int(rng.integers(1, 100))
         kind = i % 7
-        yield m, n, S.build(m, n, kind, int(rng.integers(0, 2**62)))
+        a = S.build(m, n, kind, int(rng.integers(0, 2**62)))
+        if i % 5 == 1 and n > 2:  # empty leading columns (read while r = 0)
+            lead = int(rng.integers(1, n))
+            for c in range(lead):
+                a[:, c >> 6] &= ~np.uint64(1 << (c & 63))
+        yield m, n, a
+
+
+def test_partial_ple_tiny_exhaustive():
+    """Every 2x3, 3x2 and 3x3 matrix (and the reference's
+    ColumnRankProfile sizes): restatement == compiled reference."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    for (m, n) in [(2, 3), (3, 2), (3, 3), (4, 2)]:
+        for bits in range(1 << (m * n)):
+            a = np.zeros((m, 1), dtype=np.uint64)
+            for i in range(m):
+                for j in range(n):
+                    if (bits >> (i * n + j)) & 1:
+                        a[i, 0] |= np.uint64(1 << j)
+            x, y = a.copy(), a.copy()
+            got, gp = O.partial_ple(x, m, n)
+            want, wp = O.ref_partial_ple(y, m, n)
+            assert (got.rank, gp) == (want.rank, wp) and np.array_equal(x, y), (m, n, bits)
+            assert partial_processed_rule(m, n, want.rank, want.swaps, want.q) == wp, (m, n, bits)
 
 
 def test_partial_ple_restatement_vs_reference():
@@ -156,11 +182,16 @@ def test_partial_ple_restatement_vs_reference():
         assert (got.rank, gp) == (want.rank, wp), (m, n)
         assert np.array_equal(got.swaps, want.swaps) and np.array_equal(got.q, want.q), (m, n)
         assert np.array_equal(x, y), (m, n)
-        assert partial_processed_rule(m, n, want.rank, want.swaps) == wp, (m, n)
+        assert partial_processed_rule(m, n, want.rank, want.swaps, want.q) == wp, (m, n)
         if wp < m:
             early += 1
-            # rows past the watermark are untouched (acceptance_main.cpp:127-139)
-            assert np.array_equal(y[wp:], a[wp:])
+            # rows past the watermark are untouched apart from the recorded
+            # column swaps (acceptance_main.cpp:127-139)
+            tail = a[wp:].copy()
+            cs = want.col_swaps.astype(np.uintp).reshape(-1, 3)[::-1].copy()
+            cs[:, 2] = 0  # (every swap starts above the tail)
+            O.undo_col_swaps(tail, m - wp, cs)  # reversed list, replayed backwards = forward
+            assert np.array_equal(y[wp:], tail)
         # rank / q / swaps are the complete decomposition's
         z = a.copy()
         full = O.ple(z, m, n)
