@@ -19,7 +19,8 @@ import paper_1111_6549_b200 as G  # noqa: E402
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 CFGS = {"single": G.PleConfig(single_panel=True), "multi": G.PleConfig(multi_kernel=True),
-        "super": G.PleConfig(super_step=True)}
+        "super": G.PleConfig(super_step=True), "peer2": G.PleConfig(peer_ranks=2),
+        "peer3s": G.PleConfig(peer_ranks=3, super_step=True)}
 
 
 def rand_shape():
@@ -77,7 +78,10 @@ def one(it):
 t0 = time.time()
 bad = []
 for it in range(iters):
-    ok, what = one(it)
+    try:
+        ok, what = one(it)
+    except Exception as e:  # noqa: BLE001 (check mode: Gf2cuCheckError names the step)
+        ok, what = False, f"{type(e).__name__}: {e}"
     if not ok:
         bad.append((it, what))
         print("MISMATCH", it, what, flush=True)

@@ -37,11 +37,22 @@ def test_check_mode_passes_and_is_exact(driver):
         assert got.rank == want.rank and np.array_equal(bm.words, ref), (driver, name)
 
 
+def col63_dependent(m, n, seed):
+    """Column 64w+63 a copy of column 64w+62 in every word: no panel ever has
+    a pivot in its last column, so a stray bit there is a finished column
+    holding a bit below the pivots. (In a full-rank panel every column is a
+    pivot column and every bit is a legal multiplier: invariant (iv) cannot
+    see a wrong word there.)"""
+    a = O.fill_random(m, n, 0.5, seed)
+    b62 = (a >> np.uint64(62)) & np.uint64(1)
+    return (a & ~np.uint64(1 << 63)) | (b62 << np.uint64(63))
+
+
 def test_check_mode_from_the_environment(monkeypatch):
     monkeypatch.setenv("GF2CU_CHECK", "1")
     monkeypatch.setenv("GF2CU_CHECK_INJECT", "3")  # corrupt a row's word at step 2
     with pytest.raises(Gf2cuCheckError, match="step 2"):
-        G.block_iterative_ple(G.BitMatrix(700, 700, O.fill_random(700, 700, 0.5, 8)))
+        G.block_iterative_ple(G.BitMatrix(700, 704, col63_dependent(700, 704, 8)))
 
 
 @pytest.mark.parametrize("super_step", [False, True])
@@ -49,15 +60,18 @@ def test_check_mode_detects_a_corrupted_panel_word(monkeypatch, super_step):
     """The checker's own test: GF2CU_CHECK_INJECT=s+1 flips the top bit of
     the first non-pivot row's panel word at step s; that row then carries a
     bit in a finished column, which invariant (iv) forbids."""
-    a = O.fill_random(2000, 2000, 0.5, 9)
+    a = col63_dependent(2000, 2048, 9)
     for step in (0, 6, 18):  # (even: the super-step driver applies panel a at even steps)
         monkeypatch.setenv("GF2CU_CHECK_INJECT", str(step + 1))
         with pytest.raises(Gf2cuCheckError, match=f"step {step} "):
-            G.block_iterative_ple(G.BitMatrix(2000, 2000, a.copy()),
+            G.block_iterative_ple(G.BitMatrix(2000, 2048, a.copy()),
                                   G.PleConfig(check=True, super_step=super_step, single_panel=not super_step))
     monkeypatch.delenv("GF2CU_CHECK_INJECT")
-    bm = G.BitMatrix(2000, 2000, a.copy())
-    G.block_iterative_ple(bm, G.PleConfig(check=True))  # and clean again
+    bm = G.BitMatrix(2000, 2048, a.copy())
+    ref = a.copy()
+    want = O.ple(ref, 2000, 2048)
+    got = G.block_iterative_ple(bm, G.PleConfig(check=True))  # and clean again
+    assert got.rank == want.rank and np.array_equal(bm.words, ref)
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
