@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-shared", "-Xcompiler", "-fPIC", "-cudart", "static",
+    "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-lgomp", "-cudart", "static",
 ]
 
 

@@ -6,6 +6,7 @@
 // never waits inside the loop. The host only polls a mapped pinned mirror of
 // r (a few steps behind) to stop enqueueing once every row holds a pivot.
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <chrono>
@@ -242,6 +243,118 @@ cudaStream_t pick_stream(gf2cu_matrix* a, void* s) {
 }
 
 gf2cu_status alloc_ws(gf2cu_matrix* a);
+
+// ---- pageable host memory ----------------------------------------------
+// The runtime copies pageable host memory through its own small pinned
+// buffers on one thread. Large copies from / to pageable buffers (what a C++
+// caller's gf2::BitMatrix, a std::vector, hands the drop-in) instead go
+// through pinned staging chunks that host threads fill or drain (OpenMP row
+// memcpy) while the copy engine works on the neighbouring chunk.
+struct Staging {
+    static constexpr int kBufs = 3;
+    static constexpr size_t kBytes = size_t(32) << 20;
+    unsigned char* buf[kBufs] = {};
+    cudaEvent_t ev[kBufs] = {};
+    int device = -1;
+    void release() {
+        for (int i = 0; i < kBufs; ++i) {
+            if (ev[i]) cudaEventSynchronize(ev[i]);
+            if (buf[i]) cudaFreeHost(buf[i]);
+            if (ev[i]) cudaEventDestroy(ev[i]);
+            buf[i] = nullptr;
+            ev[i] = nullptr;
+        }
+        device = -1;
+    }
+    ~Staging() { release(); }
+};
+thread_local Staging g_staging;
+
+constexpr size_t kStageMin = size_t(8) << 20;  // smaller copies: the runtime's path
+
+bool host_pageable(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
+
+gf2cu_status staging_ready(int device) {
+    Staging& g = g_staging;
+    if (g.device == device && g.buf[0]) return GF2CU_OK;
+    g.release();
+    for (int i = 0; i < Staging::kBufs; ++i) {
+        CU_TRY(cudaHostAlloc(&g.buf[i], Staging::kBytes, cudaHostAllocDefault));
+        CU_TRY(cudaEventCreateWithFlags(&g.ev[i], cudaEventDisableTiming));
+    }
+    g.device = device;
+    return GF2CU_OK;
+}
+
+void rows_memcpy(unsigned char* dst, size_t dst_pitch, const unsigned char* src, size_t src_pitch, size_t bytes,
+                 size_t rows) {
+    const int nt = std::max(1, std::min(omp_get_max_threads(), 16));
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (long long i = 0; i < (long long)rows; ++i)
+        std::memcpy(dst + (size_t)i * dst_pitch, src + (size_t)i * src_pitch, bytes);
+}
+
+// Host (pitch hp bytes) -> device (pitch dp bytes), `bytes` per row, `rows`
+// rows, ordered on s. Returns with the host buffer free to reuse.
+gf2cu_status staged_h2d(void* dev, size_t dp, const void* host, size_t hp, size_t bytes, size_t rows, int device,
+                        cudaStream_t s) {
+    if (bytes * rows < kStageMin || !host_pageable(host)) {
+        CU_TRY(cudaMemcpy2DAsync(dev, dp, host, hp, bytes, rows, cudaMemcpyHostToDevice, s));
+        return GF2CU_OK;
+    }
+    gf2cu_status st = staging_ready(device);
+    if (st != GF2CU_OK) return st;
+    Staging& g = g_staging;
+    const size_t per = std::max<size_t>(1, Staging::kBytes / bytes);
+    for (size_t c = 0, r0 = 0; r0 < rows; ++c, r0 += per) {
+        const int b = (int)(c % Staging::kBufs);
+        const size_t nr = std::min(per, rows - r0);
+        CU_TRY(cudaEventSynchronize(g.ev[b]));  // (its previous chunk has left)
+        rows_memcpy(g.buf[b], bytes, static_cast<const unsigned char*>(host) + r0 * hp, hp, bytes, nr);
+        CU_TRY(cudaMemcpy2DAsync(static_cast<unsigned char*>(dev) + r0 * dp, dp, g.buf[b], bytes, bytes, nr,
+                                 cudaMemcpyHostToDevice, s));
+        CU_TRY(cudaEventRecord(g.ev[b], s));
+    }
+    return GF2CU_OK;
+}
+
+// Device -> host, synchronous (the host buffer holds the rows on return).
+gf2cu_status staged_d2h(void* host, size_t hp, const void* dev, size_t dp, size_t bytes, size_t rows, int device,
+                        cudaStream_t s) {
+    if (bytes * rows < kStageMin || !host_pageable(host)) {
+        CU_TRY(cudaMemcpy2DAsync(host, hp, dev, dp, bytes, rows, cudaMemcpyDeviceToHost, s));
+        CU_TRY(cudaStreamSynchronize(s));
+        return GF2CU_OK;
+    }
+    gf2cu_status st = staging_ready(device);
+    if (st != GF2CU_OK) return st;
+    Staging& g = g_staging;
+    const size_t per = std::max<size_t>(1, Staging::kBytes / bytes);
+    const size_t nch = (rows + per - 1) / per;
+    auto issue = [&](size_t c) -> cudaError_t {
+        const int b = (int)(c % Staging::kBufs);
+        const size_t r0 = c * per, nr = std::min(per, rows - r0);
+        cudaError_t e = cudaMemcpy2DAsync(g.buf[b], bytes, static_cast<const unsigned char*>(dev) + r0 * dp, dp,
+                                          bytes, nr, cudaMemcpyDeviceToHost, s);
+        return e == cudaSuccess ? cudaEventRecord(g.ev[b], s) : e;
+    };
+    for (size_t c = 0; c < std::min<size_t>(nch, Staging::kBufs - 1); ++c) CU_TRY(issue(c));
+    for (size_t c = 0; c < nch; ++c) {
+        const int b = (int)(c % Staging::kBufs);
+        if (c + Staging::kBufs - 1 < nch) CU_TRY(issue(c + Staging::kBufs - 1));
+        CU_TRY(cudaEventSynchronize(g.ev[b]));
+        const size_t r0 = c * per, nr = std::min(per, rows - r0);
+        rows_memcpy(static_cast<unsigned char*>(host) + r0 * hp, hp, g.buf[b], bytes, bytes, nr);
+    }
+    return GF2CU_OK;
+}
 
 // The workspace is all-or-nothing: a failed allocation frees whatever was
 // already allocated, so the next call on the (cached) matrix retries from
@@ -787,6 +900,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             // (chunks shrink toward the end, where the late super-steps finish
             // few rows each, so that little is left to copy after the kernel)
             uint64_t* host = stream_to->data + (stream_to->col_off >> 6);
+            const bool pageable = host_pageable(host);
             for (;;) {
                 const cudaError_t qe = cudaEventQuery(kdone);
                 if (qe != cudaSuccess && qe != cudaErrorNotReady) {
@@ -799,9 +913,18 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
                 const size_t avail = *reinterpret_cast<volatile u32*>(ws.out_host);
                 const size_t chunk = std::max<size_t>(256, std::min<size_t>(m / 32, (m - sent) / 8));
                 if (avail > sent && (avail - sent >= chunk || fin)) {
-                    CU_TRY(cudaMemcpy2DAsync(host + sent * stream_to->stride, stream_to->stride * 8,
-                                             a->data + sent * a->Wp, a->Wp * 8, W * 8, avail - sent,
-                                             cudaMemcpyDeviceToHost, ws.copy));
+                    if (pageable) {  // (synchronous; the kernel goes on meanwhile)
+                        st = staged_d2h(host + sent * stream_to->stride, stream_to->stride * 8,
+                                        a->data + sent * a->Wp, a->Wp * 8, W * 8, avail - sent, a->device, ws.copy);
+                        if (st != GF2CU_OK) {
+                            cudaEventDestroy(kdone);
+                            return st;
+                        }
+                    } else {
+                        CU_TRY(cudaMemcpy2DAsync(host + sent * stream_to->stride, stream_to->stride * 8,
+                                                 a->data + sent * a->Wp, a->Wp * 8, W * 8, avail - sent,
+                                                 cudaMemcpyDeviceToHost, ws.copy));
+                    }
                     sent = avail;
                 }
                 if (fin) break;
@@ -1188,8 +1311,7 @@ gf2cu_status view_upload(const gf2cu_view* v, gf2cu_matrix* a, cudaStream_t s,
     if (m == 0 || W == 0) return GF2CU_OK;
     cudaError_t e;
     if (view_aligned(v)) {
-        e = cudaMemcpy2DAsync(a->data, a->Wp * 8, v->data + (v->col_off >> 6), v->stride * 8, W * 8,
-                              m, cudaMemcpyHostToDevice, s);
+        return staged_h2d(a->data, a->Wp * 8, v->data + (v->col_off >> 6), v->stride * 8, W * 8, m, a->device, s);
     } else {
         packed.assign(m * W, 0ull);
         for (size_t i = 0; i < m; ++i) {
@@ -1211,10 +1333,8 @@ gf2cu_status view_download(const gf2cu_view* v, const gf2cu_matrix* a, cudaStrea
     cudaError_t e;
     if (view_aligned(v)) {
         if (row_lo >= m) return GF2CU_OK;
-        e = cudaMemcpy2DAsync(v->data + (v->col_off >> 6) + row_lo * v->stride, v->stride * 8,
-                              a->data + row_lo * a->Wp, a->Wp * 8, W * 8, m - row_lo,
-                              cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        return staged_d2h(v->data + (v->col_off >> 6) + row_lo * v->stride, v->stride * 8,
+                          a->data + row_lo * a->Wp, a->Wp * 8, W * 8, m - row_lo, a->device, s);
     } else {
         packed.resize(m * W);
         e = cudaMemcpy2DAsync(packed.data(), W * 8, a->data, a->Wp * 8, W * 8, m,
@@ -1430,8 +1550,8 @@ gf2cu_status gf2cu_matrix_upload(gf2cu_matrix* a, const uint64_t* host, size_t h
     if (a->m == 0 || a->W == 0) return GF2CU_OK;
     DeviceGuard g(a->device);
     cudaStream_t s = pick_stream(a, stream);
-    CU_TRY(cudaMemcpy2DAsync(a->data, a->Wp * 8, host, host_stride * 8, a->W * 8, a->m,
-                             cudaMemcpyHostToDevice, s));
+    gf2cu_status st = staged_h2d(a->data, a->Wp * 8, host, host_stride * 8, a->W * 8, a->m, a->device, s);
+    if (st != GF2CU_OK) return st;
     CU_TRY(cudaStreamSynchronize(s));
     return GF2CU_OK;
 }
@@ -1443,10 +1563,7 @@ gf2cu_status gf2cu_matrix_download(const gf2cu_matrix* a, uint64_t* host, size_t
     if (a->m == 0 || a->W == 0) return GF2CU_OK;
     DeviceGuard g(a->device);
     cudaStream_t s = pick_stream(const_cast<gf2cu_matrix*>(a), stream);
-    CU_TRY(cudaMemcpy2DAsync(host, host_stride * 8, a->data, a->Wp * 8, a->W * 8, a->m,
-                             cudaMemcpyDeviceToHost, s));
-    CU_TRY(cudaStreamSynchronize(s));
-    return GF2CU_OK;
+    return staged_d2h(host, host_stride * 8, a->data, a->Wp * 8, a->W * 8, a->m, a->device, s);
 }
 
 gf2cu_status gf2cu_matrix_copy(gf2cu_matrix* dst, const gf2cu_matrix* src, void* stream) {

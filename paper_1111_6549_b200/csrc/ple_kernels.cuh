@@ -1124,6 +1124,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             if (sh.super) la->piv2_out[k] = sh.piv2[k];
         }
         named_bar(kBodyBar, nthr);
+        // (a) each slot's combination d for step w and its pre-step word w+1
         for (u32 k = threadIdx.x; k < nwin1; k += nthr) {
             const u32 q = r1 + k;  // position
             u64 d, pre;
@@ -1148,14 +1149,25 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 }
                 pre = sh.epb2[q - r - nwin];
             }
-            u64 x = pre;
-#pragma unroll 8
-            for (u32 s2 = 0; s2 < 64; ++s2) {
-                if (s2 >= t) break;
+            sh.nraw[k] = pre;
+            sh.ndacc[k] = d;
+        }
+        named_bar(kBodyBar, nthr);
+        // (b) word w+1 after step w = pre ^ sum_s d_s piv2[s]: four lanes per
+        // slot, 16 pivots each, folded with two shuffles (every lane of a
+        // warp runs the same iterations: nthr and 4 * kWin are multiples of 32)
+        for (u32 g = threadIdx.x; g < 4u * kWin; g += nthr) {
+            const u32 k = g >> 2, part = g & 3u;
+            const u64 d = k < nwin1 ? sh.ndacc[k] : 0ull;
+            u64 x = 0ull;
+#pragma unroll
+            for (u32 i = 0; i < 16u; ++i) {
+                const u32 s2 = 16u * part + i;  // (bits s2 >= t of d are zero)
                 x ^= sh.piv2[s2] & (0ull - ((d >> s2) & 1ull));
             }
-            sh.nraw[k] = x;
-            sh.ndacc[k] = d;
+            x ^= __shfl_xor_sync(0xffffffffu, x, 1);
+            x ^= __shfl_xor_sync(0xffffffffu, x, 2);
+            if (part == 0u && k < nwin1) sh.nraw[k] ^= x;
         }
         named_bar(kBodyBar, nthr);
     }
