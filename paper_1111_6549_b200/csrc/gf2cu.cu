@@ -51,6 +51,26 @@ u32 panel_flags() {
     return e ? (u32)std::strtoul(e, nullptr, 0) : (gf2cu::kPanelStream | gf2cu::kPanelSuperLA);
 }
 
+// Zero-fill at creation, COMPLETED before returning. A plain cudaMemset is
+// enqueued on the legacy default stream and is asynchronous with respect to
+// the host; the objects' own streams are non-blocking, so a later upload on
+// them was not ordered after it and the fill could land on top of the
+// uploaded matrix (round 2: the root cause of the rare rank-0 / wrong-word
+// results on the first call with a new shape).
+cudaError_t zero_now(void* p, size_t bytes) {
+    cudaError_t e = cudaMemsetAsync(p, 0, bytes, 0);
+    return e == cudaSuccess ? cudaStreamSynchronize(0) : e;
+}
+
+// Host -> device copy of parameters, COMPLETED before returning: a plain
+// cudaMemcpy from pageable memory returns once the source is staged, its DMA
+// runs on the legacy default stream, which the kernels' non-blocking streams
+// are not ordered after.
+cudaError_t h2d_now(void* dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? cudaStreamSynchronize(0) : e;
+}
+
 gf2cu_status fail(gf2cu_status st, const std::string& msg) {
     g_last_error = msg;
     return st;
@@ -165,6 +185,7 @@ void apply_watchdog_env(int dev) {
         if (sec > 0) {
             const unsigned long long ns = (unsigned long long)(sec * 1e9);
             cudaMemcpyToSymbol(gf2cu::g_watchdog_ns, &ns, sizeof(ns));
+            cudaStreamSynchronize(0);  // (ordered before kernels on non-blocking streams)
         }
     }
 }
@@ -215,6 +236,7 @@ struct PeerWs {
     std::vector<gf2cu::PeerParams> hp;  // host copies of the ranks' parameters
     gf2cu::PeerParams* dp = nullptr;    // device copy (the kernel argument)
     std::vector<void*> allocs;
+    std::vector<size_t> sizes;          // bytes of each allocation
 };
 
 void free_peer(PeerWs& w) {
@@ -386,7 +408,7 @@ gf2cu_status alloc_ws(gf2cu_matrix* a) {
     CU_TRY(cudaMalloc(&w.sync, sizeof(gf2cu::SyncState)));
     CU_TRY(cudaMalloc(&w.phase_ns, (8 * (a->W + 1) + 8 + 2 * 64 * 5 + 3 * 160) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.stage, 64 * wpad8(a->W) * sizeof(u64)));
-    CU_TRY(cudaMemset(w.stage, 0, 64 * wpad8(a->W) * sizeof(u64)));
+    CU_TRY(zero_now(w.stage, 64 * wpad8(a->W) * sizeof(u64)));
     CU_TRY(cudaMalloc(&w.state, sizeof(gf2cu::StepState)));
     CU_TRY(cudaMalloc(&w.pout, sizeof(gf2cu::PanelOut)));
     CU_TRY(cudaMalloc(&w.swaps, mn * sizeof(u32)));
@@ -418,6 +440,15 @@ gf2cu_status check_reset(u32* chk, cudaStream_t s) {
     static const u32 init[4] = {0xffffffffu, 0u, 0xffffffffu, 0u};
     CU_TRY(cudaMemcpyAsync(chk, init, sizeof(init), cudaMemcpyHostToDevice, s));
     return GF2CU_OK;
+}
+
+// GF2CU_POISON=<byte>: fill every scratch buffer of a factorization with
+// that byte before each run (a diagnostic: a result that depends on a stale
+// or uninitialized scratch word then fails deterministically instead of
+// depending on what an earlier call left behind).
+int poison_byte() {
+    const char* e = std::getenv("GF2CU_POISON");
+    return e && e[0] ? (int)(std::strtoul(e, nullptr, 0) & 0xff) : -1;
 }
 
 // After the factorization: the result invariants on the row-major matrix,
@@ -463,11 +494,15 @@ gf2cu::PeerBufs peer_bufs_at(void* base, size_t m, size_t Wp8) {
 // Allocates rank k's local rows and replicated state (h.p) and its exchange
 // buffers (*xbuf, h.peer[k]); every allocation is appended to `allocs`.
 gf2cu_status peer_alloc_rank(gf2cu::PeerParams& h, std::vector<void*>& allocs, size_t m, size_t n,
-                             unsigned k, unsigned G, unsigned block, void** xbuf) {
+                             unsigned k, unsigned G, unsigned block, void** xbuf,
+                             std::vector<size_t>* sizes = nullptr) {
     const size_t W = words_of(n), Wp8 = wpad8(W), mn = std::max<size_t>(1, std::min(m, n));
     auto alloc = [&](void** ptr, size_t bytes) -> cudaError_t {
         cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
-        if (e == cudaSuccess) allocs.push_back(*ptr);
+        if (e == cudaSuccess) {
+            allocs.push_back(*ptr);
+            if (sizes) sizes->push_back(std::max<size_t>(bytes, 16));
+        }
         return e;
     };
 #define PA(ptr, bytes) CU_TRY(alloc(reinterpret_cast<void**>(&(ptr)), (bytes)))
@@ -639,7 +674,7 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
             pw.hp.assign(G, gf2cu::PeerParams{});
             for (unsigned k = 0; k < G; ++k) {
                 void* xbuf = nullptr;
-                gf2cu_status st = peer_alloc_rank(pw.hp[k], pw.allocs, m, n, k, G, block, &xbuf);
+                gf2cu_status st = peer_alloc_rank(pw.hp[k], pw.allocs, m, n, k, G, block, &xbuf, &pw.sizes);
                 if (st != GF2CU_OK) return st;
             }
             for (unsigned k = 0; k < G; ++k)
@@ -647,7 +682,7 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
             gf2cu::PeerParams* dp = nullptr;
             CU_TRY(cudaMalloc(&dp, G * sizeof(gf2cu::PeerParams)));
             pw.dp = dp;
-            CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
+            CU_TRY(h2d_now(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams)));
             return GF2CU_OK;
         };
         const gf2cu_status st = setup();
@@ -674,7 +709,13 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
             pw.hp[k].p.Wpad8 = wpad;
             pw.hp[k].p.check = chk;
         }
-        CU_TRY(cudaMemcpy(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams), cudaMemcpyHostToDevice));
+        CU_TRY(h2d_now(pw.dp, pw.hp.data(), G * sizeof(gf2cu::PeerParams)));
+    }
+    if (const int pb = poison_byte(); pb >= 0) {
+        // every allocation of every rank (rows, records, replicated state,
+        // exchange buffers); the counters are reset below
+        for (size_t i = 0; i < pw.allocs.size() && i < pw.sizes.size(); ++i)
+            CU_TRY(cudaMemsetAsync(pw.allocs[i], pb, pw.sizes[i], s));
     }
     for (unsigned k = 0; k < G; ++k) {
         gf2cu_status st = peer_reset_rank(pw.hp[k], s);
@@ -706,6 +747,27 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
         if (c[gf2cu::kCtrErr]) return fail(GF2CU_ECUDA, "row-sharded PLE kernel watchdog tripped");
     }
     st = peer_outputs(pw.hp[0], super, s, swaps, q, rank, col_swaps, n_col_swaps, nullptr, stats);
+    if (st == GF2CU_OK && *rank == 0 && std::getenv("GF2CU_DEBUG_PEER")) {
+        // diagnostics of a rank-0 outcome: every rank's step state, counters
+        for (unsigned k = 0; k < G; ++k) {
+            const gf2cu::PeerParams& h = pw.hp[k];
+            u32 c[gf2cu::kCtrWords];
+            gf2cu::SyncState sy{};
+            gf2cu::StepState fin{};
+            std::vector<u32> rh(W + 1), rbh(W + 1);
+            cudaMemcpy(c, h.peer[k].ctr, sizeof(c), cudaMemcpyDeviceToHost);
+            cudaMemcpy(&sy, h.p.sync, sizeof(sy), cudaMemcpyDeviceToHost);
+            cudaMemcpy(&fin, h.p.state, sizeof(fin), cudaMemcpyDeviceToHost);
+            cudaMemcpy(rh.data(), h.p.rhist, (W + 1) * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(rbh.data(), h.p.rbhist, (W + 1) * 4, cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "PEERDBG %zux%zu G=%u block=%u super=%d rank %u: state {%u,%u} panel_done %u cap %u t %u err %u ctr",
+                         m, n, G, block, (int)super, k, fin.r, fin.rb, sy.panel_done, sy.cap_count, sy.t_count, sy.error);
+            for (int i = 0; i < gf2cu::kCtrWords; ++i) std::fprintf(stderr, " %u", c[i]);
+            std::fprintf(stderr, " rhist");
+            for (size_t w = 0; w < W; ++w) std::fprintf(stderr, " %u/%u", rh[w], rbh[w]);
+            std::fprintf(stderr, "\n");
+        }
+    }
     if (st == GF2CU_OK && checking) st = check_verdict(a, chk, *rank, sms, s);
     if (st == GF2CU_OK && stats && timing) {
         float ms = 0.f;
@@ -845,6 +907,23 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         p.out_host = ws.out_host_dev;
     }
     size_t sent = 0;
+    if (const int pb = poison_byte(); pb >= 0) {
+        const size_t mm = std::max<size_t>(1, m), mn = std::max<size_t>(1, std::min(m, n));
+        CU_TRY(cudaMemsetAsync(a->alt, pb, mm * wpad8(W) * sizeof(u64), s));
+        CU_TRY(cudaMemsetAsync(ws.pb, pb, mm * sizeof(u64), s));
+        CU_TRY(cudaMemsetAsync(ws.pb2, pb, mm * sizeof(u64), s));
+        CU_TRY(cudaMemsetAsync(ws.info, pb, 4 * mm * sizeof(ulonglong2), s));
+        CU_TRY(cudaMemsetAsync(ws.stage, pb, 64 * wpad8(W) * sizeof(u64), s));
+        CU_TRY(cudaMemsetAsync(ws.perm, pb, mm * sizeof(u32), s));
+        CU_TRY(cudaMemsetAsync(ws.pout, pb, sizeof(gf2cu::PanelOut), s));
+        CU_TRY(cudaMemsetAsync(ws.pout_b, pb, sizeof(gf2cu::PanelOut), s));
+        CU_TRY(cudaMemsetAsync(ws.sout, pb, sizeof(gf2cu::SuperOut), s));
+        CU_TRY(cudaMemsetAsync(ws.swaps, pb, mn * sizeof(u32), s));
+        CU_TRY(cudaMemsetAsync(ws.qcol, pb, mn * sizeof(u32), s));
+        CU_TRY(cudaMemsetAsync(ws.rhist, pb, (W + 1) * sizeof(u32), s));
+        CU_TRY(cudaMemsetAsync(ws.rbhist, pb, (W + 1) * sizeof(u32), s));
+        if (ws.ubuf) CU_TRY(cudaMemsetAsync(ws.ubuf, pb, ws.ucap * p.Wpad8 * sizeof(u64), s));
+    }
     if (super) {
         p.Wpad8 = Wpad4;  // the super-step driver's tile width is 32 bytes
         gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4);
@@ -1508,7 +1587,7 @@ gf2cu_status gf2cu_matrix_create(size_t m, size_t n, int device, gf2cu_matrix** 
     a->device = device;
     const size_t bytes = std::max<size_t>(1, m) * a->Wp * sizeof(u64);
     cudaError_t e = cudaMalloc(&a->data, bytes);
-    if (e == cudaSuccess) e = cudaMemset(a->data, 0, bytes);
+    if (e == cudaSuccess) e = zero_now(a->data, bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->own, cudaStreamNonBlocking);
     if (e == cudaSuccess) apply_watchdog_env(device);
     if (e != cudaSuccess) {
@@ -2009,8 +2088,8 @@ gf2cu_status gf2cu_shard_create(size_t m, size_t n, int rank, int nranks, size_t
     alloc(&s->rhist, (s->W + 1) * 4);
     alloc(&s->rbhist, (s->W + 1) * 4);
     alloc(&s->status, (8 + 2 * (size_t)nranks) * 4);
-    if (e == cudaSuccess) e = cudaMemset(s->data, 0, ml * s->Wp * 8);
-    if (e == cudaSuccess) e = cudaMemset(s->stage, 0, 64 * s->Wpad8 * 8);
+    if (e == cudaSuccess) e = zero_now(s->data, ml * s->Wp * 8);
+    if (e == cudaSuccess) e = zero_now(s->stage, 64 * s->Wpad8 * 8);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking);
     if (e == cudaSuccess) apply_watchdog_env(s->device);
     if (e != cudaSuccess) {
@@ -2337,10 +2416,10 @@ gf2cu_status gf2cu_peer_create(size_t m, size_t n, int rank, int nranks, size_t 
     if (st == GF2CU_OK) {
         const size_t bytes = std::max<size_t>(1, p->hp.m_loc) * p->Wp * 8;
         e = cudaMalloc(&p->data, bytes);
-        if (e == cudaSuccess) e = cudaMemset(p->data, 0, bytes);
-        if (e == cudaSuccess) e = cudaMemset(p->xbuf, 0, peer_xbytes(m, p->Wp8));
+        if (e == cudaSuccess) e = zero_now(p->data, bytes);
+        if (e == cudaSuccess) e = zero_now(p->xbuf, peer_xbytes(m, p->Wp8));
         if (e == cudaSuccess) e = cudaMalloc(&p->dp, sizeof(gf2cu::PeerParams));
-        if (e == cudaSuccess) e = cudaMemcpy(p->dp, &p->hp, sizeof(p->hp), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = h2d_now(p->dp, &p->hp, sizeof(p->hp));
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking);
     }
     if (st != GF2CU_OK || e != cudaSuccess) {
@@ -2396,7 +2475,7 @@ gf2cu_status gf2cu_peer_connect(gf2cu_peer* p, const void* handles) {
         p->opened.push_back(ptr);
         p->hp.peer[j] = peer_bufs_at(ptr, p->m, p->Wp8);
     }
-    CU_TRY(cudaMemcpy(p->dp, &p->hp, sizeof(p->hp), cudaMemcpyHostToDevice));
+    CU_TRY(h2d_now(p->dp, &p->hp, sizeof(p->hp)));
     p->connected = true;
     return GF2CU_OK;
 }
@@ -2473,7 +2552,7 @@ gf2cu_status gf2cu_peer_run(gf2cu_peer* p, void* stream, gf2cu_stats* stats) {
     const u32 wpad = p->super ? (u32)std::max<size_t>(4, (p->W + 3) / 4 * 4) : (u32)p->Wp8;
     if (p->hp.p.Wpad8 != wpad) {
         p->hp.p.Wpad8 = wpad;
-        CU_TRY(cudaMemcpy(p->dp, &p->hp, sizeof(p->hp), cudaMemcpyHostToDevice));
+        CU_TRY(h2d_now(p->dp, &p->hp, sizeof(p->hp)));
     }
     if (p->hp.m_loc) {
         if (p->super)
@@ -2643,7 +2722,7 @@ gf2cu_status gf2cu_litmus(int kind, unsigned rounds, int device, unsigned long l
         cudaError_t e = cudaMalloc(ptr, bytes);
         if (e == cudaSuccess) {
             allocs.push_back(*ptr);
-            e = cudaMemset(*ptr, 0, bytes);
+            e = zero_now(*ptr, bytes);
         }
         return e;
     };

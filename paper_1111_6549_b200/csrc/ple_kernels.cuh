@@ -680,9 +680,14 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         sh.super = la ? la->super_mode : 0;
     }
     named_bar(kBodyBar, nthr);
-    if (sh.super == 1 && !sh.cap_ok && !la->have_window) {
-        // panel a reads its window from the previous super-step's capture
-        // (unless the look-ahead across super-steps computed it)
+    if (la && sh.super != 2 && !sh.cap_ok && !la->have_window) {
+        // a window read from the capture (pb, perm) waits for it: panel a of
+        // a super-step (unless the look-ahead across super-steps computed its
+        // window), and step 0 of the row-sharded drivers, whose init (perm,
+        // pb[0]) runs inside the same launch. (Round 2: this wait was missing
+        // for the single-panel row-sharded driver's step 0 -- the cause of
+        // its rare mismatches, 1 in ~13,000 calls, e.g. rank 0 when the
+        // window read the previous call's words.)
         if (threadIdx.x == 0)
             sh.cap_ok = (la->sys ? spin_geq_sys(la->cap_ctr, la->cap_target, la->err)
                                  : spin_geq(la->cap_ctr, la->cap_target, la->err)) ? 1 : -1;

@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         // sweep it over the look-ahead tile (capturing words w+2, w+3)
         const bool early = S == 0 || ct == (w >> 2);
         u32 mine = 0;
-        bool loaded = false, la_ready = false;
+        bool loaded = false, la_ready = false, built = false;
         for (;;) {
             if (threadIdx.x == 0) s_ok = atomicAdd(&p.ap_claim[S], 1u);
             __syncthreads();
@@ -446,9 +446,10 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                     if (!peer_wait(s, ctr + kCtrLa, G * (S + 1u), true, s_ok)) return;
                     la_ready = true;
                 }
-                if (rba + rbb > 0) {
+                if (rba + rbb > 0 && !built) {  // (the same tables for every chunk of S)
                     peer_build16(smem, stage, ct, w, rba, rbb);
                     __syncthreads();
+                    built = true;
                 }
                 peer_trail16_rows(s, smem, S, r, ct, l0, l1 - l0, info, ipos);
             }
