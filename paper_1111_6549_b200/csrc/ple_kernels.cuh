@@ -122,12 +122,6 @@ constexpr u32 kPanelStream = 1u;
 // ... the super-step driver's panel CTA computes the next panel a's window
 // itself when the workers are ahead (ple_super.cuh, super_la_gather).
 constexpr u32 kPanelSuperLA = 2u;
-// ... the leader warp runs its epoch on the TRANSPOSED 32-row block (one
-// column bit-mask per lane, panel_leader_transposed, with a shadow warp
-// keeping the combinations) instead of one row per lane; the followers then
-// catch up at the epoch's closing barrier. Bit-exact, but not the default:
-// measured slower end to end ("tried").
-constexpr u32 kPanelTransposed = 4u;
 
 // Panel status words written when Params::status is set.
 constexpr int kStatusMiss = 0;   // 1 = aborted on a window miss (window_only)
@@ -192,173 +186,6 @@ __device__ __forceinline__ int ld_acquire_cta(const int* a) {
                  : "r"((u32)__cvta_generic_to_shared(a))
                  : "memory");
     return v;
-}
-
-// 32 x 32 bit transpose across a warp: lane i holds row i (bit k = column k);
-// returns, in lane k, column k (bit i = row i's bit k). Five butterfly stages,
-// each one shuffle and a masked merge.
-__device__ __forceinline__ u32 transpose32(u32 x) {
-    const u32 lane = threadIdx.x & 31u;
-#pragma unroll
-    for (int st = 4; st >= 0; --st) {
-        const u32 s = 1u << st;
-        const u32 m = st == 4 ? 0x0000FFFFu : st == 3 ? 0x00FF00FFu : st == 2 ? 0x0F0F0F0Fu
-                      : st == 1 ? 0x33333333u : 0x55555555u;
-        const u32 y = __shfl_xor_sync(0xffffffffu, x, (int)s);
-        x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
-    }
-    return x;
-}
-
-// One leader epoch on the transposed block (kPanelTransposed), run by TWO
-// warps on different SM sub-partitions (a single warp is issue-bound: the
-// ALU pipes take two cycles per warp instruction).
-//   leader (the warp holding slot t): its 32 window rows become 64 column
-//     masks (lane k: columns k, k+32; bit i = row i's reduced word). The
-//     first live row holding column j is the pivot P (ple.hpp:88-93); every
-//     lane XORs the candidates except P into the masks of the columns the
-//     pivot row holds (the elimination) and swaps rows t and P in them (the
-//     LAPACK swap). Masks are broadcast four columns at a time; within the
-//     group each pivot is also applied to the broadcast copies of the later
-//     columns, so the dependent chain per pivot is a few mask operations (the
-//     pivot as a bit, cand & -cand). It publishes every pivot's candidate set.
-//   shadow (another window warp): the rows' combination masks (lane s: bits
-//     s, s+32 of every row's acc), updated from the published candidate sets
-//     with D_t = acc_P ^ (1 << t) (every eliminated row gets bit t), and the
-//     q / sw records.
-// Identical decisions and row contents to the row-per-lane loop. At the end
-// both transpose back: the leader's red / acc / org are in row form again,
-// E / D of the epoch's pivots recorded (a pivot row is frozen once taken).
-__device__ __forceinline__ void mask_update(u32& M, u32 bitP, u32 tbit, u32 elim, u32 flip, u32 force) {
-    const bool bp = (M & bitP) != 0u, bt = (M & tbit) != 0u;
-    M ^= ((bp || force) ? elim : 0u) ^ ((bp != bt) ? flip : 0u);
-}
-
-constexpr int kShadowBar = 6;  // leader + shadow warps (64 threads)
-
-struct TransposedShared {
-    // per pivot t: (tag << 32) | candidate set of the window block's rows,
-    // tag = the (step, epoch) it belongs to; a word whose candidate set is
-    // empty closes the epoch. Each word validates itself, so the shadow needs
-    // no fence or flag: it polls the word it waits for.
-    u64 cand[65];
-    u64 acc[32];    // the leader block's combinations, row form (in / out)
-    u32 org[32];    // ... and origins
-};
-
-__device__ __forceinline__ u32 epoch_tag(u32 w, int epoch) { return (w << 8) | ((u32)epoch & 0xffu); }
-
-__device__ __forceinline__ void panel_leader_transposed(u64& red, u64& acc, u32& org, bool inwin, int& t,
-                                                        int& j, int tend, u32 base, u32 tag, u64* sE,
-                                                        TransposedShared& ts) {
-    // Branches below test warp votes: the epoch runs inside divergent code
-    // (the window warps' branch), so plain tests of these warp-uniform values
-    // would become divergent branches with reconvergence barriers per pivot.
-    constexpr int kG = 2;  // columns per broadcast
-    const u32 lane = threadIdx.x & 31u;
-    ts.acc[lane] = acc;
-    ts.org[lane] = org;
-    named_bar(kShadowBar, 64);
-    u32 C0 = transpose32((u32)red), C1 = transpose32((u32)(red >> 32));
-    const int t0 = t;
-    u32 live = __ballot_sync(0xffffffffu, inwin & (base + lane >= (u32)t));
-    int myq = -1;  // the column of the pivot this lane's slot becomes
-    volatile u64* vc = ts.cand;
-    bool go = t < tend;
-    while (__all_sync(0xffffffffu, go)) {
-        u32 bc[kG];
-#pragma unroll
-        for (int g = 0; g < kG; ++g) {
-            const int jj = min(j + g, 63);
-            bc[g] = __shfl_sync(0xffffffffu, jj < 32 ? C0 : C1, jj & 31);
-        }
-#pragma unroll
-        for (int g = 0; g < kG; ++g) {
-            const u32 cand = bc[g] & live;
-            if (__all_sync(0xffffffffu, cand == 0u)) {
-                go = false;
-                break;
-            }
-            vc[t] = ((u64)tag << 32) | cand;  // (every lane stores the same word)
-            const u32 tl = (u32)t & 31u;
-            const u32 bitP = cand & (0u - cand), tbit = 1u << tl;
-            const u32 elim = cand ^ bitP, flip = tbit | bitP;
-            // (elim never holds rows tl or P: the XOR and the swap commute)
-#pragma unroll
-            for (int h = g + 1; h < kG; ++h) mask_update(bc[h], bitP, tbit, elim, flip, 0u);
-            if (__all_sync(0xffffffffu, j < 32)) mask_update(C0, bitP, tbit, elim, flip, 0u);
-            mask_update(C1, bitP, tbit, elim, flip, 0u);  // (columns < 32 are done once j >= 32)
-            myq = lane == tl ? j : myq;
-            live &= ~tbit;
-            ++t;
-            ++j;
-            if (__all_sync(0xffffffffu, t >= tend)) {
-                go = false;
-                break;
-            }
-        }
-    }
-    if (lane == 0u) vc[t] = (u64)tag << 32;  // closes the epoch
-    red = (u64)transpose32(C0) | ((u64)transpose32(C1) << 32);
-    const int s = (int)(base + lane);
-    if (s >= t0 && s < t) sE[s] = red & ~low_mask64(myq + 1);  // frozen since it was taken
-    named_bar(kShadowBar, 64);
-    acc = ts.acc[lane];
-    org = ts.org[lane];
-}
-
-__device__ __forceinline__ void panel_shadow_transposed(int t, int j, u32 base, u32 tag, u64* sD, u32* sq,
-                                                        u32* ssw, TransposedShared& ts) {
-    const u32 lane = threadIdx.x & 31u;
-    named_bar(kShadowBar, 64);
-    const u64 a = ts.acc[lane];
-    const u32 org0 = ts.org[lane];
-    u32 A0 = transpose32((u32)a), A1 = transpose32((u32)(a >> 32));
-    // origins as 8 bit planes (lane b: bit b of every row's origin; an origin
-    // is a window offset < 128 or 0x80000000 | t): the swaps need no shuffle
-    const u32 okey = (org0 & 0x7fu) | ((org0 >> 24) & 0x80u);
-    u32 O = 0u;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        const u32 m = __ballot_sync(0xffffffffu, (okey >> b) & 1u);
-        O = lane == (u32)b ? m : O;
-    }
-    const int t0 = t, j0 = j;
-    const volatile u64* vc = ts.cand;
-    u64 x = vc[t];
-    // (bounded: at most 32 pivots and the closing word per epoch; the spin
-    // below is entered only when the shadow has caught up with the leader)
-    for (int it = 0; it <= 32; ++it) {
-        if (!__all_sync(0xffffffffu, (u32)(x >> 32) == tag)) {
-            do {
-                x = vc[t];
-            } while (!__all_sync(0xffffffffu, (u32)(x >> 32) == tag));
-        }
-        const u32 cand = (u32)x;
-        if (__all_sync(0xffffffffu, cand == 0u)) break;
-        x = vc[t + 1];  // the next word's load in flight while this pivot is applied
-        const u32 tl = (u32)t & 31u;
-        const u32 bitP = cand & (0u - cand), tbit = 1u << tl;
-        const u32 elim = cand ^ bitP, flip = tbit | bitP;
-        // D_t = acc_P ^ (1 << t): combination bit t is set in every eliminated row
-        mask_update(A0, bitP, tbit, elim, flip, lane == (u32)t);
-        if (__all_sync(0xffffffffu, t >= 32))  // (bits >= 32 exist from t = 32 on)
-            mask_update(A1, bitP, tbit, elim, flip, lane + 32u == (u32)t);
-        mask_update(O, bitP, tbit, 0u, flip, 0u);
-        // (every lane stores the same word: no divergent branch)
-        sq[t] = (u32)(j0 + (t - t0));
-        ssw[t] = base + (u32)(__ffs(bitP) - 1);
-        ++t;
-    }
-    const u64 acc = (u64)transpose32(A0) | ((u64)transpose32(A1) << 32);
-    u32 key = 0u;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) key |= ((__shfl_sync(0xffffffffu, O, b) >> lane) & 1u) << b;
-    ts.acc[lane] = acc;
-    ts.org[lane] = (key & 0x80u) ? (0x80000000u | (key & 0x7fu)) : key;
-    const int s = (int)(base + lane);
-    if (s >= t0 && s < t) sD[s] = acc | (1ull << s);
-    named_bar(kShadowBar, 64);
 }
 
 // Loads of data another CTA of the same (persistent) grid may have written:
@@ -562,7 +389,6 @@ struct PanelShared {
     u32 la_phys[kWin];
     unsigned char la_ent[kWin];    // 1: the row entered (outside panel b's window)
     int la_go;
-    TransposedShared tsh;  // kPanelTransposed leader / shadow exchange
     int prog;    // pivots the leader has published (kPanelStream)
     int ep_fin;  // epoch + 1 once the leader closed it (kPanelStream)
 };
@@ -760,14 +586,12 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 sh.wphys[me] = ldcg(p.perm + r + me);
             }
         }
-        if (me <= 64u) sh.tsh.cand[me] = ~0ull;  // no pivot published (shared memory starts undefined)
         if (me == 0) {
             sh.dbg_lead_cyc = sh.dbg_lead_piv = sh.dbg_cross = sh.dbg_epochs = 0u;
             sh.prog = 0;
             sh.ep_fin = 0;
         }
-        const bool transposed = (p.pflags & kPanelTransposed) != 0u;
-        const bool stream = (p.pflags & kPanelStream) != 0u && !transposed;
+        const bool stream = (p.pflags & kPanelStream) != 0u;
         named_bar(3, kWin);
         if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 6] = globaltimer();
         int t = 0;
@@ -892,22 +716,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         int j = 0, epoch = 0;
         while (j < jmax && (u32)t < nrem) {
             const int L = t >> 5;
-            if (transposed && (int)wid == (L ^ 1)) {
-                panel_shadow_transposed(t, j, 32u * (u32)L, epoch_tag(w, epoch), sh.D, sh.q, sh.sw, sh.tsh);
-            } else if ((int)wid == L && transposed) {
-                const long long dbg_c0 = clock64();
-                const int dbg_t0 = t;
-                const int lim = min(jmax - j, min((int)nrem - t, 32 * (L + 1) - t));
-                panel_leader_transposed(red, acc, org, inwin, t, j, t + lim, 32u * (u32)L, epoch_tag(w, epoch),
-                                        sh.E, sh.tsh);
-                if (lane == 0) {
-                    sh.ep_t[epoch & 1] = t;
-                    sh.ep_j[epoch & 1] = j;
-                    sh.dbg_lead_cyc += (u32)(clock64() - dbg_c0);
-                    sh.dbg_lead_piv += (u32)(t - dbg_t0);
-                    sh.dbg_epochs += 1u;
-                }
-            } else if ((int)wid == L) {
+            if ((int)wid == L) {
                 const long long dbg_c0 = clock64();
                 const int dbg_t0 = t;
                 const u32 base = 32u * (u32)L;
@@ -1129,7 +938,6 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             if (sh.super) la->piv2_out[k] = sh.piv2[k];
         }
         named_bar(kBodyBar, nthr);
-        // (a) each slot's combination d for step w and its pre-step word w+1
         for (u32 k = threadIdx.x; k < nwin1; k += nthr) {
             const u32 q = r1 + k;  // position
             u64 d, pre;
@@ -1154,27 +962,43 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 }
                 pre = sh.epb2[q - r - nwin];
             }
-            sh.nraw[k] = pre;
             sh.ndacc[k] = d;
-        }
-        named_bar(kBodyBar, nthr);
-        // (b) word w+1 after step w = pre ^ sum_s d_s piv2[s]: four lanes per
-        // slot, 16 pivots each, folded with two shuffles (every lane of a
-        // warp runs the same iterations: nthr and 4 * kWin are multiples of 32)
-        for (u32 g = threadIdx.x; g < 4u * kWin; g += nthr) {
-            const u32 k = g >> 2, part = g & 3u;
-            const u64 d = k < nwin1 ? sh.ndacc[k] : 0ull;
-            u64 x = 0ull;
-#pragma unroll
-            for (u32 i = 0; i < 16u; ++i) {
-                const u32 s2 = 16u * part + i;  // (bits s2 >= t of d are zero)
+            if (sh.super) {  // (the XOR in (b) below)
+                sh.nraw[k] = pre;
+                continue;
+            }
+            u64 x = pre;
+#pragma unroll 8
+            for (u32 s2 = 0; s2 < 64; ++s2) {
+                if (s2 >= t) break;
                 x ^= sh.piv2[s2] & (0ull - ((d >> s2) & 1ull));
             }
-            x ^= __shfl_xor_sync(0xffffffffu, x, 1);
-            x ^= __shfl_xor_sync(0xffffffffu, x, 2);
-            if (part == 0u && k < nwin1) sh.nraw[k] ^= x;
+            sh.nraw[k] = x;
         }
         named_bar(kBodyBar, nthr);
+        if (sh.super) {
+            // (b) super-step driver: word w+1 after panel a = pre ^ sum_s d_s
+            // piv2[s] with four lanes per slot, 16 pivots each, folded with two
+            // shuffles (every lane of a warp runs the same iterations: nthr and
+            // 4 * kWin are multiples of 32). Measured: 65536^2 67.49 -> 67.22
+            // ms; the single-panel driver keeps the one-lane loop above (its
+            // panel chain is shorter without the extra barrier: 4096^2 0.863
+            // vs 0.903 ms).
+            for (u32 g = threadIdx.x; g < 4u * kWin; g += nthr) {
+                const u32 k = g >> 2, part = g & 3u;
+                const u64 d = k < nwin1 ? sh.ndacc[k] : 0ull;
+                u64 x = 0ull;
+#pragma unroll
+                for (u32 i = 0; i < 16u; ++i) {
+                    const u32 s2 = 16u * part + i;  // (bits s2 >= t of d are zero)
+                    x ^= sh.piv2[s2] & (0ull - ((d >> s2) & 1ull));
+                }
+                x ^= __shfl_xor_sync(0xffffffffu, x, 1);
+                x ^= __shfl_xor_sync(0xffffffffu, x, 2);
+                if (part == 0u && k < nwin1) sh.nraw[k] ^= x;
+            }
+            named_bar(kBodyBar, nthr);
+        }
     }
     return t;
 }
@@ -1249,8 +1073,10 @@ __global__ void check_final_kernel(const u64* a, u32 m, u32 n, u32 Wp, u32 rank,
 }
 
 // Positions [lo, hi) (all >= r): multipliers, combination, compressed write.
-__device__ __forceinline__ void apply_rows(const Params& p, const ApplyShared& s, u32 w, u32 r,
-                                           u32 rb, u32 lo, u32 hi, u32 tid, u32 nthr) {
+// (Check: check mode's invariant test, compiled out of the normal path.)
+template <bool Check>
+__device__ __forceinline__ void apply_rows_t(const Params& p, const ApplyShared& s, u32 w, u32 r,
+                                             u32 rb, u32 lo, u32 hi, u32 tid, u32 nthr) {
     const u32 w0 = r >> 6, b0 = r & 63;
     for (u32 pos = lo + tid; pos < hi; pos += nthr) {
         u64 v = ldcg(p.pb + pos), a = 0, c = 0;
@@ -1268,7 +1094,7 @@ __device__ __forceinline__ void apply_rows(const Params& p, const ApplyShared& s
             c |= bit << k;
         }
         u64 epart = 0;
-        if (p.check) {
+        if constexpr (Check) {
             if (p.check_inject == w + 1u && off == rb) v ^= 1ull << 63;  // (the checker's own test)
             check_panel_word(p.check, w, v, tl, off < rb, s.q);
         }
@@ -1295,6 +1121,14 @@ __device__ __forceinline__ void apply_rows(const Params& p, const ApplyShared& s
             }
         }
     }
+}
+
+__device__ __forceinline__ void apply_rows(const Params& p, const ApplyShared& s, u32 w, u32 r, u32 rb,
+                                           u32 lo, u32 hi, u32 tid, u32 nthr) {
+    if (p.check)
+        apply_rows_t<true>(p, s, w, r, rb, lo, hi, tid, nthr);
+    else
+        apply_rows_t<false>(p, s, w, r, rb, lo, hi, tid, nthr);
 }
 
 // Raw pivot-row tails, tiles [(w+1)/8, Wpad8/8), into stage[(T*64 + t)*8 + k];

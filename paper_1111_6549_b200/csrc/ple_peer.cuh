@@ -93,9 +93,10 @@ __device__ __forceinline__ bool peer_wait(const PeerParams& s, const u32* ctr, u
 // rows, the compressed write (apply_rows with rows addressed locally and
 // positions looked up in inv). Rows already retired get d = 0; the smallest
 // row still active at step w+1 goes to lo[w+1].
-__device__ __forceinline__ void peer_apply_rows(const PeerParams& s, const ApplyShared& a, u32 w,
-                                                u32 r, u32 rb, const u64* pbw, ulonglong2* info,
-                                                u32 l0, u32 l1) {
+template <bool Check>
+__device__ __forceinline__ void peer_apply_rows_t(const PeerParams& s, const ApplyShared& a, u32 w,
+                                                  u32 r, u32 rb, const u64* pbw, ulonglong2* info,
+                                                  u32 l0, u32 l1) {
     const u32 w0 = r >> 6, b0 = r & 63;
     u32 lomin = 0xffffffffu;
     for (u32 l = l0 + threadIdx.x; l < l1; l += blockDim.x) {
@@ -119,7 +120,7 @@ __device__ __forceinline__ void peer_apply_rows(const PeerParams& s, const Apply
             c |= bit << k;
         }
         u64 epart = 0;
-        if (s.p.check) check_panel_word(s.p.check, w, v, tl, off < rb, a.q);
+        if constexpr (Check) check_panel_word(s.p.check, w, v, tl, off < rb, a.q);
         if (off < rb) {
             c |= 1ull << off;
             epart = v & ~low_mask64((int)a.q[off] + 1);
@@ -453,7 +454,10 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                 loaded = true;
             }
             const u32 l0 = lo + c * crow, l1 = min(s.m_loc, l0 + crow);
-            peer_apply_rows(s, ash, w, r, rb, pbw, info, l0, l1);
+            if (s.p.check)
+                peer_apply_rows_t<true>(s, ash, w, r, rb, pbw, info, l0, l1);
+            else
+                peer_apply_rows_t<false>(s, ash, w, r, rb, pbw, info, l0, l1);
             if (sweep) {
                 __syncthreads();
                 if (!la_ready) {

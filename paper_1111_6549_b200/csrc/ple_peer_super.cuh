@@ -29,7 +29,8 @@ __device__ __forceinline__ u64* stage4(u64* stage, u32 tile, u32 slot) {
 // apply2_rows (ple_super.cuh) on local rows [l0, l1): positions from inv,
 // records info[l] = {d~_a, d_b}, ipos[l] = position; lo[S+1] = the smallest
 // local row still active after the super-step.
-__device__ __forceinline__ void peer_apply2_rows(const PeerParams& s, const ApplyShared2& a, u32 S,
+template <bool Check>
+__device__ __forceinline__ void peer_apply2_rows_t(const PeerParams& s, const ApplyShared2& a, u32 S,
                                                  u32 r, u32 rba, u32 rbb, bool has_b,
                                                  const u64* pbw, const u64* pb2w, ulonglong2* info,
                                                  u32* ipos, u32 l0, u32 l1) {
@@ -57,7 +58,7 @@ __device__ __forceinline__ void peer_apply2_rows(const PeerParams& s, const Appl
             da ^= a.Da[k] & msk;
             c |= bit << k;
         }
-        if (s.p.check) check_panel_word(s.p.check, w, v, tla, off < rba, a.qa);
+        if constexpr (Check) check_panel_word(s.p.check, w, v, tla, off < rba, a.qa);
         if (off < rba) {
             c |= 1ull << off;
             epa = v & ~low_mask64((int)a.qa[off] + 1);
@@ -86,7 +87,7 @@ __device__ __forceinline__ void peer_apply2_rows(const PeerParams& s, const Appl
                     db ^= a.Db[k] & msk;
                     cb |= bit << k;
                 }
-                if (s.p.check) check_panel_word(s.p.check, w + 1u, v1, tlb, offb < rbb, a.qb);
+                if constexpr (Check) check_panel_word(s.p.check, w + 1u, v1, tlb, offb < rbb, a.qb);
                 if (offb < rbb) {
                     cb |= 1ull << offb;
                     epb = v1 & ~low_mask64((int)a.qb[offb] + 1);
@@ -438,8 +439,12 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                 loaded = true;
             }
             const u32 l0 = lo + c * crow, l1 = min(s.m_loc, l0 + crow);
-            peer_apply2_rows(s, ash, S, r, rba, rbb, has_b, s.peer[s.rank].pb[S & 1u],
-                             s.peer[s.rank].pb2[S & 1u], info, ipos, l0, l1);
+            if (s.p.check)
+                peer_apply2_rows_t<true>(s, ash, S, r, rba, rbb, has_b, s.peer[s.rank].pb[S & 1u],
+                                         s.peer[s.rank].pb2[S & 1u], info, ipos, l0, l1);
+            else
+                peer_apply2_rows_t<false>(s, ash, S, r, rba, rbb, has_b, s.peer[s.rank].pb[S & 1u],
+                                          s.peer[s.rank].pb2[S & 1u], info, ipos, l0, l1);
             if (sweep) {
                 __syncthreads();
                 if (!la_ready) {

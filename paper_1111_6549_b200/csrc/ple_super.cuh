@@ -168,9 +168,10 @@ __device__ __forceinline__ void compress_write(u64* mat, u32 m, u32 ph, u32 r0, 
 // info[pos] = {d~_a, d_b}, and the physical row in the u32 array that
 // follows the m records (info_phys): dense records keep the sweep's loads of
 // them at 2 + 1 L1 wavefronts per warp (the sweep is L1-bound).
-__device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2& s, u32 w, u32 r,
-                                            u32 rba, u32 rbb, bool has_b, u32 lo, u32 hi, u32 tid,
-                                            u32 nthr) {
+template <bool Check>
+__device__ __forceinline__ void apply2_rows_t(const Params& p, const ApplyShared2& s, u32 w, u32 r,
+                                              u32 rba, u32 rbb, bool has_b, u32 lo, u32 hi, u32 tid,
+                                              u32 nthr) {
     const u32 rb0 = r + rba;
     for (u32 pos = lo + tid; pos < hi; pos += nthr) {
         const u32 ph = ldcg(p.perm + pos);
@@ -189,7 +190,7 @@ __device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2&
             da ^= s.Da[k] & msk;
             c |= bit << k;
         }
-        if (p.check) {
+        if constexpr (Check) {
             if (p.check_inject == w + 1u && off == rba) v ^= 1ull << 63;  // (the checker's own test)
             check_panel_word(p.check, w, v, tla, off < rba, s.qa);
         }
@@ -222,7 +223,7 @@ __device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2&
                     db ^= s.Db[k] & msk;
                     cb |= bit << k;
                 }
-                if (p.check) check_panel_word(p.check, w + 1u, v1, tlb, offb < rbb, s.qb);
+                if constexpr (Check) check_panel_word(p.check, w + 1u, v1, tlb, offb < rbb, s.qb);
                 if (offb < rbb) {
                     cb |= 1ull << offb;
                     epb = v1 & ~low_mask64((int)s.qb[offb] + 1);
@@ -238,6 +239,14 @@ __device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2&
         p.info[pos] = make_ulonglong2(dta, db);
         info_phys(p.info, p.m)[pos] = ph;
     }
+}
+
+__device__ __forceinline__ void apply2_rows(const Params& p, const ApplyShared2& s, u32 w, u32 r, u32 rba,
+                                            u32 rbb, bool has_b, u32 lo, u32 hi, u32 tid, u32 nthr) {
+    if (p.check)
+        apply2_rows_t<true>(p, s, w, r, rba, rbb, has_b, lo, hi, tid, nthr);
+    else
+        apply2_rows_t<false>(p, s, w, r, rba, rbb, has_b, lo, hi, tid, nthr);
 }
 
 // 16 tables x 256 entries x 32 B. Table t (t < 8: panel a, byte t of d~_a;

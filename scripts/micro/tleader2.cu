@@ -5,6 +5,26 @@
 #include "ple_kernels.cuh"
 using namespace gf2cu;
 
+// (the transposed-leader helpers, removed from the product in round 2 after
+// measuring slower end to end; kept here with the micro-benchmark)
+__device__ __forceinline__ u32 transpose32(u32 x) {
+    const u32 lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int st = 4; st >= 0; --st) {
+        const u32 s = 1u << st;
+        const u32 m = st == 4 ? 0x0000FFFFu : st == 3 ? 0x00FF00FFu : st == 2 ? 0x0F0F0F0Fu
+                      : st == 1 ? 0x33333333u : 0x55555555u;
+        const u32 y = __shfl_xor_sync(0xffffffffu, x, (int)s);
+        x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+    }
+    return x;
+}
+
+__device__ __forceinline__ void mask_update(u32& M, u32 bitP, u32 tbit, u32 elim, u32 flip, u32 force) {
+    const bool bp = (M & bitP) != 0u, bt = (M & tbit) != 0u;
+    M ^= ((bp || force) ? elim : 0u) ^ ((bp != bt) ? flip : 0u);
+}
+
 template <int V>
 __device__ __forceinline__ void leader_v(u64& red, u64& acc, u32& org, int& t, int& j, int tend, u64* sE,
                                          u64* sD, u32* sq, u32* ssw) {
