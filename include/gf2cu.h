@@ -107,6 +107,11 @@ typedef struct {
                                    one panel per sweep; for the super-step driver
                                    sum over super-steps of 16*(m-r-rba-rbb)*(W-w-2)
                                    (one read + write per two panels)            */
+    size_t input_first_rows;    /* gf2cu_ple, streamed input: the factorization
+                                   started on this many leading rows ...        */
+    size_t input_first_steps;   /* ... and ran this many 128-column super-steps
+                                   on them while the other rows were uploaded
+                                   (0 / 0: the matrix was uploaded whole)       */
 } gf2cu_stats;
 
 /* Fills *cfg with the reference defaults (k=0, k_scale=0.75, table_count=4,

@@ -120,6 +120,14 @@ struct Workspace {
     gf2cu::PanelOut* pout_b = nullptr;  // super-step driver: panel b's outputs
     gf2cu::SuperOut* sout = nullptr;
     u32* check = nullptr;        // check mode: Params::check words
+    // streamed input (run_ple): upload stream and "row block arrived" events,
+    // the per-super-step panel outputs, phase A's verdict
+    cudaStream_t up = nullptr;
+    cudaEvent_t up_ev[2] = {nullptr, nullptr};
+    gf2cu::PanelOut* hist_a = nullptr;
+    gf2cu::PanelOut* hist_b = nullptr;
+    gf2cu::SuperOut* hist_so = nullptr;
+    u32* sin_abort = nullptr;
     std::vector<cudaEvent_t> ev;
 };
 
@@ -147,6 +155,13 @@ void free_ws(Workspace& w) {
     if (w.host_r) cudaFreeHost(w.host_r);
     if (w.out_host) cudaFreeHost(w.out_host);
     if (w.copy) cudaStreamDestroy(w.copy);
+    if (w.up) cudaStreamDestroy(w.up);
+    for (cudaEvent_t e : w.up_ev)
+        if (e) cudaEventDestroy(e);
+    cudaFree(w.hist_a);
+    cudaFree(w.hist_b);
+    cudaFree(w.hist_so);
+    cudaFree(w.sin_abort);
     for (cudaEvent_t e : w.ev) cudaEventDestroy(e);
     w = Workspace{};
 }
@@ -781,22 +796,69 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
     return st;
 }
 
+// Streamed input: the factorization starts on the first m0 rows (S1
+// super-steps, ple_super.cuh SuperRange) while the other rows are still
+// crossing PCIe. m0 = 0: not used for this shape.
+//   GF2CU_STREAM_IN=0 never, =1 whenever the shape allows it (tests); default:
+//   from 2^24 matrix words (128 MiB, 2.4 ms of upload) up.
+//   GF2CU_STREAM_IN_FRAC: first block's share of the rows (default 0.27: at
+//   65536^2 the super-steps on it take about as long as the rest's upload).
+struct StreamInPlan {
+    size_t m0 = 0;
+    u32 S1 = 0;
+};
+
+StreamInPlan stream_in_plan(size_t m, size_t W) {
+    StreamInPlan pl;
+    const char* e = std::getenv("GF2CU_STREAM_IN");
+    const int mode = e ? std::atoi(e) : -1;
+    if (mode == 0) return pl;
+    if (mode < 0 && (double)m * (double)W < 16777216.0) return pl;
+    const char* fe = std::getenv("GF2CU_STREAM_IN_FRAC");
+    const double f = fe ? std::min(0.9, std::max(0.01, std::atof(fe))) : 0.27;
+    const size_t nss = (W + 1) / 2;
+    size_t m0 = ((size_t)(f * (double)m) + 255) / 256 * 256;
+    // (every super-step of the first phase keeps a full window and a full
+    // next window among the first block's rows)
+    m0 = std::min(m0, 128 * (nss - 1) + 256);
+    if (m0 + 256 > m || m0 < 512) return pl;
+    const size_t S1 = std::min((m0 - 256) / 128, nss - 1);
+    if (S1 < (mode > 0 ? 1u : 16u)) return pl;
+    pl.m0 = m0;
+    pl.S1 = (u32)S1;
+    return pl;
+}
+
 // Launches the whole decomposition on `s`; outputs are copied to the host.
 // stream_to (an aligned host view of the matrix, may be null): with the
 // super-step driver, the rows the kernel finishes are copied into it while
 // the factorization runs; *rows_streamed = how many leading rows already
 // hold their final value there (the caller downloads the rest).
+// stream_from (an aligned host view, may be null): the input is still on the
+// host; this call uploads it -- in two row blocks with the factorization
+// started on the first one when the shape is worth it (StreamInPlan).
 gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_t* q,
                      size_t* rank, gf2cu_colswap* col_swaps, size_t* n_col_swaps,
                      gf2cu_stats* stats, const gf2cu_view* stream_to = nullptr,
-                     size_t* rows_streamed = nullptr) {
+                     size_t* rows_streamed = nullptr, const gf2cu_view* stream_from = nullptr) {
     if (rows_streamed) *rows_streamed = 0;
-    if (const unsigned pr = cfg ? (cfg->flags >> 16) & 15u : 0u)
+    cudaStream_t s = pick_stream(a, cfg ? cfg->stream : nullptr);
+    // (rows [lo, hi) of stream_from into the row-major device matrix)
+    auto upload_rows = [&](size_t lo, size_t hi, cudaStream_t on) -> gf2cu_status {
+        const uint64_t* host = stream_from->data + (stream_from->col_off >> 6);
+        return staged_h2d(a->data + lo * a->Wp, a->Wp * 8, host + lo * stream_from->stride,
+                          stream_from->stride * 8, a->W * 8, hi - lo, a->device, on);
+    };
+    if (const unsigned pr = cfg ? (cfg->flags >> 16) & 15u : 0u) {
+        if (stream_from) {
+            const gf2cu_status su = upload_rows(0, a->m, s);
+            if (su != GF2CU_OK) return su;
+        }
         return run_ple_peer(a, cfg, pr, swaps, q, rank, col_swaps, n_col_swaps, stats);
+    }
     gf2cu_status st = ensure_ws(a);
     if (st != GF2CU_OK) return st;
     Workspace& ws = a->ws;
-    cudaStream_t s = pick_stream(a, cfg ? cfg->stream : nullptr);
     const bool timing = cfg && (cfg->flags & GF2CU_FLAG_TIME_KERNELS);
     const size_t m = a->m, n = a->n, W = a->W;
 
@@ -868,6 +930,29 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     const bool super = !multi && !(fl & GF2CU_FLAG_SINGLE_PANEL) &&
                        ((fl & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= kSuperStepWords);
     const u32 Wpad4 = (u32)std::max<size_t>(4, (W + 3) / 4 * 4);
+    StreamInPlan sin;
+    if (stream_from && super && !timing) sin = stream_in_plan(m, W);
+    if (stream_from && !sin.m0) {
+        st = upload_rows(0, m, s);
+        if (st != GF2CU_OK) return st;
+    }
+    if (sin.m0) {
+        const size_t nss = (W + 1) / 2;
+        if (!ws.up) CU_TRY(cudaStreamCreateWithFlags(&ws.up, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : ws.up_ev)
+            if (!e) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        if (!ws.hist_a) CU_TRY(cudaMalloc(&ws.hist_a, nss * sizeof(gf2cu::PanelOut)));
+        if (!ws.hist_b) CU_TRY(cudaMalloc(&ws.hist_b, nss * sizeof(gf2cu::PanelOut)));
+        if (!ws.hist_so) CU_TRY(cudaMalloc(&ws.hist_so, nss * sizeof(gf2cu::SuperOut)));
+        if (!ws.sin_abort) CU_TRY(cudaMalloc(&ws.sin_abort, sizeof(u32)));
+        // the first block starts on its way now; what was enqueued on s so
+        // far (an earlier call's work on this matrix) stays ahead of it
+        CU_TRY(cudaEventRecord(ws.up_ev[0], s));
+        CU_TRY(cudaStreamWaitEvent(ws.up, ws.up_ev[0], 0));
+        st = upload_rows(0, sin.m0, ws.up);
+        if (st != GF2CU_OK) return st;
+        CU_TRY(cudaEventRecord(ws.up_ev[0], ws.up));
+    }
     if (!multi) {
         if (!ws.ubuf) {
             const size_t cap = std::max<size_t>(1, std::min(m, n));
@@ -926,8 +1011,10 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
     if (super) {
         p.Wpad8 = Wpad4;  // the super-step driver's tile width is 32 bytes
-        gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4);
-        gf2cu::ple_init4_kernel<<<sms * 4, 256, 0, s>>>(p, a->data, (u32)a->Wp);
+        if (sin.m0) CU_TRY(cudaStreamWaitEvent(s, ws.up_ev[0], 0));
+        const u32 hi = sin.m0 ? (u32)sin.m0 : (u32)m;
+        gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4, 0u, hi);
+        gf2cu::ple_init4_kernel<<<sms * 4, 256, 0, s>>>(p, a->data, (u32)a->Wp, 0u, hi);
     } else {
         gf2cu::tile_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, p.Wpad8);
         gf2cu::ple_init_kernel<<<sms * 4, 256, 0, s>>>(p);
@@ -961,10 +1048,48 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         }
         p.worker_ns = wns;
         if (super) {
-            u32 nss = (u32)((W + 1) / 2);
-            void* sargs[] = {&p, &ws.pout_b, &ws.sout, &nss};
-            CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_super_kernel, dim3(grid),
-                                               dim3(gf2cu::kTrailThreads), sargs, gf2cu::kTableBytes, s));
+            const u32 nss = (u32)((W + 1) / 2);
+            auto launch = [&](gf2cu::Params pp, gf2cu::PanelOut* pob, gf2cu::SuperOut* so,
+                              gf2cu::SuperRange rg) -> cudaError_t {
+                void* sargs[] = {&pp, &pob, &so, &rg};
+                return cudaLaunchCooperativeKernel((void*)gf2cu::ple_super_kernel, dim3(grid),
+                                                   dim3(gf2cu::kTrailThreads), sargs, gf2cu::kTableBytes, s);
+            };
+            if (!sin.m0) {
+                CU_TRY(launch(p, ws.pout_b, ws.sout, gf2cu::SuperRange{0u, nss, 0u, 0u, 0u, nullptr}));
+            } else {
+                // streamed input (ple_super.cuh, SuperRange): A on the first
+                // block while the second one uploads, B = the second block's
+                // replay of A's super-steps, C = the rest on all rows
+                const u32 S1 = sin.S1, m0 = (u32)sin.m0, nwk = (u32)grid - 1u;
+                CU_TRY(cudaMemsetAsync(ws.sin_abort, 0, sizeof(u32), s));
+                gf2cu::Params pa = p;
+                pa.pout = ws.hist_a;
+                pa.out = nullptr;
+                pa.out_host = nullptr;
+                gf2cu::Params pA = pa;
+                pA.mv = m0;
+                pA.partial = 1u;
+                CU_TRY(launch(pA, ws.hist_b, ws.hist_so, gf2cu::SuperRange{0u, S1, 0u, 0u, 1u, ws.sin_abort}));
+                st = upload_rows(m0, m, ws.up);
+                if (st != GF2CU_OK) return st;
+                CU_TRY(cudaEventRecord(ws.up_ev[1], ws.up));
+                CU_TRY(cudaStreamWaitEvent(s, ws.up_ev[1], 0));
+                gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4, m0, (u32)m);
+                gf2cu::ple_init4_kernel<<<sms * 4, 256, 0, s>>>(p, a->data, (u32)a->Wp, m0, (u32)m);
+                CU_TRY(cudaMemsetAsync(ws.apctr, 0, 2 * (W + 1) * sizeof(u32), s));
+                gf2cu::sync_preset_kernel<<<1, 1, 0, s>>>(ws.sync, S1, 0u, 0u, ws.sin_abort);
+                CU_TRY(launch(pa, ws.hist_b, ws.hist_so, gf2cu::SuperRange{0u, S1, m0, 1u, 1u, ws.sin_abort}));
+                CU_TRY(cudaMemsetAsync(ws.apctr, 0, 2 * (W + 1) * sizeof(u32), s));
+                // (the first output batch of C: the first multiple of kOutEvery >= S1)
+                const u32 sf = std::max(gf2cu::kOutEvery, (S1 + gf2cu::kOutEvery - 1) / gf2cu::kOutEvery * gf2cu::kOutEvery);
+                gf2cu::sync_preset_kernel<<<1, 1, 0, s>>>(ws.sync, S1, nwk * S1, nwk * (sf / gf2cu::kOutEvery - 1u),
+                                                          ws.sin_abort);
+                gf2cu::Params pC = p;
+                pC.pout = ws.hist_a;
+                CU_TRY(launch(pC, ws.hist_b, ws.hist_so, gf2cu::SuperRange{S1, nss, 0u, 0u, 1u, ws.sin_abort}));
+                CU_TRY(cudaGetLastError());
+            }
         } else {
             CU_TRY(cudaLaunchCooperativeKernel((void*)gf2cu::ple_persistent_kernel, dim3(grid),
                                                dim3(gf2cu::kTrailThreads), args, gf2cu::kTableBytes, s));
@@ -1013,8 +1138,18 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
             CU_TRY(cudaStreamSynchronize(ws.copy));
         }
         gf2cu::SyncState sy{};
+        u32 gave_up = 0;
         CU_TRY(cudaMemcpyAsync(&sy, ws.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
+        if (sin.m0) CU_TRY(cudaMemcpyAsync(&gave_up, ws.sin_abort, sizeof(u32), cudaMemcpyDeviceToHost, s));
         CU_TRY(cudaStreamSynchronize(s));
+        if (gave_up == 2u) return fail(GF2CU_ECUDA, "persistent PLE kernel watchdog tripped (streamed input)");
+        if (gave_up) {
+            // a column had no pivot among the first block's rows: the whole
+            // matrix decides. Nothing was written to a->data or to the host
+            // view (the first phases produce no output), and the upload is
+            // complete: factor it the ordinary way.
+            return run_ple(a, cfg, swaps, q, rank, col_swaps, n_col_swaps, stats, stream_to, rows_streamed, nullptr);
+        }
         if (wns) {
             std::vector<u64> h(wn_words);
             cudaMemcpy(h.data(), wns, wn_words * sizeof(u64), cudaMemcpyDeviceToHost);
@@ -1139,6 +1274,8 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         stats->trailing_launches = launches;
         stats->kernel_ms = kernel_ms;
         stats->driver = multi ? 0 : super ? 2 : 1;
+        stats->input_first_rows = sin.m0;
+        stats->input_first_steps = sin.m0 ? sin.S1 : 0;
         if (timing && !multi) {
             std::vector<u64> ph(8 * steps);
             CU_TRY(cudaMemcpy(ph.data(), ws.phase_ns, ph.size() * sizeof(u64), cudaMemcpyDeviceToHost));
@@ -1431,9 +1568,11 @@ gf2cu_status view_download(const gf2cu_view* v, const gf2cu_matrix* a, cudaStrea
 
 // Host view <-> the cached device matrix of its shape: upload,
 // body(matrix, cfg), download.
+// (body_uploads: the body copies the view's rows to the device itself)
 template <class Body>
 gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* stats, Body&& body,
-                       size_t* rows_done = nullptr, const size_t* rows_limit = nullptr) {
+                       size_t* rows_done = nullptr, const size_t* rows_limit = nullptr,
+                       bool body_uploads = false) {
     gf2cu_cfg c;
     gf2cu_default_config(&c);
     if (cfg) c = *cfg;
@@ -1443,8 +1582,10 @@ gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* s
     DeviceGuard g(c.device);
     cudaStream_t s = pick_stream(a, c.stream);
     std::vector<u64> packed;
-    st = view_upload(v, a, s, packed);
-    if (st != GF2CU_OK) return st;
+    if (!body_uploads) {
+        st = view_upload(v, a, s, packed);
+        if (st != GF2CU_OK) return st;
+    }
     c.stream = s;
     st = body(a, c);
     if (st == GF2CU_OK) {
@@ -1842,15 +1983,16 @@ gf2cu_status gf2cu_ple(const gf2cu_view* v, const gf2cu_cfg* cfg, size_t* swaps,
         if (stats) std::memset(stats, 0, sizeof(*stats));
         return GF2CU_OK;
     }
-    // aligned views receive the finished rows while the kernel runs
+    // aligned views receive the finished rows while the kernel runs, and
+    // (large ones) are factored while their rows are still arriving
     size_t streamed = 0;
     const gf2cu_view* to = view_aligned(v) ? v : nullptr;
     return with_view(
         v, cfg, stats,
         [&](gf2cu_matrix* a, const gf2cu_cfg& c) {
-            return run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats, to, &streamed);
+            return run_ple(a, &c, swaps, q, rank, col_swaps, n_col_swaps, stats, to, &streamed, to);
         },
-        &streamed);
+        &streamed, nullptr, to != nullptr);
 }
 
 gf2cu_status gf2cu_matrix_mul(gf2cu_matrix* c, const gf2cu_matrix* a, const gf2cu_matrix* b,

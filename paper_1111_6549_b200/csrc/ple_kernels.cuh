@@ -114,7 +114,16 @@ struct Params {
     // first bad final row, final violations}, see check_panel_word
     u32* check;
     u32 check_inject;  // test hook (check mode): step + 1 whose first non-pivot row is corrupted
+    // streamed input (super-step driver, ple_super.cuh SuperRange): positions
+    // >= mv are not on the device yet (0 = all m rows are); partial = 1: a
+    // column with no pivot among the visible rows aborts the panel (a row still
+    // on its way might hold one)
+    u32 mv;
+    u32 partial;
 };
+
+// Row positions the step may look at (Params::mv).
+__device__ __forceinline__ u32 vis_rows(const Params& p) { return p.mv ? p.mv : p.m; }
 
 // Params::pflags: the window warps behind the leader apply its pivots as it
 // publishes them (instead of all at the epoch's closing barrier).
@@ -410,6 +419,7 @@ struct LookAhead {
     u64* piv2_out = nullptr;  // panel a: its pivot rows' pre-super-step word w+1
     u64* C_out = nullptr;     // panel b: panel-a combination of each of its pivot rows
     bool sys = false;         // cap_ctr is signalled by other GPUs (system-scope acquire)
+    PanelOut* pout = nullptr; // where E / D / qb go instead of Params::pout (per-step history)
 };
 
 // All `nthr` threads: scan positions r + [nwin, nrem) reducing each raw panel
@@ -520,13 +530,15 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         named_bar(kBodyBar, nthr);
     }
     const u32 r = sh.r;
+    const u32 M = vis_rows(p);
+    PanelOut* const pout = (la && la->pout) ? la->pout : p.pout;
     if (threadIdx.x == 0) {
         p.state->r = r;
         p.state->rb = 0;
         p.rhist[w] = r;
         p.rbhist[w] = 0;
     }
-    if (r >= p.m) {
+    if (r >= M) {
         if (threadIdx.x == 0 && p.host_r) {
             *p.host_r = r;
             __threadfence_system();
@@ -539,7 +551,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         named_bar(kBodyBar, nthr);
         return 0;
     }
-    const u32 nrem = p.m - r;
+    const u32 nrem = M - r;
     const u32 nwin = nrem < (u32)kWin ? nrem : (u32)kWin;
     const int jmax = (int)min(64u, p.n - 64u * w);
 
@@ -640,8 +652,8 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 org = mv ? tro : org;
             } else {
                 // ---- window miss: the remaining rows decide ----
-                if (j < out_next) return 0;  // no row outside has this column
-                if (p.window_only) {
+                if (j < out_next && !p.partial) return 0;  // no row outside has this column
+                if (p.window_only || (p.partial && j < out_next)) {
                     // sharded driver: the host gathers the whole panel column
                     // and runs the step again (nothing global was written)
                     aborted = true;
@@ -660,12 +672,15 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                 named_bar(1, nthr);
                 panel_scan(p, sh, r, nwin, nrem, nthr);
                 const u64 best = sh.best;
-                if (best == ~0ull) {
-                    out_next = 64;
+                out_next = best == ~0ull ? 64 : (int)(best >> 32);
+                if (out_next != j) {
+                    // column j has no pivot among the rows on the device
+                    if (p.partial) {
+                        aborted = true;
+                        return 2;
+                    }
                     return 0;
                 }
-                out_next = (int)(best >> 32);
-                if (out_next != j) return 0;  // column j has no pivot anywhere
                 // pivot from outside the window: it takes position t; the
                 // window row t moves to the pivot's old position P
                 P = (u32)(best & 0xffffffffu);
@@ -824,7 +839,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         if (la && !aborted && sh.super != 2 && w + 1 < p.W) {
             if (!sh.super && inwin) f_pb2 = ldcg(p.pb2 + r + me);
             const u32 qe = r + nwin + me;
-            if (me < 64u && qe < p.m) {
+            if (me < 64u && qe < M) {
                 f_epb = ldcg(p.pb + qe);
                 f_epb2 = ldcg(p.pb2 + qe);
                 f_eph = ldcg(p.perm + qe);
@@ -889,9 +904,9 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         }
     }
     for (u32 k = threadIdx.x; k < t; k += nthr) {
-        p.pout->E[k] = sh.E[k];
-        p.pout->D[k] = sh.D[k];
-        p.pout->qb[k] = sh.q[k];
+        pout->E[k] = sh.E[k];
+        pout->D[k] = sh.D[k];
+        pout->qb[k] = sh.q[k];
         p.swaps[r + k] = r + sh.sw[k];
         p.qcol[r + k] = 64u * w + sh.q[k];
     }
@@ -920,13 +935,13 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         }
         if (threadIdx.x == 0) sh.rba = t;
     }
-    if (la && sh.super != 2 && w + 1 < p.W && (r + t < p.m || sh.super == 1)) {
+    if (la && sh.super != 2 && w + 1 < p.W && (r + t < M || sh.super == 1)) {
         // ---- next window: word w+1 after step w, for positions
         //      [r + t, r + t + 128), from the pre-step capture pb2 (the
         //      super-step driver needs the pivot rows' word w+1 even when no
         //      row is left for a next window) ----
         const u32 r1 = r + t;
-        const u32 nwin1 = r1 < p.m ? min((u32)kWin, p.m - r1) : 0u;
+        const u32 nwin1 = r1 < M ? min((u32)kWin, M - r1) : 0u;
         // pre-step word w+1 of each pivot row
         // (super-step driver: pb2 was permuted by the writeback; the window
         // rows' pre-super-step words are in shared memory)

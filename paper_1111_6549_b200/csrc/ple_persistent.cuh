@@ -54,8 +54,8 @@ __device__ __forceinline__ void signal_step(PanelShared& sh, int nbody, u32 w, b
     if (threadIdx.x == 0) st_release_cta(&sh.sig_step, (int)((w + 1u) | (last ? 0x80000000u : 0u)));
 }
 
-__device__ __noinline__ void signal_loop(PanelShared& sh, SyncState* sy, u32 nsteps) {
-    for (u32 w = 0; w < nsteps; ++w) {
+__device__ __noinline__ void signal_loop(PanelShared& sh, SyncState* sy, u32 nsteps, u32 first = 0u) {
+    for (u32 w = first; w < nsteps; ++w) {
         const u64 t0 = globaltimer();
         u32 st;
         for (u32 spin = 0;; ++spin) {

@@ -45,13 +45,15 @@ __device__ __forceinline__ const u32* info_phys(const ulonglong2* info, u32 m) {
 }
 
 // row-major (stride Wp) -> 32-byte tiles (Wpad4 words per row)
+// (rows [row_lo, row_hi) only: streamed input tiles the row blocks as they arrive)
 __global__ void tile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst, u32 m, u32 Wp,
-                             u32 Wpad4) {
+                             u32 Wpad4, u32 row_lo = 0u, u32 row_hi = 0xffffffffu) {
     const u32 per_row = Wpad4 >> 1;
-    const u64 total = (u64)m * per_row;
+    row_hi = min(row_hi, m);
+    const u64 total = (u64)(row_hi - row_lo) * per_row;
     for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (u64)gridDim.x * blockDim.x) {
-        const u32 row = (u32)(e / per_row), x = 2u * (u32)(e - (u64)row * per_row);
+        const u32 rr = (u32)(e / per_row), row = row_lo + rr, x = 2u * (u32)(e - (u64)rr * per_row);
         *reinterpret_cast<ulonglong2*>(tw4(dst, m, row, x)) =
             *reinterpret_cast<const ulonglong2*>(src + (size_t)row * Wp + x);
     }
@@ -103,14 +105,16 @@ __device__ __forceinline__ void out_rows4(const Params& p, u32 lo, u32 hi, u32 p
 
 // Initial state of the super-step driver: identity order, pb / pb2 = words
 // 0 / 1 of every row (read from the row-major input).
-__global__ void ple_init4_kernel(Params p, const u64* __restrict__ rowmajor, u32 Wp) {
+__global__ void ple_init4_kernel(Params p, const u64* __restrict__ rowmajor, u32 Wp, u32 row_lo = 0u,
+                                 u32 row_hi = 0xffffffffu) {
     const u32 stride = gridDim.x * blockDim.x;
-    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
+    row_hi = min(row_hi, p.m);
+    for (u32 i = row_lo + blockIdx.x * blockDim.x + threadIdx.x; i < row_hi; i += stride) {
         p.perm[i] = i;
         p.pb[i] = rowmajor[(size_t)i * Wp];
         if (p.W > 1) p.pb2[i] = rowmajor[(size_t)i * Wp + 1];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (row_lo == 0u && blockIdx.x == 0 && threadIdx.x == 0) {
         p.state->r = 0;
         p.state->rb = 0;
     }
@@ -456,7 +460,7 @@ __device__ __forceinline__ void wstamp(const Params& p, u32 S, u32 wk, u32 nwork
 __device__ __forceinline__ bool super_la_gather(const Params& p, PanelShared& sh, u32 w, u32 r_a, u32 rba,
                                                 u32 r_b, u32 nwin_b, u32 rbb, int nthr) {
     const u32 r2 = r_b + rbb;
-    const u32 nwin2 = min((u32)kWin, p.m - r2);
+    const u32 nwin2 = min((u32)kWin, vis_rows(p) - r2);
     const bool has3 = w + 3u < p.W;
     for (u32 k = threadIdx.x; k < nwin2; k += nthr) {
         const u32 q = r2 + k, slot = q - r_b;
@@ -500,7 +504,7 @@ __device__ __forceinline__ bool super_la_gather(const Params& p, PanelShared& sh
 __device__ __forceinline__ void super_la_compute(const Params& p, PanelShared& sh, u32 rba, u32 r_b,
                                                  u32 rbb, int nthr) {
     const u32 r2 = r_b + rbb;
-    const u32 nwin2 = min((u32)kWin, p.m - r2);
+    const u32 nwin2 = min((u32)kWin, vis_rows(p) - r2);
     for (u32 k = threadIdx.x; k < nwin2; k += nthr) {
         u64 da, db;
         if (sh.la_ent[k]) {
@@ -540,10 +544,48 @@ __device__ __forceinline__ void super_la_compute(const Params& p, PanelShared& s
     named_bar(kBodyBar, nthr);
 }
 
-// One launch, grid = #SMs: CTA 0 runs the panels, CTAs 1.. the sweep. `nss` =
-// number of super-steps (ceil(W / 2)). panel_done counts published super-steps.
+// Streamed input (gf2cu.cu, run_ple): the factorization of a host matrix as
+// three launches of ple_super_kernel, so that it starts on the first row
+// block while the rest is still on its way over PCIe.
+//   A  super-steps [0, S1) on the rows that have arrived (Params::mv = m0,
+//      partial = 1): pivots, swaps and updates are the complete
+//      factorization's as long as every column finds its pivot among those
+//      rows (the first row with a 1, ple.hpp:88-93, is then one of them); a
+//      column that does not sets *abort and the host starts over with the
+//      whole matrix.
+//   B  replay = 1: the rows [m0, m) catch up on the same super-steps. The
+//      panels are A's, from the per-super-step history (hist = 1: pout[S],
+//      pout_b[S], so[S], rhist, perm); a late row is never a pivot row of
+//      these steps, so this is the workers' part alone (apply, sweep,
+//      capture) on row positions >= row_lo. Their tables come from the pivot
+//      rows' in-matrix copies, which keep their pre-step tails (the swept
+//      tails are in ubuf).
+//   C  super-steps [S1, nss) on all rows, as usual.
+// The host presets the cumulative counters between the launches
+// (sync_preset_kernel): panel_done = s_begin (B: s_end), t_count = nworkers *
+// s_begin, out_count for the first output batch.
+struct SuperRange {
+    u32 s_begin, s_end;  // super-steps [s_begin, s_end) of this launch
+    u32 row_lo;          // the workers' rows start at max(r, row_lo)
+    u32 replay;          // 1: no panel CTA, panels from the history
+    u32 hist;            // 1: panel outputs indexed by super-step
+    u32* abort;          // phase A's verdict (null without streamed input)
+};
+
+// (a watchdog error of the previous launch turns the later ones into no-ops)
+__global__ void sync_preset_kernel(SyncState* sy, u32 panel_done, u32 t_count, u32 out_count, u32* abort) {
+    if (sy->error == 1u) *abort = 2u;
+    *sy = SyncState{};
+    sy->panel_done = panel_done;
+    sy->t_count = t_count;
+    sy->out_count = out_count;
+}
+
+// One launch, grid = #SMs: CTA 0 runs the panels, CTAs 1.. the sweep.
+// rg.s_end = number of super-steps (ceil(W / 2)) unless the input is streamed.
+// panel_done counts published super-steps.
 __global__ void __launch_bounds__(kTrailThreads, 1)
-    ple_super_kernel(Params p, PanelOut* pout_b, SuperOut* so, u32 nss) {
+    ple_super_kernel(Params p, PanelOut* pout_b, SuperOut* so, SuperRange rg) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ PanelShared psh;
     __shared__ ApplyShared2 ash;
@@ -551,10 +593,13 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
     __shared__ u32 s_pa[64], s_pb[64];
     SyncState* sy = p.sync;
     const u32 nworkers = gridDim.x - 1;
+    const u32 M = vis_rows(p);
+    if (rg.abort && ldcg(rg.abort)) return;  // streamed input: phase A gave up
 
     if (blockIdx.x == 0) {
         // ------------------------------------------------------ panel CTA
         // (the last warp only signals; see signal_step)
+        if (rg.replay) return;
         const int nbody = (int)blockDim.x - 32;
         if (threadIdx.x == 0) {
             psh.sig_step = 0;
@@ -562,56 +607,74 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         }
         __syncthreads();
         if ((int)threadIdx.x >= nbody) {
-            if (threadIdx.x == (u32)nbody) signal_loop(psh, sy, nss);
+            if (threadIdx.x == (u32)nbody) signal_loop(psh, sy, rg.s_end, rg.s_begin);
             return;
         }
-        LookAhead la{0u, false, p.ap_done, 0u, &sy->error};
-        la.piv2_out = so->piv2;
-        la.C_out = so->C;
-        Params pb_par = p;
-        pb_par.pout = pout_b;
-        u32 prev_r = 0u;
+        // (a launch that starts at s_begin > 0 continues from the previous
+        // launch's rank; its capture is complete)
+        const u32 r_begin =
+            rg.s_begin ? ldcg(p.rhist + 2u * rg.s_begin - 1u) + ldcg(p.rbhist + 2u * rg.s_begin - 1u) : 0u;
+        LookAhead la{r_begin, false, p.ap_done, 0u, &sy->error};
+        u32 prev_r = r_begin;
         bool la_next = false;  // panel a's window came from the look-ahead
         const bool la_on = (p.pflags & kPanelSuperLA) != 0u;
-        for (u32 S = 0; S < nss; ++S) {
+        // streamed input, phase A: a column without a pivot among the rows on
+        // the device ends the attempt (every CTA leaves through the error word)
+        auto gave_up = [&]() -> bool {
+            if (!p.partial || psh.t >= 0) return false;
+            if (threadIdx.x == 0) {
+                *rg.abort = 1u;
+                __threadfence();
+                atomicExch(&sy->error, 2u);
+            }
+            return true;
+        };
+        for (u32 S = rg.s_begin; S < rg.s_end; ++S) {
             const u32 w = 2u * S;
+            const u32 hi = rg.hist ? S : 0u;  // this super-step's panel outputs
+            la.piv2_out = so[hi].piv2;
+            la.C_out = so[hi].C;
             // nothing left: publish an empty super-step so the workers stop
-            const bool done0 = la.r >= p.m;
+            const bool done0 = la.r >= M;
             // panel a: its window and scans read the previous super-step's
             // capture (all of its pre-work chunks) -- the window only without
             // the look-ahead across super-steps
             la.cap_ctr = p.ap_done + (S > 0 ? S - 1 : 0);
-            la.cap_target = S > 0 ? pw_chunks(p.m - prev_r, p.pw_div) : 0u;
+            la.cap_target = S > rg.s_begin ? pw_chunks(M - prev_r, p.pw_div) : 0u;
             prev_r = la.r;
             la.super_mode = 1;
             la.have_window = la_next;
+            la.pout = p.pout + hi;
             la_next = false;
             const u32 r_a = la.r;
             stamp2(p, w, 0);
             const u32 rba = panel_factor_body(p, w, psh, nbody, &la);
+            if (gave_up()) return;
             // (an aborted panel returns 0: then check the error word itself)
             if (*(volatile int*)&psh.sig_err || (rba == 0u && *(volatile u32*)&sy->error)) return;
             la.r += rba;
             if (w + 1u < p.W) {
-                if (!done0 && la.r < p.m) {
+                if (!done0 && la.r < M) {
                     // panel b: window = word w+1 after panel a (panel a's
                     // look-ahead); nothing to wait for
                     la.super_mode = 2;
                     la.have_window = true;
                     la.cap_target = 0u;
-                    const u32 rbb = panel_factor_body(pb_par, w + 1u, psh, nbody, &la);
+                    la.pout = pout_b + hi;
+                    const u32 rbb = panel_factor_body(p, w + 1u, psh, nbody, &la);
+                    if (gave_up()) return;
                     if (*(volatile int*)&psh.sig_err || (rbb == 0u && *(volatile u32*)&sy->error)) return;
                     la.r += rbb;
                     // look-ahead across super-steps, only while the workers
                     // are already through S-1 (the panel chain is the
                     // bottleneck; S-1 has also finished the tile holding
                     // words w+2, w+3 everywhere)
-                    if (la_on && w + 2u < p.W && la.r < p.m) {
+                    if (la_on && w + 2u < p.W && la.r < M) {
                         if (threadIdx.x == 0) psh.la_go = ld_acquire(&sy->t_count) >= nworkers * S ? 1 : 0;
                         named_bar(kBodyBar, nbody);
                         if (psh.la_go) {
                             const u32 r_b = r_a + rba;
-                            la_next = super_la_gather(p, psh, w, r_a, rba, r_b, min((u32)kWin, p.m - r_b),
+                            la_next = super_la_gather(p, psh, w, r_a, rba, r_b, min((u32)kWin, M - r_b),
                                                       rbb, nbody);
                         }
                     }
@@ -630,18 +693,20 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
 
     // ---------------------------------------------------------- workers
     const u32 wk = blockIdx.x - 1;
-    for (u32 S = 0; S < nss; ++S) {
+    for (u32 S = rg.s_begin; S < rg.s_end; ++S) {
         if (!cta_wait(sy, &sy->panel_done, S + 1, s_ok)) return;
         // the first pre-work claim now: its latency overlaps the loads below
         if (threadIdx.x == 0) s_claim = atomicAdd(&p.ap_claim[S], 1u);
         const u32 w = 2u * S;
+        const u32 hi = rg.hist ? S : 0u;  // this super-step's panel outputs
         const bool has_b = w + 1u < p.W;
         const u32 r = *(volatile u32*)&p.rhist[w], rba = *(volatile u32*)&p.rbhist[w];
-        if (r >= p.m) return;
+        if (r >= M) return;
         const u32 rbb = has_b ? *(volatile u32*)&p.rbhist[w + 1u] : 0u;
         Params q = p;
         q.info = p.info + (size_t)(S & 1u) * 2u * p.m;
-        const u32 nrows = p.m - r;
+        const u32 lo = max(r, rg.row_lo);  // (replay: the late rows only)
+        const u32 nrows = M - lo;
         const bool sweep = w + 2u < p.W;
         const u32 ct = (w + 2u) >> 2;  // look-ahead tile (words w+2, w+3)
         const u32 crow = pw_rows(nrows, p.pw_div), nch = pw_chunks(nrows, p.pw_div);
@@ -670,11 +735,11 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             if (c >= nch) break;
             const bool build = sweep && rba + rbb > 0 && !built;
             if (!loaded) {  // the panel outputs stay S's while any chunk of S is open
-                apply2_load(p, p.pout, pout_b, so, ash, rba, rbb);
+                apply2_load(p, p.pout + hi, pout_b + hi, so + hi, ash, rba, rbb);
                 __syncthreads();
                 loaded = true;
             }
-            const u32 a0 = r + c * crow, a1 = min(p.m, a0 + crow);
+            const u32 a0 = lo + c * crow, a1 = min(M, a0 + crow);
             apply2_rows(q, ash, w, r, rba, rbb, has_b, a0, a1, threadIdx.x, blockDim.x);
             if (sweep) {
                 __syncthreads();
@@ -699,12 +764,15 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         __syncthreads();
         if (!s_ok) return;
         if (p.out && S > 0 && S % kOutEvery == 0u) {
+            // (the first batch of a launch that did not start the factorization
+            // also covers the rows finished before it)
+            const u32 out_lo = S < rg.s_begin + kOutEvery ? 0u : *(volatile u32*)&p.rhist[w - 2u * kOutEvery];
             // S-1 is finished everywhere: the pivot rows of the last kOutEvery
             // super-steps are final; write them out row-major and tell the
             // host (which copies them while the factorization goes on). In
             // batches, so that the fence before the count is paid every
             // kOutEvery super-steps only.
-            out_rows4(p, *(volatile u32*)&p.rhist[w - 2u * kOutEvery], r, wk, nworkers);
+            out_rows4(p, out_lo, r, wk, nworkers);
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();
@@ -723,8 +791,9 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             const u64 end = total * (wk + 1) / nworkers;
             while (u < end) {
                 const u32 tile = ct + 1 + (u32)(u / nrows);
-                const u32 row0 = (u32)(u % nrows);
-                const u32 cnt = (u32)min((u64)(nrows - row0), end - u);
+                const u32 rr = (u32)(u % nrows);
+                const u32 row0 = rr + (lo - r);  // offset from r
+                const u32 cnt = (u32)min((u64)(nrows - rr), end - u);
                 if (rba + rbb > 0) {
                     __syncthreads();
                     build16(q, smem, tile, w, s_pa, rba, s_pb, rbb);
