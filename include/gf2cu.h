@@ -109,9 +109,10 @@ typedef struct {
                                    (one read + write per two panels)            */
     size_t input_first_rows;    /* gf2cu_ple, streamed input: the factorization
                                    started on this many leading rows ...        */
-    size_t input_first_steps;   /* ... and ran this many 128-column super-steps
-                                   on them while the other rows were uploaded
+    size_t input_first_steps;   /* ... and this many 128-column super-steps had
+                                   run when the last row block joined
                                    (0 / 0: the matrix was uploaded whole)       */
+    size_t input_blocks;        /* row blocks the upload was cut into (0: whole) */
 } gf2cu_stats;
 
 /* Fills *cfg with the reference defaults (k=0, k_scale=0.75, table_count=4,

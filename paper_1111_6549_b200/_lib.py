@@ -78,7 +78,8 @@ class gf2cu_stats(C.Structure):
                 ("trailing_ms", C.c_double), ("panel_ms", C.c_double), ("coef_ms", C.c_double),
                 ("alg_bytes", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
                 ("kernel_ms", C.c_double), ("driver", C.c_int), ("sweep_bytes", C.c_double),
-                ("input_first_rows", C.c_size_t), ("input_first_steps", C.c_size_t)]
+                ("input_first_rows", C.c_size_t), ("input_first_steps", C.c_size_t),
+                ("input_blocks", C.c_size_t)]
 
 
 FLAG_TIME_KERNELS = 1

@@ -123,7 +123,7 @@ struct Workspace {
     // streamed input (run_ple): upload stream and "row block arrived" events,
     // the per-super-step panel outputs, phase A's verdict
     cudaStream_t up = nullptr;
-    cudaEvent_t up_ev[2] = {nullptr, nullptr};
+    cudaEvent_t up_ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     gf2cu::PanelOut* hist_a = nullptr;
     gf2cu::PanelOut* hist_b = nullptr;
     gf2cu::SuperOut* hist_so = nullptr;
@@ -306,6 +306,54 @@ struct Staging {
     ~Staging() { release(); }
 };
 thread_local Staging g_staging;
+
+// GF2CU_TRACE=1 (diagnostic): host timestamps and stream events of one
+// drop-in call, printed to stderr in ms since the call began.
+struct Trace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0;
+    cudaEvent_t base = nullptr;
+    std::vector<std::pair<std::string, double>> host;
+    std::vector<std::pair<std::string, cudaEvent_t>> gpu;
+};
+thread_local Trace g_trace;
+
+void trace_begin(cudaStream_t s) {
+    const char* e = std::getenv("GF2CU_TRACE");
+    g_trace.on = e && std::atoi(e) > 0;
+    if (!g_trace.on) return;
+    g_trace.host.clear();
+    g_trace.gpu.clear();
+    cudaStreamSynchronize(s);
+    cudaEventCreate(&g_trace.base);
+    g_trace.t0 = std::chrono::steady_clock::now();
+    cudaEventRecord(g_trace.base, s);
+}
+void trace_host(const char* what) {
+    if (!g_trace.on) return;
+    g_trace.host.emplace_back(what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - g_trace.t0).count());
+}
+void trace_gpu(const std::string& what, cudaStream_t s) {
+    if (!g_trace.on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    g_trace.gpu.emplace_back(what, e);
+}
+void trace_end() {
+    if (!g_trace.on) return;
+    trace_host("return");
+    cudaDeviceSynchronize();
+    for (auto& h : g_trace.host) std::fprintf(stderr, "[trace host] %8.3f  %s\n", h.second, h.first.c_str());
+    for (auto& g : g_trace.gpu) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g_trace.base, g.second);
+        std::fprintf(stderr, "[trace gpu ] %8.3f  %s\n", ms, g.first.c_str());
+        cudaEventDestroy(g.second);
+    }
+    cudaEventDestroy(g_trace.base);
+    g_trace.on = false;
+}
 
 constexpr size_t kStageMin = size_t(8) << 20;  // smaller copies: the runtime's path
 
@@ -796,36 +844,107 @@ gf2cu_status run_ple_peer(gf2cu_matrix* a, const gf2cu_cfg* cfg, unsigned G, siz
     return st;
 }
 
-// Streamed input: the factorization starts on the first m0 rows (S1
-// super-steps, ple_super.cuh SuperRange) while the other rows are still
-// crossing PCIe. m0 = 0: not used for this shape.
-//   GF2CU_STREAM_IN=0 never, =1 whenever the shape allows it (tests); default:
-//   from 2^24 matrix words (128 MiB, 2.4 ms of upload) up.
-//   GF2CU_STREAM_IN_FRAC: first block's share of the rows (default 0.27: at
-//   65536^2 the super-steps on it take about as long as the rest's upload).
+// Streamed input: the factorization starts on the first row block while the
+// others are still crossing PCIe (ple_super.cuh, SuperRange). The rows arrive
+// in K blocks with boundaries rows[0] < ... < rows[K-1] = m; steps[k] = the
+// number of super-steps already done when block k joins (steps[0] = 0):
+//   A_k  super-steps [steps[k], steps[k+1]) on the rows [0, rows[k]), k < K-1
+//   B_k  the rows [rows[k-1], rows[k]) replay the super-steps [0, steps[k])
+//   C    super-steps [steps[K-1], nss) on all rows
+// in the order A_0, B_1, A_1, ..., B_{K-1}, C. The blocks grow geometrically,
+// so the first one is there after a fraction of a millisecond and a late block
+// replays few super-steps; steps[] comes from a time model (A_k runs until
+// block k+1 is expected) -- a wrong estimate only costs idle time or a longer
+// replay, never correctness. Empty plan: the matrix is uploaded whole.
+//   GF2CU_STREAM_IN=0 never, =1 whenever the shape allows it (tests; every A_k
+//   then runs as many super-steps as its rows allow); default: from 2^24 matrix
+//   words (128 MiB, 2.4 ms of upload) up.
+//   GF2CU_STREAM_IN_BLOCKS=f0,f1,..: the blocks' cumulative shares of the rows
+//   (default 1/16, 3/16, 7/16); GF2CU_STREAM_IN_FRAC=f: one first block of that
+//   share; GF2CU_STREAM_IN_STEPS=T1,T2,..: steps[1..] instead of the model's.
 struct StreamInPlan {
-    size_t m0 = 0;
-    u32 S1 = 0;
+    std::vector<size_t> rows;
+    std::vector<u32> steps;
+    size_t m0() const { return rows.empty() ? 0 : rows[0]; }
 };
 
-StreamInPlan stream_in_plan(size_t m, size_t W) {
+std::vector<double> env_list(const char* name) {
+    std::vector<double> v;
+    if (const char* e = std::getenv(name)) {
+        const char* c = e;
+        while (*c) {
+            char* end = nullptr;
+            const double x = std::strtod(c, &end);
+            if (end == c) break;
+            v.push_back(x);
+            c = end;
+            while (*c == ',' || *c == ' ') ++c;
+        }
+    }
+    return v;
+}
+
+StreamInPlan stream_in_plan(size_t m, size_t W, bool pageable) {
     StreamInPlan pl;
     const char* e = std::getenv("GF2CU_STREAM_IN");
     const int mode = e ? std::atoi(e) : -1;
     if (mode == 0) return pl;
     if (mode < 0 && (double)m * (double)W < 16777216.0) return pl;
-    const char* fe = std::getenv("GF2CU_STREAM_IN_FRAC");
-    const double f = fe ? std::min(0.9, std::max(0.01, std::atof(fe))) : 0.27;
+    std::vector<double> fr = env_list("GF2CU_STREAM_IN_BLOCKS");
+    if (fr.empty()) {
+        if (const char* fe = std::getenv("GF2CU_STREAM_IN_FRAC"))
+            fr = {std::atof(fe)};
+        else
+            fr = {1.0 / 16, 3.0 / 16, 7.0 / 16};
+    }
+    if (fr.size() > 7) fr.resize(7);  // (Workspace::up_ev)
     const size_t nss = (W + 1) / 2;
-    size_t m0 = ((size_t)(f * (double)m) + 255) / 256 * 256;
-    // (every super-step of the first phase keeps a full window and a full
-    // next window among the first block's rows)
-    m0 = std::min(m0, 128 * (nss - 1) + 256);
-    if (m0 + 256 > m || m0 < 512) return pl;
-    const size_t S1 = std::min((m0 - 256) / 128, nss - 1);
-    if (S1 < (mode > 0 ? 1u : 16u)) return pl;
-    pl.m0 = m0;
-    pl.S1 = (u32)S1;
+    // every super-step on a block keeps a full window and a full next window
+    // among its rows: at most (rows - 256) / 128 super-steps, and blocks past
+    // the last super-step's window add nothing
+    const size_t cap = 128 * (nss - 1) + 256;
+    std::vector<size_t> rows;
+    for (double f : fr) {
+        f = std::min(0.9, std::max(0.01, f));
+        size_t b = std::min(((size_t)(f * (double)m) + 255) / 256 * 256, cap);
+        b = std::max<size_t>(b, 512);
+        if (b + 256 > m) break;
+        if (!rows.empty() && b <= rows.back()) continue;
+        rows.push_back(b);
+    }
+    if (rows.empty()) return pl;
+    rows.push_back(m);
+    const size_t K = rows.size();
+    auto limit = [&](size_t k) { return (u32)std::min((rows[k] - 256) / 128, nss - 1); };
+    std::vector<u32> steps(K, 0u);
+    const std::vector<double> ts = env_list("GF2CU_STREAM_IN_STEPS");
+    if (!ts.empty() || mode > 0) {
+        for (size_t k = 1; k < K; ++k) {
+            const u32 want = k - 1 < ts.size() ? (u32)std::max(0.0, ts[k - 1]) : 0xffffffffu;
+            steps[k] = std::max(steps[k - 1], std::min(want, limit(k - 1)));
+        }
+    } else {
+        // time model (ms): PCIe delivers `rate` bytes per ms; a super-step S
+        // on R rows sweeps R * (W - 2S) words at `cw` ms per word plus a fixed
+        // cost (panel chain and step barrier; the replay has no panel chain)
+        const double rate = pageable ? 47e6 : 53e6, cw = 5.0e-9, fix_a = 0.018, fix_b = 0.012;
+        auto arrive = [&](size_t k) { return 0.05 + (double)rows[k] * (double)W * 8.0 / rate; };
+        double t = arrive(0) + 0.05;
+        u32 T = 0;
+        for (size_t k = 0; k + 1 < K; ++k) {
+            const u32 lim = limit(k);
+            while (T < lim && t < arrive(k + 1)) {
+                t += cw * (double)rows[k] * (double)(W - 2 * T) + fix_a;
+                ++T;
+            }
+            steps[k + 1] = T;
+            t = std::max(t, arrive(k + 1)) + 0.05;
+            for (u32 s2 = 0; s2 < T; ++s2) t += cw * (double)(rows[k + 1] - rows[k]) * (double)(W - 2 * s2) + fix_b;
+        }
+    }
+    if (steps.back() < (mode > 0 ? 1u : 8u)) return pl;
+    pl.rows = std::move(rows);
+    pl.steps = std::move(steps);
     return pl;
 }
 
@@ -931,12 +1050,14 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
                        ((fl & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= kSuperStepWords);
     const u32 Wpad4 = (u32)std::max<size_t>(4, (W + 3) / 4 * 4);
     StreamInPlan sin;
-    if (stream_from && super && !timing) sin = stream_in_plan(m, W);
-    if (stream_from && !sin.m0) {
+    if (stream_from && super && !timing)
+        sin = stream_in_plan(m, W, host_pageable(stream_from->data + (stream_from->col_off >> 6)));
+    if (stream_from && !sin.m0()) {
         st = upload_rows(0, m, s);
         if (st != GF2CU_OK) return st;
+        trace_gpu("uploaded whole", s);
     }
-    if (sin.m0) {
+    if (sin.m0()) {
         const size_t nss = (W + 1) / 2;
         if (!ws.up) CU_TRY(cudaStreamCreateWithFlags(&ws.up, cudaStreamNonBlocking));
         for (cudaEvent_t& e : ws.up_ev)
@@ -949,9 +1070,10 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         // far (an earlier call's work on this matrix) stays ahead of it
         CU_TRY(cudaEventRecord(ws.up_ev[0], s));
         CU_TRY(cudaStreamWaitEvent(ws.up, ws.up_ev[0], 0));
-        st = upload_rows(0, sin.m0, ws.up);
+        st = upload_rows(0, sin.m0(), ws.up);
         if (st != GF2CU_OK) return st;
         CU_TRY(cudaEventRecord(ws.up_ev[0], ws.up));
+        trace_gpu("block 0 uploaded", ws.up);
     }
     if (!multi) {
         if (!ws.ubuf) {
@@ -1011,8 +1133,8 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
     if (super) {
         p.Wpad8 = Wpad4;  // the super-step driver's tile width is 32 bytes
-        if (sin.m0) CU_TRY(cudaStreamWaitEvent(s, ws.up_ev[0], 0));
-        const u32 hi = sin.m0 ? (u32)sin.m0 : (u32)m;
+        if (sin.m0()) CU_TRY(cudaStreamWaitEvent(s, ws.up_ev[0], 0));
+        const u32 hi = sin.m0() ? (u32)sin.m0() : (u32)m;
         gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4, 0u, hi);
         gf2cu::ple_init4_kernel<<<sms * 4, 256, 0, s>>>(p, a->data, (u32)a->Wp, 0u, hi);
     } else {
@@ -1055,39 +1177,66 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
                 return cudaLaunchCooperativeKernel((void*)gf2cu::ple_super_kernel, dim3(grid),
                                                    dim3(gf2cu::kTrailThreads), sargs, gf2cu::kTableBytes, s);
             };
-            if (!sin.m0) {
+            if (!sin.m0()) {
+                trace_gpu("kernel begins", s);
                 CU_TRY(launch(p, ws.pout_b, ws.sout, gf2cu::SuperRange{0u, nss, 0u, 0u, 0u, nullptr}));
+                trace_gpu("kernel ends", s);
             } else {
-                // streamed input (ple_super.cuh, SuperRange): A on the first
-                // block while the second one uploads, B = the second block's
-                // replay of A's super-steps, C = the rest on all rows
-                const u32 S1 = sin.S1, m0 = (u32)sin.m0, nwk = (u32)grid - 1u;
+                // streamed input (StreamInPlan): A_0, then per later block k
+                // its upload, B_k (its replay of the super-steps so far) and
+                // A_k (the next super-steps on every row up to it; k = K-1:
+                // all the remaining ones on all rows, with the streamed output)
+                const u32 nwk = (u32)grid - 1u;
+                const size_t K = sin.rows.size();
                 CU_TRY(cudaMemsetAsync(ws.sin_abort, 0, sizeof(u32), s));
                 gf2cu::Params pa = p;
                 pa.pout = ws.hist_a;
                 pa.out = nullptr;
                 pa.out_host = nullptr;
-                gf2cu::Params pA = pa;
-                pA.mv = m0;
-                pA.partial = 1u;
-                CU_TRY(launch(pA, ws.hist_b, ws.hist_so, gf2cu::SuperRange{0u, S1, 0u, 0u, 1u, ws.sin_abort}));
-                st = upload_rows(m0, m, ws.up);
-                if (st != GF2CU_OK) return st;
-                CU_TRY(cudaEventRecord(ws.up_ev[1], ws.up));
-                CU_TRY(cudaStreamWaitEvent(s, ws.up_ev[1], 0));
-                gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4, m0, (u32)m);
-                gf2cu::ple_init4_kernel<<<sms * 4, 256, 0, s>>>(p, a->data, (u32)a->Wp, m0, (u32)m);
-                CU_TRY(cudaMemsetAsync(ws.apctr, 0, 2 * (W + 1) * sizeof(u32), s));
-                gf2cu::sync_preset_kernel<<<1, 1, 0, s>>>(ws.sync, S1, 0u, 0u, ws.sin_abort);
-                CU_TRY(launch(pa, ws.hist_b, ws.hist_so, gf2cu::SuperRange{0u, S1, m0, 1u, 1u, ws.sin_abort}));
-                CU_TRY(cudaMemsetAsync(ws.apctr, 0, 2 * (W + 1) * sizeof(u32), s));
-                // (the first output batch of C: the first multiple of kOutEvery >= S1)
-                const u32 sf = std::max(gf2cu::kOutEvery, (S1 + gf2cu::kOutEvery - 1) / gf2cu::kOutEvery * gf2cu::kOutEvery);
-                gf2cu::sync_preset_kernel<<<1, 1, 0, s>>>(ws.sync, S1, nwk * S1, nwk * (sf / gf2cu::kOutEvery - 1u),
-                                                          ws.sin_abort);
-                gf2cu::Params pC = p;
-                pC.pout = ws.hist_a;
-                CU_TRY(launch(pC, ws.hist_b, ws.hist_so, gf2cu::SuperRange{S1, nss, 0u, 0u, 1u, ws.sin_abort}));
+                for (size_t k = 0; k < K; ++k) {
+                    const bool last = k + 1 == K;
+                    const u32 lo = k ? (u32)sin.rows[k - 1] : 0u, hi = (u32)sin.rows[k];
+                    const u32 Tk = sin.steps[k], Tn = last ? nss : sin.steps[k + 1];
+                    if (k) {
+                        st = upload_rows(lo, hi, ws.up);
+                        if (st != GF2CU_OK) return st;
+                        CU_TRY(cudaEventRecord(ws.up_ev[k], ws.up));
+                        trace_gpu("block " + std::to_string(k) + " uploaded", ws.up);
+                        trace_gpu("stream ready for block " + std::to_string(k), s);
+                        CU_TRY(cudaStreamWaitEvent(s, ws.up_ev[k], 0));
+                        gf2cu::tile4_kernel<<<sms * 8, 256, 0, s>>>(a->data, a->alt, (u32)m, (u32)a->Wp, Wpad4, lo, hi);
+                        gf2cu::ple_init4_kernel<<<sms * 4, 256, 0, s>>>(p, a->data, (u32)a->Wp, lo, hi);
+                        if (Tk) {
+                            CU_TRY(cudaMemsetAsync(ws.apctr, 0, 2 * (W + 1) * sizeof(u32), s));
+                            gf2cu::sync_preset_kernel<<<1, 1, 0, s>>>(ws.sync, Tk, 0u, 0u, ws.sin_abort);
+                            gf2cu::Params pB = pa;
+                            pB.mv = last ? 0u : hi;
+                            trace_gpu("B" + std::to_string(k) + " begins (" + std::to_string(Tk) + " super-steps)", s);
+                            CU_TRY(launch(pB, ws.hist_b, ws.hist_so, gf2cu::SuperRange{0u, Tk, lo, 1u, 1u, ws.sin_abort}));
+                            trace_gpu("B" + std::to_string(k) + " ends", s);
+                        }
+                    }
+                    if (Tn == Tk) continue;
+                    u32 out_count = 0;
+                    if (last) {
+                        // (the first output batch of C: the first multiple of kOutEvery >= steps[K-1])
+                        const u32 sf = std::max(gf2cu::kOutEvery, (Tk + gf2cu::kOutEvery - 1) / gf2cu::kOutEvery * gf2cu::kOutEvery);
+                        out_count = nwk * (sf / gf2cu::kOutEvery - 1u);
+                    }
+                    if (k) {
+                        CU_TRY(cudaMemsetAsync(ws.apctr, 0, 2 * (W + 1) * sizeof(u32), s));
+                        gf2cu::sync_preset_kernel<<<1, 1, 0, s>>>(ws.sync, Tk, nwk * Tk, out_count, ws.sin_abort);
+                    }
+                    gf2cu::Params pA = last ? p : pa;
+                    pA.pout = ws.hist_a;
+                    if (!last) {
+                        pA.mv = hi;
+                        pA.partial = 1u;
+                    }
+                    trace_gpu("A" + std::to_string(k) + " begins [" + std::to_string(Tk) + ", " + std::to_string(Tn) + ")", s);
+                    CU_TRY(launch(pA, ws.hist_b, ws.hist_so, gf2cu::SuperRange{Tk, Tn, 0u, 0u, 1u, ws.sin_abort}));
+                    trace_gpu("A" + std::to_string(k) + " ends", s);
+                }
                 CU_TRY(cudaGetLastError());
             }
         } else {
@@ -1135,12 +1284,14 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
                 std::this_thread::sleep_for(std::chrono::microseconds(20));
             }
             cudaEventDestroy(kdone);
+            trace_host("kernel seen finished");
             CU_TRY(cudaStreamSynchronize(ws.copy));
+            trace_host("streamed copies done");
         }
         gf2cu::SyncState sy{};
         u32 gave_up = 0;
         CU_TRY(cudaMemcpyAsync(&sy, ws.sync, sizeof(sy), cudaMemcpyDeviceToHost, s));
-        if (sin.m0) CU_TRY(cudaMemcpyAsync(&gave_up, ws.sin_abort, sizeof(u32), cudaMemcpyDeviceToHost, s));
+        if (sin.m0()) CU_TRY(cudaMemcpyAsync(&gave_up, ws.sin_abort, sizeof(u32), cudaMemcpyDeviceToHost, s));
         CU_TRY(cudaStreamSynchronize(s));
         if (gave_up == 2u) return fail(GF2CU_ECUDA, "persistent PLE kernel watchdog tripped (streamed input)");
         if (gave_up) {
@@ -1230,8 +1381,10 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
     CU_TRY(cudaGetLastError());
     if (rows_streamed) *rows_streamed = sent;
+    trace_gpu("untile done", s);
 
     CU_TRY(cudaStreamSynchronize(s));
+    trace_host("run_ple synchronized");
     if (checking) {
         st = check_verdict(a, ws.check, rk, sms, s);
         if (st != GF2CU_OK) return st;
@@ -1274,8 +1427,9 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
         stats->trailing_launches = launches;
         stats->kernel_ms = kernel_ms;
         stats->driver = multi ? 0 : super ? 2 : 1;
-        stats->input_first_rows = sin.m0;
-        stats->input_first_steps = sin.m0 ? sin.S1 : 0;
+        stats->input_first_rows = sin.m0();
+        stats->input_first_steps = sin.m0() ? sin.steps.back() : 0;
+        stats->input_blocks = sin.rows.size();
         if (timing && !multi) {
             std::vector<u64> ph(8 * steps);
             CU_TRY(cudaMemcpy(ph.data(), ws.phase_ns, ph.size() * sizeof(u64), cudaMemcpyDeviceToHost));
@@ -1582,20 +1736,24 @@ gf2cu_status with_view(const gf2cu_view* v, const gf2cu_cfg* cfg, gf2cu_stats* s
     DeviceGuard g(c.device);
     cudaStream_t s = pick_stream(a, c.stream);
     std::vector<u64> packed;
+    trace_begin(s);
     if (!body_uploads) {
         st = view_upload(v, a, s, packed);
         if (st != GF2CU_OK) return st;
     }
     c.stream = s;
     st = body(a, c);
+    trace_host("body done");
     if (st == GF2CU_OK) {
         st = view_download(v, a, s, packed, rows_done ? *rows_done : 0,
                            rows_limit ? *rows_limit : ~size_t(0));
+        trace_host("download done");
         if (stats) {
             stats->h2d_bytes = double(a->m) * a->W * 8;
             stats->d2h_bytes = double(a->m) * a->W * 8;
         }
     }
+    trace_end();
     return st;
 }
 

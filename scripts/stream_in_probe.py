@@ -11,7 +11,8 @@ import torch
 import paper_1111_6549_b200 as G
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
-fracs = sys.argv[2:] or ["0.2", "0.27", "0.33"]
+# each setting: a GF2CU_STREAM_IN_BLOCKS list, optionally "@T1,T2,.." = GF2CU_STREAM_IN_STEPS
+fracs = sys.argv[2:] or ["0.27", "0.0625,0.1875,0.4375", "0.125,0.375", "0.03125,0.09375,0.21875,0.46875"]
 W = n // 64
 pin = torch.empty((n, W), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
 d = G.DeviceMatrix(n, n)
@@ -36,13 +37,17 @@ def run(buf, label, reps=4):
         want = (h, o.rank)
     ok = (h, o.rank) == want
     print(f"{label}: {[round(1e3 * t, 2) for t in ts]} ms  rank {o.rank} first block {o.stats['input_first_rows']} rows / "
-          f"{o.stats['input_first_steps']} super-steps  same result: {ok}", flush=True)
+          f"{o.stats['input_first_steps']} super-steps / {o.stats['input_blocks']} blocks  same result: {ok}", flush=True)
 
 
 for name, buf in (("pinned", pin), ("pageable", np.empty((n, W), dtype=np.uint64))):
     os.environ["GF2CU_STREAM_IN"] = "0"
     run(buf, f"{name} whole upload")
-    os.environ["GF2CU_STREAM_IN"] = "1"
+    os.environ.pop("GF2CU_STREAM_IN", None)  # the default rule: the time model picks the super-steps
     for f in fracs:
-        os.environ["GF2CU_STREAM_IN_FRAC"] = f
-        run(buf, f"{name} streamed f={f}")
+        b, _, t = f.partition("@")
+        os.environ["GF2CU_STREAM_IN_BLOCKS"] = b
+        os.environ.pop("GF2CU_STREAM_IN_STEPS", None)
+        if t:
+            os.environ["GF2CU_STREAM_IN_STEPS"] = t
+        run(buf, f"{name} streamed blocks={f}")

@@ -1,7 +1,7 @@
 """Streamed input of the drop-in gf2cu_ple (run_ple / SuperRange): the
-factorization starts on the first row block while the second one is uploaded,
-the late rows replay those super-steps from the panel history, and the rest
-runs on all rows. Bit-exact against the oracle like every other path; a column
+factorization starts on the first row block while the later ones are uploaded,
+each late block replays the super-steps so far from the panel history, and the
+rest runs on all rows. Bit-exact against the oracle like every other path; a column
 without a pivot among the first block's rows must fall back to the ordinary
 path (sparse, rank-deficient and zero inputs)."""
 import numpy as np
@@ -71,6 +71,24 @@ def test_streamed_input_block_sizes(stream_in, frac):
     ref, want, bm, got = run_both(a, m, n, G.PleConfig(super_step=True))
     assert_same(ref, want, bm, got, what=f"frac {frac}")
     assert got.stats["input_first_rows"] > 0
+
+
+@pytest.mark.parametrize("blocks,steps", [
+    ("0.125,0.25,0.5", None),             # as many super-steps per block as its rows allow
+    ("0.2,0.6", "3,9"),
+    ("0.125,0.375,0.625,0.875", "2,2,10,12"),  # a block that joins without new super-steps
+    ("0.3,0.5", "0,5"),                   # nothing runs on the first block alone
+    ("0.0625,0.1875,0.4375", None),       # the default shares
+])
+@pytest.mark.parametrize("m,n,kind", [(4096, 4096, "dense"), (8192, 4096, "dup"), (5000, 8192, "ctr")])
+def test_streamed_input_multi_block(stream_in, blocks, steps, m, n, kind):
+    stream_in.setenv("GF2CU_STREAM_IN_BLOCKS", blocks)
+    if steps:
+        stream_in.setenv("GF2CU_STREAM_IN_STEPS", steps)
+    a = make(kind, m, n, m + n)
+    ref, want, bm, got = run_both(a, m, n, G.PleConfig(super_step=True))
+    assert_same(ref, want, bm, got, what=f"blocks {blocks} steps {steps} {kind} {m}x{n}")
+    assert got.stats["input_blocks"] >= 3 and got.stats["input_first_steps"] >= 1
 
 
 @pytest.mark.parametrize("kind", ["p64", "p256", "dupcols", "zero", "late"])
