@@ -472,6 +472,9 @@ def gpu_arm(args, rank, world, local_rank):
                 "rank_matches_device_run": bool(e2e_parity),
                 "output_matches_device_run": e2e_words,
                 "host_memory": "pinned (torch pin_memory)",
+                "streamed_input": {"row_blocks": int(o2.stats["input_blocks"]),
+                                   "first_block_rows": int(o2.stats["input_first_rows"]),
+                                   "super_steps_before_last_block": int(o2.stats["input_first_steps"])},
                 "pageable": {"value": round(pg_bytes / pg_s / 1e9, 2), "unit": UNIT, "steps": pg_steps,
                              "ms_per_step": round(1e3 * pg_s / pg_steps, 3),
                              "output_matches_device_run": pg_words}},

@@ -1106,7 +1106,9 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     }
 
     *ws.host_r = 0;
-    const bool streaming = super && stream_to && rows_streamed;
+    // (GF2CU_STREAM_OUT=0, diagnostic: download everything after the kernel)
+    const char* so_env = std::getenv("GF2CU_STREAM_OUT");
+    const bool streaming = super && stream_to && rows_streamed && !(so_env && std::atoi(so_env) == 0);
     if (streaming) {
         *reinterpret_cast<volatile u32*>(ws.out_host) = 0;
         p.out = a->data;
