@@ -378,3 +378,42 @@ def test_undo_column_swaps_device():
     assert np.array_equal(d.download(), want)
     with pytest.raises(IndexError):
         G.undo_column_swaps(G.BitMatrix(4, 4), [G.ColSwap(0, 4, 0)])
+
+
+def test_concurrent_host_threads():
+    """The reference is re-entrant (no globals on the path; callers
+    may factor different matrices from different threads). The drop-in keeps its
+    device buffers, streams and staging per host thread: four threads factoring,
+    echelonizing and multiplying different shapes at once, each result against
+    the oracle."""
+    import threading
+
+    errors = []
+
+    def worker(tid):
+        try:
+            rng = np.random.default_rng(1000 + tid)
+            for it in range(12):
+                m, n = int(rng.integers(50, 900)), int(rng.integers(50, 900))
+                a = S.build(m, n, int(rng.integers(2, 7)), int(rng.integers(0, 2**40)))
+                cfg = [None, G.PleConfig(super_step=True), G.PleConfig(single_panel=True),
+                       G.PleConfig(peer_ranks=2)][(tid + it) % 4]
+                assert_same(*run_both(a, m, n, cfg), what=f"thread {tid} it {it} {m}x{n}")
+                rref = a.copy()
+                r = O.echelonize(rref, m, n, True)
+                bm = G.BitMatrix(m, n, a.copy())
+                assert G.echelonize(bm, True) == r and np.array_equal(bm.words, rref), f"thread {tid} echelonize"
+                k = int(rng.integers(1, 300))
+                b = O.fill_random(n, k, 0.5, tid * 100 + it)
+                got = G.mul(G.BitMatrix(m, n, a), G.BitMatrix(n, k, b)).words
+                assert np.array_equal(got, O.mul(a, n, b, k)), f"thread {tid} mul"
+        except BaseException as e:  # noqa: BLE001
+            errors.append(f"thread {tid}: {e!r}")
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in ts), "a thread hangs"
+    assert not errors, errors
