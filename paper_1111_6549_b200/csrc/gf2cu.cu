@@ -386,6 +386,16 @@ void rows_memcpy(unsigned char* dst, size_t dst_pitch, const unsigned char* src,
         std::memcpy(dst + (size_t)i * dst_pitch, src + (size_t)i * src_pitch, bytes);
 }
 
+// Rows per staging piece: a quarter of the copy (at least 1 MiB, at most a
+// whole staging buffer), so that even a copy that fits one buffer -- a row
+// block of the streamed input, a batch of the streamed output -- overlaps its
+// host memcpy with its DMA.
+size_t stage_piece_rows(size_t bytes, size_t rows) {
+    const size_t total = bytes * rows;
+    const size_t target = std::min(Staging::kBytes, std::max<size_t>(size_t(1) << 20, total / 4));
+    return std::max<size_t>(1, target / bytes);
+}
+
 // Host (pitch hp bytes) -> device (pitch dp bytes), `bytes` per row, `rows`
 // rows, ordered on s. Returns with the host buffer free to reuse.
 gf2cu_status staged_h2d(void* dev, size_t dp, const void* host, size_t hp, size_t bytes, size_t rows, int device,
@@ -397,7 +407,7 @@ gf2cu_status staged_h2d(void* dev, size_t dp, const void* host, size_t hp, size_
     gf2cu_status st = staging_ready(device);
     if (st != GF2CU_OK) return st;
     Staging& g = g_staging;
-    const size_t per = std::max<size_t>(1, Staging::kBytes / bytes);
+    const size_t per = stage_piece_rows(bytes, rows);
     for (size_t c = 0, r0 = 0; r0 < rows; ++c, r0 += per) {
         const int b = (int)(c % Staging::kBufs);
         const size_t nr = std::min(per, rows - r0);
@@ -421,7 +431,7 @@ gf2cu_status staged_d2h(void* host, size_t hp, const void* dev, size_t dp, size_
     gf2cu_status st = staging_ready(device);
     if (st != GF2CU_OK) return st;
     Staging& g = g_staging;
-    const size_t per = std::max<size_t>(1, Staging::kBytes / bytes);
+    const size_t per = stage_piece_rows(bytes, rows);
     const size_t nch = (rows + per - 1) / per;
     auto issue = [&](size_t c) -> cudaError_t {
         const int b = (int)(c % Staging::kBufs);
@@ -1281,6 +1291,7 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
                                                  cudaMemcpyDeviceToHost, ws.copy));
                     }
                     sent = avail;
+                    if (g_trace.on) trace_host(("streamed rows up to " + std::to_string(sent) + (fin ? " (kernel finished)" : "")).c_str());
                 }
                 if (fin) break;
                 std::this_thread::sleep_for(std::chrono::microseconds(20));
