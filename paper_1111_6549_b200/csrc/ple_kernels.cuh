@@ -425,54 +425,69 @@ struct LookAhead {
 // All `nthr` threads: scan positions r + [nwin, nrem) reducing each raw panel
 // word by the t pivots found so far; sh.best = the smallest (first set column
 // >= j, offset), with the winner's reduced state in sh.o_*.
+// The rows are scanned in position order in chunks that double in size, and
+// the scan stops after the first chunk that holds a candidate for column j
+// itself: the first row with a 1 in column j (ple.hpp:88-93) is then in that
+// chunk, and no later row can beat the key (j, offset). On sparse inputs
+// (BASELINE config 3, p = 1/256: the pivot is ~256 rows down) a miss reads a
+// couple of thousand rows instead of all of them. Only a column without any
+// candidate is scanned to the end; the key then names the next column that has
+// one (the caller's out_next).
 __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem, int nthr) {
     const int t = sh.t, j = sh.j;
     const bool two = sh.super == 2;
-    u64 best = ~0ull, b_red = 0, b_acc = 0, b_da = 0;
-    for (u32 off = nwin + threadIdx.x; off < nrem; off += nthr) {
-        u64 v = ldcg(p.pb + r + off), a = 0, da = 0;
-        if (two) {
-            // panel b of a super-step: word w+1 after panel a, from the row's
-            // pre-super-step words (pb = word w, pb2 = word w+1)
-            for (u32 s = 0; s < sh.rba; ++s) {
-                const u64 msk = 0ull - ((v >> sh.qa[s]) & 1ull);
-                v ^= sh.Ea[s] & msk;
-                da ^= sh.Da[s] & msk;
-            }
-            v = ldcg(p.pb2 + r + off);
-            for (u32 s = 0; s < sh.rba; ++s) v ^= sh.piv2[s] & (0ull - ((da >> s) & 1ull));
-        }
-        for (int s = 0; s < t; ++s) {
-            const u64 msk = 0ull - ((v >> sh.q[s]) & 1ull);
-            v ^= sh.E[s] & msk;
-            a ^= sh.D[s] & msk;
-        }
-        const u64 mk = v & ~low_mask64(j);
-        if (mk) {
-            const u64 key = ((u64)(__ffsll((long long)mk) - 1) << 32) | off;
-            if (key < best) {
-                best = key;
-                b_red = v;
-                b_acc = a;
-                b_da = da;
-            }
-        }
-    }
-    u64 wb = best;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const u64 other = __shfl_xor_sync(0xffffffffu, wb, o);
-        wb = other < wb ? other : wb;
-    }
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) sh.warp_best[wid] = wb;
-    named_bar(2, nthr);
-    if (threadIdx.x == 0) {
-        u64 b = ~0ull;
-        for (int k = 0; k < nthr / 32; ++k) b = sh.warp_best[k] < b ? sh.warp_best[k] : b;
-        sh.best = b;
+    u64 best = ~0ull, b_red = 0, b_acc = 0, b_da = 0;
+    u32 lo = nwin, csize = 4u * (u32)nthr;
+    for (;;) {
+        const u32 hi = nrem - lo > csize ? lo + csize : nrem;
+        for (u32 off = lo + threadIdx.x; off < hi; off += nthr) {
+            u64 v = ldcg(p.pb + r + off), a = 0, da = 0;
+            if (two) {
+                // panel b of a super-step: word w+1 after panel a, from the row's
+                // pre-super-step words (pb = word w, pb2 = word w+1)
+                for (u32 s = 0; s < sh.rba; ++s) {
+                    const u64 msk = 0ull - ((v >> sh.qa[s]) & 1ull);
+                    v ^= sh.Ea[s] & msk;
+                    da ^= sh.Da[s] & msk;
+                }
+                v = ldcg(p.pb2 + r + off);
+                for (u32 s = 0; s < sh.rba; ++s) v ^= sh.piv2[s] & (0ull - ((da >> s) & 1ull));
+            }
+            for (int s = 0; s < t; ++s) {
+                const u64 msk = 0ull - ((v >> sh.q[s]) & 1ull);
+                v ^= sh.E[s] & msk;
+                a ^= sh.D[s] & msk;
+            }
+            const u64 mk = v & ~low_mask64(j);
+            if (mk) {
+                const u64 key = ((u64)(__ffsll((long long)mk) - 1) << 32) | off;
+                if (key < best) {
+                    best = key;
+                    b_red = v;
+                    b_acc = a;
+                    b_da = da;
+                }
+            }
+        }
+        u64 wb = best;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const u64 other = __shfl_xor_sync(0xffffffffu, wb, o);
+            wb = other < wb ? other : wb;
+        }
+        if (lane == 0) sh.warp_best[wid] = wb;
+        named_bar(2, nthr);
+        if (threadIdx.x == 0) {
+            u64 b = ~0ull;
+            for (int k = 0; k < nthr / 32; ++k) b = sh.warp_best[k] < b ? sh.warp_best[k] : b;
+            sh.best = b;
+        }
+        named_bar(2, nthr);
+        lo = hi;
+        if (lo >= nrem || (int)(sh.best >> 32) == j) break;
+        csize *= 2u;
     }
-    named_bar(2, nthr);
     if (best != ~0ull && best == sh.best) {
         const u32 off = (u32)(best & 0xffffffffu);
         sh.o_red = b_red;
