@@ -433,40 +433,72 @@ struct LookAhead {
 // couple of thousand rows instead of all of them. Only a column without any
 // candidate is scanned to the end; the key then names the next column that has
 // one (the caller's out_next).
+constexpr int kScanRows = 4;  // rows per thread in flight in panel_scan
+
 __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem, int nthr) {
     const int t = sh.t, j = sh.j;
     const bool two = sh.super == 2;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     u64 best = ~0ull, b_red = 0, b_acc = 0, b_da = 0;
-    u32 lo = nwin, csize = 4u * (u32)nthr;
+    u32 lo = nwin, csize = (u32)kScanRows * (u32)nthr;
     for (;;) {
         const u32 hi = nrem - lo > csize ? lo + csize : nrem;
-        for (u32 off = lo + threadIdx.x; off < hi; off += nthr) {
-            u64 v = ldcg(p.pb + r + off), a = 0, da = 0;
+        // kScanRows rows per thread at a time: their loads are issued together
+        // and their (dependent, per row) reductions interleaved
+        for (u32 base = lo; base < hi; base += kScanRows * (u32)nthr) {
+            u64 v[kScanRows], a[kScanRows], da[kScanRows], v2[kScanRows];
+            u32 off[kScanRows];
+#pragma unroll
+            for (int k = 0; k < kScanRows; ++k) {
+                off[k] = base + (u32)k * (u32)nthr + threadIdx.x;
+                const bool val = off[k] < hi;
+                v[k] = val ? ldcg(p.pb + r + off[k]) : 0ull;
+                v2[k] = (val && two) ? ldcg(p.pb2 + r + off[k]) : 0ull;
+                a[k] = 0ull;
+                da[k] = 0ull;
+            }
             if (two) {
                 // panel b of a super-step: word w+1 after panel a, from the row's
                 // pre-super-step words (pb = word w, pb2 = word w+1)
                 for (u32 s = 0; s < sh.rba; ++s) {
-                    const u64 msk = 0ull - ((v >> sh.qa[s]) & 1ull);
-                    v ^= sh.Ea[s] & msk;
-                    da ^= sh.Da[s] & msk;
+                    const u32 qs = sh.qa[s];
+                    const u64 Es = sh.Ea[s], Ds = sh.Da[s];
+#pragma unroll
+                    for (int k = 0; k < kScanRows; ++k) {
+                        const u64 msk = 0ull - ((v[k] >> qs) & 1ull);
+                        v[k] ^= Es & msk;
+                        da[k] ^= Ds & msk;
+                    }
                 }
-                v = ldcg(p.pb2 + r + off);
-                for (u32 s = 0; s < sh.rba; ++s) v ^= sh.piv2[s] & (0ull - ((da >> s) & 1ull));
+#pragma unroll
+                for (int k = 0; k < kScanRows; ++k) v[k] = v2[k];
+                for (u32 s = 0; s < sh.rba; ++s) {
+                    const u64 ps = sh.piv2[s];
+#pragma unroll
+                    for (int k = 0; k < kScanRows; ++k) v[k] ^= ps & (0ull - ((da[k] >> s) & 1ull));
+                }
             }
             for (int s = 0; s < t; ++s) {
-                const u64 msk = 0ull - ((v >> sh.q[s]) & 1ull);
-                v ^= sh.E[s] & msk;
-                a ^= sh.D[s] & msk;
+                const u32 qs = sh.q[s];
+                const u64 Es = sh.E[s], Ds = sh.D[s];
+#pragma unroll
+                for (int k = 0; k < kScanRows; ++k) {
+                    const u64 msk = 0ull - ((v[k] >> qs) & 1ull);
+                    v[k] ^= Es & msk;
+                    a[k] ^= Ds & msk;
+                }
             }
-            const u64 mk = v & ~low_mask64(j);
-            if (mk) {
-                const u64 key = ((u64)(__ffsll((long long)mk) - 1) << 32) | off;
-                if (key < best) {
-                    best = key;
-                    b_red = v;
-                    b_acc = a;
-                    b_da = da;
+#pragma unroll
+            for (int k = 0; k < kScanRows; ++k) {
+                const u64 mk = v[k] & ~low_mask64(j);
+                if (off[k] < hi && mk) {
+                    const u64 key = ((u64)(__ffsll((long long)mk) - 1) << 32) | off[k];
+                    if (key < best) {
+                        best = key;
+                        b_red = v[k];
+                        b_acc = a[k];
+                        b_da = da[k];
+                    }
                 }
             }
         }
