@@ -360,6 +360,7 @@ struct PanelShared {
     int t, j;
     u64 warp_best[32];
     u64 best;  // (first column << 32) | offset
+    u64 wor[4];  // per window warp: OR of its live rows' remaining columns (column skip)
     u64 o_red, o_acc, o_raw, o_raw2;
     u32 o_phys;
     u32 r;
@@ -864,7 +865,25 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
             const int st = cross_step(j);
             if (me == 0) sh.dbg_cross += 1u;
             if (st == 2) break;
-            ++j;
+            if (st == 0) {
+                // Column j has no pivot. Skip to the next column that can have
+                // one: the first column > j some live window row holds, or
+                // out_next, the first column with a candidate among the other
+                // rows (still exact: no outside row holds a column below it, so
+                // window pivots left of it do not change them). An exhausted
+                // trailing matrix (rank-deficient inputs) ends the panel here
+                // instead of stepping through every column.
+                const u64 x = (inwin & (me >= (u32)t)) ? (red & ~low_mask64(j + 1)) : 0ull;
+                const u32 xl = __reduce_or_sync(0xffffffffu, (u32)x);
+                const u32 xh = __reduce_or_sync(0xffffffffu, (u32)(x >> 32));
+                if (lane == 0) sh.wor[wid] = ((u64)xh << 32) | xl;
+                named_bar(3, kWin);
+                const u64 any = sh.wor[0] | sh.wor[1] | sh.wor[2] | sh.wor[3];
+                const int nw = any ? __ffsll((long long)any) - 1 : 64;
+                j = min(nw, out_next);
+            } else {
+                ++j;
+            }
         }
         if (p.phase_ns && me == 0) p.phase_ns[(size_t)w * 8 + 7] = globaltimer();
         if (p.phase_ns) named_bar(3, kWin);
