@@ -436,18 +436,45 @@ struct LookAhead {
 // one (the caller's out_next).
 constexpr int kScanRows = 4;  // rows per thread in flight in panel_scan
 
-__device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem, int nthr) {
+// OR of (1 << q[s]) for s < n (n <= 64), computed by one warp (all lanes).
+__device__ __forceinline__ u64 pivot_mask(const u32* q, u32 n) {
+    const u32 lane = threadIdx.x & 31u;
+    const u64 x = (lane < n ? 1ull << q[lane] : 0ull) | (lane + 32u < n ? 1ull << q[lane + 32u] : 0ull);
+    const u32 lo = __reduce_or_sync(0xffffffffu, (u32)x), hi = __reduce_or_sync(0xffffffffu, (u32)(x >> 32));
+    return ((u64)hi << 32) | lo;
+}
+
+// v reduced by the pivots whose columns are the bits of pm (pivot s = the s-th
+// set bit: the columns increase with s), acc ^= their D. Walks the row's set
+// pivot bits instead of all pivots: E[s] only holds columns right of q[s], so
+// taking the bits in increasing order is the step-by-step elimination; a
+// sparse row costs a couple of iterations instead of one step per pivot.
+__device__ __forceinline__ void reduce_sparse(u64& v, u64& acc, u64 pm, const u64* E, const u64* D) {
+    u64 rem = pm;
+    for (;;) {
+        const u64 x = v & rem;
+        if (!x) break;
+        const int c = __ffsll((long long)x) - 1;
+        const int s = __popcll(pm & low_mask64(c));
+        v ^= E[s];
+        acc ^= D[s];
+        rem &= ~low_mask64(c + 1);
+    }
+}
+
+__device__ __forceinline__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem, int nthr) {
     const int t = sh.t, j = sh.j;
     const bool two = sh.super == 2;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     u64 best = ~0ull, b_red = 0, b_acc = 0, b_da = 0;
+    const u64 pm = pivot_mask(sh.q, (u32)t);
+    const u64 pma = two ? pivot_mask(sh.qa, sh.rba) : 0ull;
     u32 lo = nwin, csize = (u32)kScanRows * (u32)nthr;
     for (;;) {
         const u32 hi = nrem - lo > csize ? lo + csize : nrem;
         // kScanRows rows per thread at a time: their loads are issued together
-        // and their (dependent, per row) reductions interleaved
         for (u32 base = lo; base < hi; base += kScanRows * (u32)nthr) {
-            u64 v[kScanRows], a[kScanRows], da[kScanRows], v2[kScanRows];
+            u64 v[kScanRows], v2[kScanRows];
             u32 off[kScanRows];
 #pragma unroll
             for (int k = 0; k < kScanRows; ++k) {
@@ -455,50 +482,26 @@ __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u3
                 const bool val = off[k] < hi;
                 v[k] = val ? ldcg(p.pb + r + off[k]) : 0ull;
                 v2[k] = (val && two) ? ldcg(p.pb2 + r + off[k]) : 0ull;
-                a[k] = 0ull;
-                da[k] = 0ull;
-            }
-            if (two) {
-                // panel b of a super-step: word w+1 after panel a, from the row's
-                // pre-super-step words (pb = word w, pb2 = word w+1)
-                for (u32 s = 0; s < sh.rba; ++s) {
-                    const u32 qs = sh.qa[s];
-                    const u64 Es = sh.Ea[s], Ds = sh.Da[s];
-#pragma unroll
-                    for (int k = 0; k < kScanRows; ++k) {
-                        const u64 msk = 0ull - ((v[k] >> qs) & 1ull);
-                        v[k] ^= Es & msk;
-                        da[k] ^= Ds & msk;
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < kScanRows; ++k) v[k] = v2[k];
-                for (u32 s = 0; s < sh.rba; ++s) {
-                    const u64 ps = sh.piv2[s];
-#pragma unroll
-                    for (int k = 0; k < kScanRows; ++k) v[k] ^= ps & (0ull - ((da[k] >> s) & 1ull));
-                }
-            }
-            for (int s = 0; s < t; ++s) {
-                const u32 qs = sh.q[s];
-                const u64 Es = sh.E[s], Ds = sh.D[s];
-#pragma unroll
-                for (int k = 0; k < kScanRows; ++k) {
-                    const u64 msk = 0ull - ((v[k] >> qs) & 1ull);
-                    v[k] ^= Es & msk;
-                    a[k] ^= Ds & msk;
-                }
             }
 #pragma unroll
             for (int k = 0; k < kScanRows; ++k) {
-                const u64 mk = v[k] & ~low_mask64(j);
+                u64 x = v[k], a = 0ull, da = 0ull;
+                if (two) {
+                    // panel b of a super-step: word w+1 after panel a, from the row's
+                    // pre-super-step words (pb = word w, pb2 = word w+1)
+                    reduce_sparse(x, da, pma, sh.Ea, sh.Da);
+                    x = v2[k];
+                    for (u64 dr = da; dr; dr &= dr - 1ull) x ^= sh.piv2[__ffsll((long long)dr) - 1];
+                }
+                reduce_sparse(x, a, pm, sh.E, sh.D);
+                const u64 mk = x & ~low_mask64(j);
                 if (off[k] < hi && mk) {
                     const u64 key = ((u64)(__ffsll((long long)mk) - 1) << 32) | off[k];
                     if (key < best) {
                         best = key;
-                        b_red = v[k];
-                        b_acc = a[k];
-                        b_da = da[k];
+                        b_red = x;
+                        b_acc = a;
+                        b_da = da;
                     }
                 }
             }
@@ -533,6 +536,15 @@ __device__ void panel_scan(const Params& p, PanelShared& sh, u32 r, u32 nwin, u3
     named_bar(2, nthr);
 }
 
+// panel_scan as a real call. The single-panel persistent kernel is faster with
+// the scan out of line (4096^2 0.887 -> 0.854 ms: the panel chain's code stays
+// compact); the two-panel kernels are not (the call's register convention costs
+// their sweep 284 bytes of spills, 32768^2 13.1 -> 16.8 ms), so they inline it.
+__device__ __noinline__ void panel_scan_call(const Params& p, PanelShared& sh, u32 r, u32 nwin, u32 nrem,
+                                             int nthr) {
+    panel_scan(p, sh, r, nwin, nrem, nthr);
+}
+
 // The panel step w. Called by every thread of ONE CTA of `nthr` >= 256
 // threads. Warps 0-3 hold the 128-row window, one row per thread (`red` =
 // the row's panel word reduced by the pivots so far, `acc` = its combination
@@ -550,6 +562,7 @@ __device__ __forceinline__ void la_wait_cap(const LookAhead* la, PanelShared& sh
     named_bar(bar_id, bar_cnt);
 }
 
+template <bool kCallScan = false>
 __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nthr,
                                  const LookAhead* la = nullptr) {
     if (threadIdx.x == 0) {
@@ -607,7 +620,10 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
         for (;;) {
             named_bar(1, nthr);
             if (sh.cmd != 0) break;
-            panel_scan(p, sh, r, nwin, nrem, nthr);
+            if constexpr (kCallScan)
+                panel_scan_call(p, sh, r, nwin, nrem, nthr);
+            else
+                panel_scan(p, sh, r, nwin, nrem, nthr);
         }
     } else {
         // ---- window warps: thread `me` holds window row `me` ----
@@ -718,7 +734,10 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
                     sh.j = j;
                 }
                 named_bar(1, nthr);
-                panel_scan(p, sh, r, nwin, nrem, nthr);
+                if constexpr (kCallScan)
+                    panel_scan_call(p, sh, r, nwin, nrem, nthr);
+                else
+                    panel_scan(p, sh, r, nwin, nrem, nthr);
                 const u64 best = sh.best;
                 out_next = best == ~0ull ? 64 : (int)(best >> 32);
                 if (out_next != j) {
@@ -1086,7 +1105,7 @@ __device__ u32 panel_factor_body(const Params& p, u32 w, PanelShared& sh, int nt
 
 __global__ void __launch_bounds__(kPanelThreads, 1) panel_factor_kernel(Params p, u32 w) {
     __shared__ PanelShared sh;
-    panel_factor_body(p, w, sh, kPanelThreads);
+    panel_factor_body<true>(p, w, sh, kPanelThreads);
 }
 
 // ===========================================================================

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             Params q = p;
             q.pb = s.peer[s.rank].pb[w & 1u];
             q.pb2 = s.peer[s.rank].pb2[w & 1u];
-            const u32 rb = panel_factor_body(q, w, psh, blockDim.x, &la);
+            const u32 rb = panel_factor_body<true>(q, w, psh, blockDim.x, &la);
             if (*(volatile u32*)err) {
                 if (threadIdx.x == 0) peer_fail(s);
                 return;

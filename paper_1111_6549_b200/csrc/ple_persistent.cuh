@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1) ple_persistent_kernel(Params
             la.cap_target = w > 0 ? pw_chunks(p.m - prev_r, p.pw_div) : 0u;
             prev_r = la.r;
             stamp(p, w, 0);
-            const u32 rb = panel_factor_body(p, w, psh, nbody, &la);
+            const u32 rb = panel_factor_body<true>(p, w, psh, nbody, &la);
             stamp(p, w, 1);
             // (an aborted panel returns 0: then check the error word itself)
             if (rb == 0u && *(volatile u32*)&sy->error) {

@@ -58,7 +58,10 @@ kinds = {
     "all ones": lambda: O.fill_random(n, n, 1.0, 1),
 }
 d = G.DeviceMatrix(n, n)
+only = set(sys.argv[2:])
 for name, make in kinds.items():
+    if only and name not in only:
+        continue
     a = make()
     ref = a.copy()
     t0 = time.perf_counter()
