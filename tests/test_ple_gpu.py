@@ -417,3 +417,47 @@ def test_concurrent_host_threads():
         t.join(timeout=600)
     assert not any(t.is_alive() for t in ts), "a thread hangs"
     assert not errors, errors
+
+
+def _structured(kind, m, n, seed):
+    rng = np.random.default_rng(seed)
+    W = (n + 63) // 64
+    if kind == "permutation":  # every pivot is a window miss, found at a random depth
+        a = np.zeros((m, W), dtype=np.uint64)
+        p = rng.permutation(max(m, n))[:m] % n
+        a[np.arange(m), p >> 6] = np.uint64(1) << (p & 63).astype(np.uint64)
+        return a
+    if kind == "zero_top":  # the first half of the rows is empty: scans go thousands of rows deep
+        a = O.fill_random(m, n, 0.5, seed)
+        a[: m // 2] = 0
+        return a
+    if kind == "nnz3":
+        return O.fill_random_rows(m, n, 3, seed)
+    if kind == "p1024":
+        return O.fill_random(m, n, 1 / 1024, seed)
+    if kind == "rank40":  # the trailing matrix is exhausted after the first panel
+        return O.mul(O.fill_random(m, 40, 0.5, seed), 40, O.fill_random(40, n, 0.5, seed + 1), n)
+    if kind == "zero_left":  # whole panels without a pivot, then a dense block
+        a = O.fill_random(m, n, 0.5, seed)
+        a[:, : W // 2] = 0
+        return a
+    if kind == "deep_single":  # one column whose only 1 sits in the last row
+        a = O.fill_random(m, n, 0.5, seed)
+        a[:, 1] &= ~np.uint64(1 << 7)
+        a[m - 1, 1] |= np.uint64(1 << 7)
+        return a
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("driver", ["single", "super", "peer2", "peer3s"])
+@pytest.mark.parametrize("kind", ["permutation", "zero_top", "nnz3", "p1024", "rank40", "zero_left",
+                                  "deep_single"])
+def test_structured_inputs_deep_scans(kind, driver):
+    """Window-miss scans that go past their first chunk (several doubling
+    rounds), rows that are dead for a whole panel, pivotless panels and the
+    column skip after them, on every persistent driver."""
+    m, n = 6200, 6144
+    cfg = {"single": G.PleConfig(single_panel=True), "super": G.PleConfig(super_step=True),
+           "peer2": G.PleConfig(peer_ranks=2), "peer3s": G.PleConfig(peer_ranks=3, super_step=True)}[driver]
+    a = _structured(kind, m, n, 77)
+    assert_same(*run_both(a, m, n, cfg), what=f"{kind} {driver}")
