@@ -938,6 +938,11 @@ std::vector<double> env_list(const char* name) {
     return v;
 }
 
+bool sparse_rule_on() {
+    const char* e = std::getenv("GF2CU_SPARSE_RULE");
+    return !(e && std::atoi(e) == 0);
+}
+
 StreamInPlan stream_in_plan(size_t m, size_t W, bool pageable) {
     StreamInPlan pl;
     const char* e = std::getenv("GF2CU_STREAM_IN");
@@ -1100,8 +1105,36 @@ gf2cu_status run_ple(gf2cu_matrix* a, const gf2cu_cfg* cfg, size_t* swaps, size_
     // synchronization, but the panel CTA's chain per super-step is longer:
     // it pays from ~2^24 matrix words up (measured crossover near 32768^2).
     const unsigned fl = cfg ? cfg->flags : 0u;
-    const bool super = !multi && !(fl & GF2CU_FLAG_SINGLE_PANEL) &&
-                       ((fl & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= kSuperStepWords);
+    bool super = !multi && !(fl & GF2CU_FLAG_SINGLE_PANEL) &&
+                 ((fl & GF2CU_FLAG_SUPER_STEP) || (double)m * (double)W >= kSuperStepWords);
+    // Sparse inputs are bound by window misses, not by the sweep, and a miss
+    // costs the two-panel driver more (panel b's scan reduces every row by
+    // panel a first): 32768^2 at p = 1/1024 takes 54 ms with it and 38 ms with
+    // the single-panel driver; at p = 1/256 they tie. Below a sampled density
+    // of 1/384 the size rule's choice falls back to the single-panel driver
+    // (one word per row sampled; a forced driver is left alone;
+    // GF2CU_SPARSE_RULE=0 turns the rule off).
+    if (super && !(fl & GF2CU_FLAG_SUPER_STEP) && sparse_rule_on()) {
+        double ones = 0.0;
+        if (stream_from) {
+            const uint64_t* host = stream_from->data + (stream_from->col_off >> 6);
+            // (2048 evenly spaced rows: the cache misses of more would show in e2e)
+            const size_t ns = std::min<size_t>(m, 2048), step = m / ns;
+            for (size_t k = 0; k < ns; ++k) {
+                const size_t i = k * step;
+                ones += (double)__builtin_popcountll(host[i * stream_from->stride + ((u32)i * 0x9e3779b1u) % W]);
+            }
+            ones *= (double)m / (double)ns;
+        } else {
+            u32 cnt = 0;
+            CU_TRY(cudaMemsetAsync(ws.rhist, 0, sizeof(u32), s));
+            gf2cu::density_sample_kernel<<<sms, 256, 0, s>>>(a->data, (u32)m, (u32)W, (u32)a->Wp, ws.rhist);
+            CU_TRY(cudaMemcpyAsync(&cnt, ws.rhist, sizeof(u32), cudaMemcpyDeviceToHost, s));
+            CU_TRY(cudaStreamSynchronize(s));
+            ones = (double)cnt;
+        }
+        if (ones < (double)m * 64.0 / 384.0) super = false;
+    }
     const u32 Wpad4 = (u32)std::max<size_t>(4, (W + 3) / 4 * 4);
     StreamInPlan sin;
     if (stream_from && super && !timing)

@@ -1527,6 +1527,16 @@ __global__ void fill_ctr_kernel(u64* mat, u32 m, u32 n, u32 Wp, u64 seed) {
 }
 
 // Per-row FNV-1a over the W logical words (combined over rows on the host).
+// Density estimate of a row-major matrix: the set bits of one pseudo-randomly
+// chosen word per row, summed into *ones (run_ple's driver choice).
+__global__ void density_sample_kernel(const u64* __restrict__ mat, u32 m, u32 W, u32 Wp, u32* ones) {
+    u32 acc = 0;
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        acc += (u32)__popcll(mat[(size_t)i * Wp + (i * 0x9e3779b1u) % W]);
+    acc = __reduce_add_sync(0xffffffffu, acc);
+    if ((threadIdx.x & 31u) == 0u && acc) atomicAdd(ones, acc);
+}
+
 __global__ void row_hash_kernel(const u64* mat, u32 m, u32 W, u32 Wp, u64* out) {
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         u64 h = 0xcbf29ce484222325ull;

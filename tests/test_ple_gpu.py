@@ -461,3 +461,33 @@ def test_structured_inputs_deep_scans(kind, driver):
            "peer2": G.PleConfig(peer_ranks=2), "peer3s": G.PleConfig(peer_ranks=3, super_step=True)}[driver]
     a = _structured(kind, m, n, 77)
     assert_same(*run_both(a, m, n, cfg), what=f"{kind} {driver}")
+
+
+def test_sparse_inputs_take_the_single_panel_driver(monkeypatch):
+    """The size rule's two-panel driver falls back to the single-panel one for
+    sparse inputs (sampled density below 1/384), on device-resident and host
+    matrices; dense inputs, forced drivers and GF2CU_SPARSE_RULE=0 are not
+    affected. Bit-exact either way."""
+    m = n = 20480  # above the size rule's switch
+    for p, want in ((1 / 1024, 1), (0.5, 2)):
+        a = O.fill_random(m, n, p, 5)
+        d = G.DeviceMatrix(m, n)
+        d.upload(a)
+        out = G.block_iterative_ple(d)
+        assert out.stats["driver"] == want, (p, out.stats["driver"])
+        bm = G.BitMatrix(m, n, a.copy())
+        o2 = G.block_iterative_ple(bm)
+        assert o2.stats["driver"] == want and o2.rank == out.rank
+        got = np.empty_like(a)
+        d.download(got)
+        assert np.array_equal(got, bm.words) and np.array_equal(out.q, o2.q)
+        if want == 1:
+            d.upload(a)
+            assert G.block_iterative_ple(d, G.PleConfig(super_step=True)).stats["driver"] == 2
+            d.download(got)
+            assert np.array_equal(got, bm.words)
+            monkeypatch.setenv("GF2CU_SPARSE_RULE", "0")
+            d.upload(a)
+            assert G.block_iterative_ple(d).stats["driver"] == 2
+            monkeypatch.delenv("GF2CU_SPARSE_RULE")
+        d.close()
