@@ -13,7 +13,10 @@ value      = effective GB/s = algorithmic trailing-update bytes / device time,
              restores the input from a pristine HBM copy inside the timed
              region (the 512 MiB D2D copy is counted in the time).
 e2e        = the same metric through the C ABI drop-in gf2cu_ple() on pinned
-             HOST buffers: H2D of the input + PLE + D2H of L\\E every step.
+             HOST buffers: H2D of the input + PLE + D2H of L\\E every step
+             (the library uploads in row blocks and starts on the first one,
+             and streams finished rows back while the kernel runs; the same
+             call on pageable memory is reported beside it).
 roofline   = trailing_update (the dominant kernel): algorithmic bytes per
              launch / average CUDA-event launch duration, vs the measured HBM
              copy bandwidth in MEASURED_PEAKS.json.
