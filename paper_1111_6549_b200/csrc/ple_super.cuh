@@ -44,18 +44,47 @@ __device__ __forceinline__ const u32* info_phys(const ulonglong2* info, u32 m) {
     return reinterpret_cast<const u32*>(info + m);
 }
 
+// Layout conversions go through shared memory in blocks of 32 rows x 16 tiles
+// (512 bytes per row), so that both sides move long runs: 512 contiguous
+// bytes per row on the row-major side, 32 rows x 32 bytes = 1 KiB contiguous
+// per tile on the tile-major side (a direct copy scatters one side in 32-byte
+// pieces and reached about half the HBM bandwidth). Rows are padded by 32
+// bytes in shared memory: the tile-major side walks down the rows.
+constexpr u32 kCvRows = 32, kCvTiles = 16, kCvPitch = kCvTiles * 32u + 32u;
+
 // row-major (stride Wp) -> 32-byte tiles (Wpad4 words per row)
 // (rows [row_lo, row_hi) only: streamed input tiles the row blocks as they arrive)
-__global__ void tile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst, u32 m, u32 Wp,
-                             u32 Wpad4, u32 row_lo = 0u, u32 row_hi = 0xffffffffu) {
-    const u32 per_row = Wpad4 >> 1;
+__global__ void __launch_bounds__(256) tile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst, u32 m,
+                                                    u32 Wp, u32 Wpad4, u32 row_lo = 0u,
+                                                    u32 row_hi = 0xffffffffu) {
+    __shared__ __align__(16) unsigned char buf[kCvRows * kCvPitch];
     row_hi = min(row_hi, m);
-    const u64 total = (u64)(row_hi - row_lo) * per_row;
-    for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (u64)gridDim.x * blockDim.x) {
-        const u32 rr = (u32)(e / per_row), row = row_lo + rr, x = 2u * (u32)(e - (u64)rr * per_row);
-        *reinterpret_cast<ulonglong2*>(tw4(dst, m, row, x)) =
-            *reinterpret_cast<const ulonglong2*>(src + (size_t)row * Wp + x);
+    if (row_hi <= row_lo) return;
+    const u32 ntile = Wpad4 >> 2, tblocks = (ntile + kCvTiles - 1) / kCvTiles;
+    const u32 rblocks = (row_hi - row_lo + kCvRows - 1) / kCvRows;
+    const u32 tid = threadIdx.x;
+    for (u32 blk = blockIdx.x; blk < tblocks * rblocks; blk += gridDim.x) {
+        const u32 row0 = row_lo + (blk / tblocks) * kCvRows, tile0 = (blk % tblocks) * kCvTiles;
+        // row-major side: 32 threads cover a row's 512 bytes, 8 rows per pass
+#pragma unroll
+        for (u32 i = 0; i < 4; ++i) {
+            const u32 rr = (tid >> 5) + 8u * i, u = tid & 31u;
+            const u32 row = row0 + rr, x = tile0 * 4u + 2u * u;
+            if (row < row_hi && x < Wpad4)
+                *reinterpret_cast<ulonglong2*>(buf + rr * kCvPitch + u * 16u) =
+                    *reinterpret_cast<const ulonglong2*>(src + (size_t)row * Wp + x);
+        }
+        __syncthreads();
+        // tile-major side: 64 threads cover a tile's 32 rows x 32 bytes, 4 tiles per pass
+#pragma unroll
+        for (u32 i = 0; i < 4; ++i) {
+            const u32 t = (tid >> 6) + 4u * i, rr = (tid & 63u) >> 1, h = tid & 1u;
+            const u32 row = row0 + rr, x = (tile0 + t) * 4u + 2u * h;
+            if (row < row_hi && x < Wpad4)
+                *reinterpret_cast<ulonglong2*>(tw4(dst, m, row, x)) =
+                    *reinterpret_cast<const ulonglong2*>(buf + rr * kCvPitch + t * 32u + h * 16u);
+        }
+        __syncthreads();
     }
 }
 
@@ -74,17 +103,36 @@ __device__ __forceinline__ const u64* final4(const u64* src, const u32* perm, u3
 }
 
 // (positions below row_lo were already written, by the kernel's streamed output)
-__global__ void untile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst,
-                               const u32* __restrict__ perm, u32 m, u32 Wp, u32 Wpad4,
-                               const u64* __restrict__ ubuf, u32 ucap, const u32* __restrict__ qcol,
-                               u32 rank, u32 W, u32 row_lo = 0u) {
-    const u32 per_row = Wpad4 >> 1;
-    const u64 total = (u64)(m - row_lo) * per_row;
-    for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (u64)gridDim.x * blockDim.x) {
-        const u32 row = row_lo + (u32)(e / per_row), x = 2u * (u32)(e - (u64)(row - row_lo) * per_row);
-        *reinterpret_cast<ulonglong2*>(dst + (size_t)row * Wp + x) =
-            *reinterpret_cast<const ulonglong2*>(final4(src, perm, m, ubuf, ucap, qcol, rank, W, row, x));
+__global__ void __launch_bounds__(256) untile4_kernel(const u64* __restrict__ src, u64* __restrict__ dst,
+                                                      const u32* __restrict__ perm, u32 m, u32 Wp, u32 Wpad4,
+                                                      const u64* __restrict__ ubuf, u32 ucap,
+                                                      const u32* __restrict__ qcol, u32 rank, u32 W,
+                                                      u32 row_lo = 0u) {
+    __shared__ __align__(16) unsigned char buf[kCvRows * kCvPitch];
+    if (m <= row_lo) return;
+    const u32 ntile = Wpad4 >> 2, tblocks = (ntile + kCvTiles - 1) / kCvTiles;
+    const u32 rblocks = (m - row_lo + kCvRows - 1) / kCvRows;
+    const u32 tid = threadIdx.x;
+    for (u32 blk = blockIdx.x; blk < tblocks * rblocks; blk += gridDim.x) {
+        const u32 row0 = row_lo + (blk / tblocks) * kCvRows, tile0 = (blk % tblocks) * kCvTiles;
+#pragma unroll
+        for (u32 i = 0; i < 4; ++i) {
+            const u32 t = (tid >> 6) + 4u * i, rr = (tid & 63u) >> 1, h = tid & 1u;
+            const u32 row = row0 + rr, x = (tile0 + t) * 4u + 2u * h;
+            if (row < m && x < Wpad4)
+                *reinterpret_cast<ulonglong2*>(buf + rr * kCvPitch + t * 32u + h * 16u) =
+                    *reinterpret_cast<const ulonglong2*>(final4(src, perm, m, ubuf, ucap, qcol, rank, W, row, x));
+        }
+        __syncthreads();
+#pragma unroll
+        for (u32 i = 0; i < 4; ++i) {
+            const u32 rr = (tid >> 5) + 8u * i, u = tid & 31u;
+            const u32 row = row0 + rr, x = tile0 * 4u + 2u * u;
+            if (row < m && x < Wpad4)
+                *reinterpret_cast<ulonglong2*>(dst + (size_t)row * Wp + x) =
+                    *reinterpret_cast<const ulonglong2*>(buf + rr * kCvPitch + u * 16u);
+        }
+        __syncthreads();
     }
 }
 
