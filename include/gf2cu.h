@@ -380,6 +380,15 @@ gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, 
 gf2cu_status gf2cu_litmus(int kind, unsigned rounds, int device, unsigned long long* checked,
                           unsigned long long* failures);
 
+/* Diagnostic (host only, no device needed): the row-block plan gf2cu_ple
+ * would use to stream an m x (64 W)-column host matrix in:
+ * rows[k] = the k-th block's end row, steps[k] = the 128-column super-steps
+ * done when block k joins (steps[0] = 0); *blocks = their number, 0 = the
+ * matrix is uploaded whole. rows / steps need capacity 8. The plan obeys
+ * GF2CU_STREAM_IN, GF2CU_STREAM_IN_BLOCKS / _FRAC / _STEPS like the call. */
+gf2cu_status gf2cu_stream_in_plan(size_t m, size_t words_per_row, int pageable, size_t* rows, unsigned* steps,
+                                  size_t* blocks);
+
 #ifdef __cplusplus
 }
 #endif

@@ -161,6 +161,7 @@ SYMBOLS = {
     "gf2cu_peer_finish": (C.c_int, [_mp, _szp, _szp, _szp, C.POINTER(C.c_uint32), C.c_void_p]),
     "gf2cu_litmus": (C.c_int, [C.c_int, C.c_uint, C.c_int, C.POINTER(C.c_ulonglong),
                                C.POINTER(C.c_ulonglong)]),
+    "gf2cu_stream_in_plan": (C.c_int, [_sz, _sz, C.c_int, _szp, C.POINTER(C.c_uint), _szp]),
     "gf2cu_fill_random": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_double, C.c_uint64]),
     "gf2cu_fill_ctr": (C.c_int, [_u64p, _sz, _sz, _sz, C.c_uint64]),
     "gf2cu_fill_random_rows": (C.c_int, [_u64p, _sz, _sz, _sz, _sz, C.c_uint64]),

@@ -3093,6 +3093,20 @@ gf2cu_status gf2cu_fill_ctr(uint64_t* words, size_t m, size_t n, size_t stride, 
     return GF2CU_OK;
 }
 
+gf2cu_status gf2cu_stream_in_plan(size_t m, size_t words_per_row, int pageable, size_t* rows, unsigned* steps,
+                                  size_t* blocks) {
+    if (!rows || !steps || !blocks) return fail(GF2CU_EINVAL, "null argument");
+    *blocks = 0;
+    if (m == 0 || words_per_row == 0) return GF2CU_OK;
+    const StreamInPlan pl = stream_in_plan(m, words_per_row, pageable != 0);
+    *blocks = pl.rows.size();
+    for (size_t k = 0; k < pl.rows.size(); ++k) {
+        rows[k] = pl.rows[k];
+        steps[k] = pl.steps[k];
+    }
+    return GF2CU_OK;
+}
+
 // Message-passing litmus runs of the drivers' hand-offs (litmus.cuh).
 gf2cu_status gf2cu_litmus(int kind, unsigned rounds, int device, unsigned long long* checked,
                           unsigned long long* failures) {
