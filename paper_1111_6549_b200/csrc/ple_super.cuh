@@ -592,6 +592,44 @@ __device__ __forceinline__ void super_la_compute(const Params& p, PanelShared& s
     named_bar(kBodyBar, nthr);
 }
 
+// Exhausted trailing matrix (panel CTA body threads, after a super-step in
+// which neither panel found a pivot): are the rows at positions >= r zero in
+// every word from w+2 on? Then every remaining panel is empty too -- the
+// reference would scan each of their columns and find nothing -- and the
+// factorization can stop here with the outputs it has (rank-deficient inputs:
+// BASELINE config 4 spends its last 128 panels this way). The matrix is final
+// once every worker is through S-1 (S itself changes nothing); the scan leaves
+// at the first tile that holds a set bit, so it is only long when it pays.
+// Returns 1 = all zero, 0 = not, -1 = error / watchdog.
+__device__ __forceinline__ int trailing_is_zero(const Params& p, PanelShared& sh, SyncState* sy, u32 w, u32 r,
+                                                u32 M, u32 t_target, int nthr) {
+    if (threadIdx.x == 0) sh.la_go = spin_geq(&sy->t_count, t_target, &sy->error) ? 0 : -1;
+    named_bar(kBodyBar, nthr);
+    if (sh.la_go < 0) return -1;
+    const u32 ntile = p.Wpad8 >> 2;  // (Wpad4 words per row in this driver)
+    const u32 first = (w + 2u) >> 2;
+    const bool upper_only = ((w + 2u) & 3u) != 0u;  // words w, w+1 share the first tile
+    // (from the last tile down: data right of empty panels usually reaches the last column)
+    for (u32 tile = ntile - 1u; tile + 1u > first; --tile) {
+        u64 any = 0ull;
+        for (u32 pos = r + threadIdx.x; pos < M; pos += (u32)nthr) {
+            const u64* e = tw4(p.mat, p.m, ldcg(p.perm + pos), 4u * tile);
+            const ulonglong2 hi = ldcg(reinterpret_cast<const ulonglong2*>(e + 2));
+            any |= hi.x | hi.y;
+            if (!(upper_only && tile == first)) {
+                const ulonglong2 lo = ldcg(reinterpret_cast<const ulonglong2*>(e));
+                any |= lo.x | lo.y;
+            }
+        }
+        if (any) sh.la_go = 1;
+        named_bar(kBodyBar, nthr);
+        const int found = sh.la_go;
+        named_bar(kBodyBar, nthr);  // (everyone has read it before the next tile may set it)
+        if (found) return 0;
+    }
+    return 1;
+}
+
 // Streamed input (gf2cu.cu, run_ple): the factorization of a host matrix as
 // three launches of ple_super_kernel, so that it starts on the first row
 // block while the rest is still on its way over PCIe.
@@ -665,6 +703,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
         LookAhead la{r_begin, false, p.ap_done, 0u, &sy->error};
         u32 prev_r = r_begin;
         bool la_next = false;  // panel a's window came from the look-ahead
+        u32 zc_skip = 0u, zc_wait = 1u;  // exhausted-matrix check: empty super-steps to skip, back-off
         const bool la_on = (p.pflags & kPanelSuperLA) != 0u;
         // streamed input, phase A: a column without a pivot among the rows on
         // the device ends the attempt (every CTA leaves through the error word)
@@ -701,6 +740,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
             // (an aborted panel returns 0: then check the error word itself)
             if (*(volatile int*)&psh.sig_err || (rba == 0u && *(volatile u32*)&sy->error)) return;
             la.r += rba;
+            u32 rbb_found = 0xffffffffu;
             if (w + 1u < p.W) {
                 if (!done0 && la.r < M) {
                     // panel b: window = word w+1 after panel a (panel a's
@@ -713,6 +753,7 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                     if (gave_up()) return;
                     if (*(volatile int*)&psh.sig_err || (rbb == 0u && *(volatile u32*)&sy->error)) return;
                     la.r += rbb;
+                    rbb_found = rbb;
                     // look-ahead across super-steps, only while the workers
                     // are already through S-1 (the panel chain is the
                     // bottleneck; S-1 has also finished the tile holding
@@ -729,6 +770,32 @@ __global__ void __launch_bounds__(kTrailThreads, 1)
                 } else if (threadIdx.x == 0) {
                     p.rhist[w + 1u] = la.r;
                     p.rbhist[w + 1u] = 0u;
+                }
+            }
+            // Neither panel found a pivot: if nothing is left right of them in
+            // the rows below the rank, stop (checked with a doubling back-off,
+            // so inputs whose empty panels are followed by data pay little).
+            // (only in the launch that runs to the last super-step: the streamed
+            // input's earlier phases are followed by replays of their history)
+            if (rba == 0u && rbb_found == 0u && !done0 && la.r < M && w + 2u < p.W && !p.partial &&
+                rg.s_end == (p.W + 1u) / 2u) {
+                if (zc_skip > 0u) {
+                    --zc_skip;
+                } else {
+                    const int zero = trailing_is_zero(p, psh, sy, w, la.r, M, nworkers * S, nbody);
+                    if (zero < 0) return;
+                    if (zero) {
+                        // the workers stop at a step whose rank equals the row count
+                        if (threadIdx.x == 0) {
+                            p.rhist[w] = M;
+                            p.rhist[w + 1u] = M;
+                        }
+                        stamp2(p, w, 1);
+                        signal_step(psh, nbody, S, true);
+                        return;
+                    }
+                    zc_wait = min(2u * zc_wait, 64u);
+                    zc_skip = zc_wait;
                 }
             }
             stamp2(p, w, 1);

@@ -441,6 +441,10 @@ def _structured(kind, m, n, seed):
         a = O.fill_random(m, n, 0.5, seed)
         a[:, : W // 2] = 0
         return a
+    if kind == "zero_left_rank40":  # empty panels followed by data, then an exhausted trailing matrix
+        a = O.mul(O.fill_random(m, 40, 0.5, seed), 40, O.fill_random(40, n, 0.5, seed + 1), n)
+        a[:, : W // 3] = 0
+        return a
     if kind == "deep_single":  # one column whose only 1 sits in the last row
         a = O.fill_random(m, n, 0.5, seed)
         a[:, 1] &= ~np.uint64(1 << 7)
@@ -451,11 +455,13 @@ def _structured(kind, m, n, seed):
 
 @pytest.mark.parametrize("driver", ["single", "super", "peer2", "peer3s"])
 @pytest.mark.parametrize("kind", ["permutation", "zero_top", "nnz3", "p1024", "rank40", "zero_left",
-                                  "deep_single"])
+                                  "zero_left_rank40", "deep_single"])
 def test_structured_inputs_deep_scans(kind, driver):
     """Window-miss scans that go past their first chunk (several doubling
     rounds), rows that are dead for a whole panel, pivotless panels and the
-    column skip after them, on every persistent driver."""
+    column skip after them, exhausted trailing matrices (the two-panel
+    driver's early stop, with and without data after the first empty panels),
+    on every persistent driver."""
     m, n = 6200, 6144
     cfg = {"single": G.PleConfig(single_panel=True), "super": G.PleConfig(super_step=True),
            "peer2": G.PleConfig(peer_ranks=2), "peer3s": G.PleConfig(peer_ranks=3, super_step=True)}[driver]
